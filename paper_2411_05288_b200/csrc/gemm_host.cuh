@@ -1,0 +1,120 @@
+// Host side of the tcgen05 GEMM: TMA descriptor encoding and launch.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+
+#include "gemm_sm100.cuh"
+
+namespace vp {
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point, so the
+// library needs no -lcuda at link time.
+using PFN_encodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                     const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                     CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+inline PFN_encodeTiled get_encode_fn() {
+  static PFN_encodeTiled fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || p == nullptr)
+      throw std::runtime_error("cuTensorMapEncodeTiled entry point unavailable");
+    return reinterpret_cast<PFN_encodeTiled>(p);
+  }();
+  return fn;
+}
+
+// 2-D bf16 tensor map over a row-major [outer x inner] matrix with leading
+// dimension `ld` (elements), SWIZZLE_128B boxes of [box_outer x box_inner].
+// Out-of-bounds elements of a box read as zero.
+inline CUtensorMap make_tmap_bf16(const void* ptr, uint64_t inner, uint64_t outer, uint64_t ld, uint32_t box_inner,
+                                  uint32_t box_outer) {
+  if ((reinterpret_cast<uintptr_t>(ptr) & 15) != 0) throw std::invalid_argument("tensor map: base not 16-B aligned");
+  if ((ld * 2) % 16 != 0) throw std::invalid_argument("tensor map: row stride not a multiple of 16 B");
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {inner, outer};
+  const cuuint64_t strides[1] = {ld * 2};
+  const cuuint32_t box[2] = {box_inner, box_outer};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = get_encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box,
+                               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
+  return m;
+}
+
+// One GEMM operand: row-major storage `ptr` with leading dimension `ld`.
+//   K-major : storage [rows x K]  (A: rows = M, B: rows = N)
+//   MN-major: storage [K x rows]
+struct Operand {
+  const void* ptr;
+  int64_t ld;
+  bool mn_major;
+};
+
+template <int CG, bool A_MN, bool B_MN, class Epi>
+inline void launch_gemm_t(const Operand& A, const Operand& B, int M, int N, int K, int raster,
+                          const typename Epi::Params& ep, int num_sms, cudaStream_t st) {
+  using C = GemmCfg<CG>;
+  const CUtensorMap ta = A_MN ? make_tmap_bf16(A.ptr, uint64_t(M), uint64_t(K), uint64_t(A.ld), 64, 64)
+                              : make_tmap_bf16(A.ptr, uint64_t(K), uint64_t(M), uint64_t(A.ld), 64, C::BM_CTA);
+  const CUtensorMap tb = B_MN ? make_tmap_bf16(B.ptr, uint64_t(N), uint64_t(K), uint64_t(B.ld), 64, 64)
+                              : make_tmap_bf16(B.ptr, uint64_t(K), uint64_t(N), uint64_t(B.ld), 64, C::B_ROWS);
+  GemmGeom g;
+  g.M = M;
+  g.N = N;
+  g.K = K;
+  g.tiles_m = (M + C::BM - 1) / C::BM;
+  g.tiles_n = (N + C::BN - 1) / C::BN;
+  g.num_kb = (K + C::BK - 1) / C::BK;
+  g.raster = raster;
+  auto kern = gemm_sm100_kernel<CG, A_MN, B_MN, Epi>;
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
+    if (e != cudaSuccess) throw std::runtime_error(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
+    attr_done = true;
+  }
+  const int tiles = g.tiles_m * g.tiles_n;
+  const int clusters = tiles < num_sms / CG ? tiles : num_sms / CG;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned(clusters * CG), 1, 1);
+  cfg.blockDim = dim3(C::THREADS, 1, 1);
+  cfg.dynamicSmemBytes = C::SMEM_BYTES;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CG;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta, tb, g, ep);
+  if (e != cudaSuccess) throw std::runtime_error(std::string("gemm launch: ") + cudaGetErrorString(e));
+}
+
+// Runtime dispatch over (cta_group, operand majors).
+template <class Epi>
+inline void launch_gemm(int cg, const Operand& A, const Operand& B, int M, int N, int K, int raster,
+                        const typename Epi::Params& ep, int num_sms, cudaStream_t st) {
+#define VP_GEMM_CASE(CGV, AM, BM_)                                                     \
+  if (cg == CGV && A.mn_major == AM && B.mn_major == BM_) {                            \
+    launch_gemm_t<CGV, AM, BM_, Epi>(A, B, M, N, K, raster, ep, num_sms, st);           \
+    return;                                                                            \
+  }
+  VP_GEMM_CASE(2, false, false)
+  VP_GEMM_CASE(2, false, true)
+  VP_GEMM_CASE(2, true, true)
+  VP_GEMM_CASE(1, false, false)
+  VP_GEMM_CASE(1, false, true)
+  VP_GEMM_CASE(1, true, true)
+#undef VP_GEMM_CASE
+  throw std::invalid_argument("launch_gemm: unsupported operand layout combination");
+}
+
+}  // namespace vp

@@ -1,0 +1,357 @@
+// Persistent, warp-specialised tcgen05 GEMM for sm_100a with pluggable
+// epilogues.  D[M x N] = A[M x K] * B[N x K]^T, bf16 operands, fp32
+// accumulation in TMEM.
+//
+//   * operands arrive by TMA (SWIZZLE_128B) into a STAGES-deep smem ring;
+//     each operand is K-major (row-major [rows x K]) or MN-major
+//     (row-major [K x rows]) — the three vocab GEMMs need all of
+//       K1 logits  Y  = X . W_k^T      A: X [T x h]        K-major
+//                                      B: W_k [V_k x h]    K-major
+//       K3 dX      A  = P' . W_k       A: P' [T x V_k]     K-major
+//                                      B: W_k [V_k x h]    MN-major
+//       K4 dW      dW = P'^T . X~      A: P' [T x V_k]     MN-major
+//                                      B: X~ [T x h]       MN-major
+//   * CG = 2 runs one 256 x 256 tile per CTA pair (cta_group::2): each CTA
+//     loads 128 rows of A and 128 rows of B, the leader CTA's single thread
+//     issues tcgen05.mma for the pair, and each CTA's TMEM holds its 128
+//     accumulator rows.  CG = 1 runs 128 x 256 tiles per CTA.
+//   * TMEM holds two 256-column accumulators so the epilogue of tile i
+//     overlaps the main loop of tile i+1.
+//   * warp roles (256 threads): w0 TMA producer, w1 MMA issuer (leader CTA),
+//     w2 TMEM allocator, w3 idle, w4..w7 epilogue (TMEM lanes 0..127, one
+//     accumulator row per thread).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "sm100_ptx.cuh"
+
+namespace vp {
+
+struct GemmGeom {
+  int M, N, K;
+  int tiles_m, tiles_n, num_kb;
+  // Tile rasterisation.  raster >= 0: M-fastest inside groups of `raster`
+  // m-tiles (0 = all); raster < 0: N-fastest inside groups of -raster
+  // n-tiles.  Picks which operand band stays L2-resident while the
+  // concurrently running tiles sweep the other.
+  int raster;
+};
+
+template <int CG>
+struct GemmCfg {
+  static constexpr int BM_CTA = 128;          // accumulator rows per CTA
+  static constexpr int BM = 128 * CG;         // MMA M
+  static constexpr int BN = 256;              // MMA N
+  static constexpr int BK = 64;               // 128 B of bf16 = one swizzle row
+  static constexpr int UK = 16;               // K per tcgen05.mma (kind::f16)
+  static constexpr int B_ROWS = BN / CG;      // B rows loaded per CTA
+  static constexpr int STAGES = CG == 2 ? 6 : 4;
+  static constexpr int A_BYTES = BM_CTA * BK * 2;
+  static constexpr int B_BYTES = B_ROWS * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int BAR_BYTES = 8 * (2 * STAGES + 4) + 16;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + BAR_BYTES + 1024;
+  static constexpr int THREADS = 256;
+  static constexpr int TMEM_COLS = 512;
+};
+
+__device__ __forceinline__ void tile_coords(const GemmGeom& g, int t, int& mb, int& nb) {
+  if (g.raster >= 0) {
+    const int G = g.raster > 0 ? g.raster : g.tiles_m;
+    const int per = G * g.tiles_n;
+    const int grp = t / per, r = t - grp * per;
+    const int first = grp * G;
+    const int gs = min(G, g.tiles_m - first);
+    mb = first + r % gs;
+    nb = r / gs;
+  } else {
+    const int G = -g.raster;
+    const int per = G * g.tiles_m;
+    const int grp = t / per, r = t - grp * per;
+    const int first = grp * G;
+    const int gs = min(G, g.tiles_n - first);
+    nb = first + r % gs;
+    mb = r / gs;
+  }
+}
+
+template <int CG, bool A_MN, bool B_MN, class Epi>
+__global__ void __launch_bounds__(256, 1)
+    gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                      const GemmGeom g, const typename Epi::Params ep) {
+  using C = GemmCfg<CG>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sbase = ptx::smem_u32(smem);
+  const uint32_t sA = sbase;
+  const uint32_t sB = sbase + C::STAGES * C::A_BYTES;
+  const uint32_t bar_full = sbase + C::STAGES * C::STAGE_BYTES;
+  const uint32_t bar_empty = bar_full + 8 * C::STAGES;
+  const uint32_t bar_tfull = bar_empty + 8 * C::STAGES;
+  const uint32_t bar_tempty = bar_tfull + 16;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::STAGES * C::STAGE_BYTES + 8 * (2 * C::STAGES + 4));
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = CG == 2 ? ptx::cluster_ctarank() : 0u;
+  const int cluster = blockIdx.x / CG, nclusters = gridDim.x / CG;
+  const int num_tiles = g.tiles_m * g.tiles_n;
+
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&tmA);
+    ptx::prefetch_tmap(&tmB);
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      ptx::mbar_init(bar_full + 8 * s, 1);    // leader's expect_tx arrival (covers the pair)
+      ptx::mbar_init(bar_empty + 8 * s, 1);   // one tcgen05.commit
+    }
+    for (int a = 0; a < 2; ++a) {
+      ptx::mbar_init(bar_tfull + 8 * a, 1);        // one tcgen05.commit
+      ptx::mbar_init(bar_tempty + 8 * a, 4 * CG);  // one arrival per epilogue warp of the pair
+    }
+    ptx::fence_barrier_init();
+  }
+  if (warp == 2) ptx::tmem_alloc<CG>(ptx::smem_u32(tmem_slot), C::TMEM_COLS);
+  ptx::tc_fence_before();
+  if constexpr (CG == 2) ptx::cluster_sync(); else __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *reinterpret_cast<volatile uint32_t*>(tmem_slot);
+
+  if (warp == 0 && lane == 0) {
+    // ===== TMA producer =====
+    const uint64_t polA = Epi::kAStreams ? ptx::policy_evict_first() : ptx::policy_evict_last();
+    const uint64_t polB = Epi::kAStreams ? ptx::policy_evict_last() : ptx::policy_evict_first();
+    uint32_t it = 0;
+    for (int t = cluster; t < num_tiles; t += nclusters) {
+      int mb, nb;
+      tile_coords(g, t, mb, nb);
+      const int m0 = mb * C::BM + int(rank) * C::BM_CTA;
+      const int n0 = nb * C::BN + int(rank) * C::B_ROWS;
+      for (int kb = 0; kb < g.num_kb; ++kb, ++it) {
+        const uint32_t s = it % C::STAGES, ph = (it / C::STAGES) & 1u;
+        ptx::mbar_wait(bar_empty + 8 * s, ph ^ 1u);
+        const uint32_t fb = CG == 1 ? bar_full + 8 * s : ptx::mapa(bar_full + 8 * s, 0);
+        // The leader's barrier expects the bytes of BOTH CTAs of the pair; the
+        // peer only issues its TMA (a remote arrive would cost a GPU-scope
+        // membar per stage).
+        if (rank == 0) ptx::mbar_arrive_expect_tx(bar_full + 8 * s, C::STAGE_BYTES * CG);
+        const uint32_t a_dst = sA + s * C::A_BYTES, b_dst = sB + s * C::B_BYTES;
+        const int k0 = kb * C::BK;
+        auto load = [&](const CUtensorMap* m, uint32_t dst, int c0, int c1, uint64_t pol) {
+          if constexpr (CG == 1) ptx::tma_load_2d(m, fb, dst, c0, c1, pol);
+          else ptx::tma_load_2d_cg2(m, fb, dst, c0, c1, pol);
+        };
+        if constexpr (!A_MN) {
+          load(&tmA, a_dst, k0, m0, polA);
+        } else {
+#pragma unroll
+          for (int j = 0; j < C::BM_CTA / 64; ++j) load(&tmA, a_dst + j * 8192, m0 + 64 * j, k0, polA);
+        }
+        if constexpr (!B_MN) {
+          load(&tmB, b_dst, k0, n0, polB);
+        } else {
+#pragma unroll
+          for (int j = 0; j < C::B_ROWS / 64; ++j) load(&tmB, b_dst + j * 8192, n0 + 64 * j, k0, polB);
+        }
+      }
+    }
+  } else if (warp == 1 && lane == 0 && rank == 0) {
+    // ===== MMA issuer (leader CTA, one thread) =====
+    constexpr uint32_t idesc = ptx::idesc_bf16_f32(C::BM, C::BN, A_MN, B_MN);
+    uint32_t it = 0, tc = 0;
+    for (int t = cluster; t < num_tiles; t += nclusters, ++tc) {
+      const uint32_t acc = tc & 1u, aph = (tc >> 1) & 1u;
+      if constexpr (CG == 2) ptx::mbar_wait_cluster(bar_tempty + 8 * acc, aph ^ 1u);
+      else ptx::mbar_wait(bar_tempty + 8 * acc, aph ^ 1u);
+      ptx::tc_fence_after();
+      const uint32_t d = tmem_base + acc * C::BN;
+      for (int kb = 0; kb < g.num_kb; ++kb, ++it) {
+        const uint32_t s = it % C::STAGES, ph = (it / C::STAGES) & 1u;
+        ptx::mbar_wait(bar_full + 8 * s, ph);
+        ptx::tc_fence_after();
+        const uint32_t a_base = sA + s * C::A_BYTES, b_base = sB + s * C::B_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < C::BK / C::UK; ++kk) {
+          // K-major: advance 32 B inside the 128 B swizzle row; SBO = 8 rows.
+          // MN-major: advance 16 K-rows (2 KB); LBO = 64-wide MN atom (8 KB box).
+          const uint64_t ad = A_MN ? ptx::sdesc_sw128(a_base + kk * 2048, 8192, 1024)
+                                   : ptx::sdesc_sw128(a_base + kk * 32, 16, 1024);
+          const uint64_t bd = B_MN ? ptx::sdesc_sw128(b_base + kk * 2048, 8192, 1024)
+                                   : ptx::sdesc_sw128(b_base + kk * 32, 16, 1024);
+          ptx::mma_bf16<CG>(d, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+        }
+        ptx::mma_commit<CG>(bar_empty + 8 * s);
+      }
+      ptx::mma_commit<CG>(bar_tfull + 8 * acc);
+    }
+  } else if (warp >= 4) {
+    // ===== epilogue =====
+    const int ew = warp - 4;
+    uint32_t tc = 0;
+    for (int t = cluster; t < num_tiles; t += nclusters, ++tc) {
+      int mb, nb;
+      tile_coords(g, t, mb, nb);
+      const uint32_t acc = tc & 1u, aph = (tc >> 1) & 1u;
+      ptx::mbar_wait(bar_tfull + 8 * acc, aph);
+      ptx::tc_fence_after();
+      const uint32_t taddr = tmem_base + acc * C::BN + (uint32_t(ew * 32) << 16);
+      const int row = mb * C::BM + int(rank) * C::BM_CTA + ew * 32 + lane;
+      Epi::apply(ep, g, taddr, row, nb * C::BN, nb);
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if constexpr (CG == 1) ptx::mbar_arrive(bar_tempty + 8 * acc);
+        else ptx::mbar_arrive_remote(bar_tempty + 8 * acc, 0);
+      }
+    }
+  }
+  __syncwarp();
+  ptx::tc_fence_before();
+  if constexpr (CG == 2) ptx::cluster_sync(); else __syncthreads();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc<CG>(tmem_base, C::TMEM_COLS);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Epilogues.  apply() runs on one epilogue warp: thread `lane` owns
+// accumulator row `row` (may be >= M: masked), columns [col0, col0 + 256).
+// tcgen05.ld is warp-collective, so loads stay outside row masks.
+// ---------------------------------------------------------------------------
+
+// D -> fp32 out (row-major, ldo), optionally also the per-(row, tile) max of
+// the valid columns (naive F1: logits + local max).
+struct EpiStoreF32 {
+  static constexpr bool kAStreams = true;
+  struct Params {
+    float* out;
+    int64_t ldo;
+    float* tile_max;     // optional [tiles_n x ld_stats]
+    int64_t ld_stats;
+  };
+  __device__ static void apply(const Params& p, const GemmGeom& g, uint32_t taddr, int row, int col0, int nb) {
+    const bool row_ok = row < g.M;
+    const int nvalid = min(GemmCfg<1>::BN, g.N - col0);
+    float* dst = p.out + int64_t(row) * p.ldo + col0;
+    const bool vec = ((p.ldo & 3) == 0) && ((reinterpret_cast<uintptr_t>(p.out) & 15) == 0);
+    float mx = -INFINITY;
+#pragma unroll 1
+    for (int c = 0; c < 8; ++c) {
+      if (c * 32 >= nvalid) break;  // warp-uniform
+      uint32_t r[32];
+      ptx::tmem_ld32(taddr + c * 32, r);
+      ptx::tmem_ld_wait();
+      const int nv = nvalid - c * 32;
+      if (p.tile_max) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (j < nv) mx = fmaxf(mx, __uint_as_float(r[j]));
+      }
+      if (row_ok) {
+        if (nv >= 32 && vec) {
+          float4* d4 = reinterpret_cast<float4*>(dst + c * 32);
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            d4[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (j < nv) dst[c * 32 + j] = __uint_as_float(r[j]);
+        }
+      }
+    }
+    if (p.tile_max && row_ok) p.tile_max[int64_t(nb) * p.ld_stats + row] = mx;
+  }
+};
+
+// K1 fused stats epilogue (forward of the output layer).  For row i and
+// vocab tile j (256 columns of this shard):
+//   m_ij = max_v Y[i,v];  s_ij = sum_v exp(Y[i,v] - m_ij)
+//   P[i,v] = bf16(exp(Y[i,v] - m_ij))          (never the raw logits)
+//   y_tgt[i] = Y[i, g_i - row_begin]  when the label falls in this tile.
+// Full-vocab logits are never written to or re-read from HBM.
+struct EpiLogitStats {
+  static constexpr bool kAStreams = false;  // A = X is reused by every vocab tile
+  struct Params {
+    __nv_bfloat16* P;
+    int64_t ldp;
+    float* tile_m;        // [tiles_n x ld_stats]
+    float* tile_s;        // [tiles_n x ld_stats]
+    int64_t ld_stats;
+    const int64_t* labels;  // [M] global vocab ids (may be null)
+    int64_t row_begin, row_end;
+    float* y_tgt;         // [M]
+  };
+  __device__ static void apply(const Params& p, const GemmGeom& g, uint32_t taddr, int row, int col0, int nb) {
+    constexpr float kLog2e = 1.4426950408889634f;
+    const bool row_ok = row < g.M;
+    const int nvalid = min(GemmCfg<1>::BN, g.N - col0);
+    int lb = -1;
+    if (row_ok && p.labels) {
+      const int64_t gl = p.labels[row];
+      if (gl >= p.row_begin && gl < p.row_end) lb = int(gl - p.row_begin) - col0;  // offset inside tile
+    }
+    float mx = -INFINITY, yt = 0.f;
+    bool has_t = false;
+#pragma unroll 1
+    for (int c = 0; c < 8; ++c) {
+      if (c * 32 >= nvalid) break;
+      uint32_t r[32];
+      ptx::tmem_ld32(taddr + c * 32, r);
+      ptx::tmem_ld_wait();
+      const int nv = nvalid - c * 32;
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (j < nv) mx = fmaxf(mx, __uint_as_float(r[j]));
+      const int off = lb - c * 32;
+      if (off >= 0 && off < 32 && off < nv) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (j == off) yt = __uint_as_float(r[j]);
+        has_t = true;
+      }
+    }
+    const float mxs = mx * kLog2e;
+    float sum = 0.f;
+    __nv_bfloat16* dst = p.P + int64_t(row) * p.ldp + col0;
+    const bool vec = ((p.ldp & 7) == 0) && ((reinterpret_cast<uintptr_t>(p.P) & 15) == 0);
+#pragma unroll 1
+    for (int c = 0; c < 8; ++c) {
+      if (c * 32 >= nvalid) break;
+      uint32_t r[32];
+      ptx::tmem_ld32(taddr + c * 32, r);
+      ptx::tmem_ld_wait();
+      const int nv = nvalid - c * 32;
+      uint32_t pk[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const float e0 = (2 * j < nv) ? ptx::ex2(fmaf(__uint_as_float(r[2 * j]), kLog2e, -mxs)) : 0.f;
+        const float e1 = (2 * j + 1 < nv) ? ptx::ex2(fmaf(__uint_as_float(r[2 * j + 1]), kLog2e, -mxs)) : 0.f;
+        sum += e0 + e1;
+        pk[j] = ptx::pack_bf16(e0, e1);
+      }
+      if (row_ok) {
+        if (nv >= 32 && vec) {
+          uint4* d4 = reinterpret_cast<uint4*>(dst + c * 32);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) d4[j] = make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+        } else {
+          uint16_t* d16 = reinterpret_cast<uint16_t*>(dst + c * 32);
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (j < nv) d16[j] = uint16_t((j & 1) ? (pk[j >> 1] >> 16) : (pk[j >> 1] & 0xFFFFu));
+        }
+      }
+    }
+    if (row_ok) {
+      p.tile_m[int64_t(nb) * p.ld_stats + row] = mx;
+      p.tile_s[int64_t(nb) * p.ld_stats + row] = sum;
+      if (has_t) p.y_tgt[row] = yt;
+    }
+  }
+};
+
+}  // namespace vp
