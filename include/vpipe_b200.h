@@ -1,0 +1,179 @@
+/*
+ * vpipe_b200.h — C ABI of the B200-native vocabulary-parallel layers.
+ *
+ * This is the drop-in boundary for the reference's vocab-math module
+ * (/root/reference/proj/include/vpipe/vocab_math.hpp, "VM.hpp" below, and
+ * /root/reference/proj/src/vocab_math.cpp, "VM.cpp").  Every entry point
+ * names the reference function it replaces.  The C++ mirror of the
+ * reference's own header (same names, structs and argument order) is
+ * include/vpipe/vocab_math.hpp, implemented on top of this ABI.
+ *
+ * Conventions
+ *   - All tensors are DEVICE buffers owned by the caller, row-major, with
+ *     explicit leading dimensions in elements.  Operands X and W are bf16;
+ *     gradients, losses and stats are fp32; ids are int64.
+ *   - h and every leading dimension of a bf16 tensor must be multiples of 8
+ *     (16-byte TMA rows); base pointers 16-byte aligned.
+ *   - Calls are asynchronous on the context's stream.  Hot calls do not
+ *     allocate once vp_ctx_reserve / the first call of a shape has sized the
+ *     workspace.
+ *   - Return codes: VP_OK, VP_EINVAL (the reference's std::invalid_argument,
+ *     same message text, retrievable with vp_last_error()), VP_ECUDA,
+ *     VP_ENCCL.  Errors found on the device (negative token ids, VM.cpp:232,
+ *     :247) are reported by the next vp_ctx_sync() as VP_EINVAL.
+ *   - Sharding: shard k owns vocab rows [row_begin, row_end) (VM.cpp:65-80).
+ *     A context either drives several shards on ONE device (functions take
+ *     arrays of n shard states; the reference's in-process "collectives"
+ *     become device kernels, merged in k order), or — after
+ *     vp_ctx_comm_init — is one rank of an NCCL group with one shard per
+ *     rank (n must be 1; the exchanges are NCCL collectives over NVLink).
+ */
+#ifndef VPIPE_B200_H_
+#define VPIPE_B200_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VP_OK 0
+#define VP_EINVAL 1
+#define VP_ECUDA 2
+#define VP_ENCCL 3
+#define VP_EINTERNAL 4
+
+#define VP_ABI_VERSION 1
+
+typedef struct vp_ctx_s* vp_ctx_t;
+typedef struct vp_state_s* vp_state_t;
+
+/* EmbeddingShard (VM.hpp:21-31): W_k = rows [row_begin, row_end) of W. */
+typedef struct {
+  const void* W;      /* bf16 [rows x h] */
+  int64_t ldw;        /* elements */
+  int64_t row_begin;
+  int64_t row_end;
+  int32_t index;      /* shard index k */
+} vp_shard_t;
+
+/* TokenBatch (VM.hpp:15-18): X [n_tok x h] plus labels [n_tok]. */
+typedef struct {
+  const void* X;            /* bf16 [n_tok x h] */
+  int64_t ldx;
+  const int64_t* labels;    /* [n_tok], global vocab ids */
+  int64_t n_tok;
+  int64_t h;
+} vp_batch_t;
+
+/* GlobalStats (VM.hpp:45-48): per-token global max and exp-sum, fp32 [n_tok]. */
+typedef struct {
+  float* m;
+  float* sum;
+} vp_stats_t;
+
+/* ---- library / context ------------------------------------------------- */
+int vp_abi_version(void);
+const char* vp_last_error(void);
+
+int vp_ctx_create(int device, vp_ctx_t* out);
+int vp_ctx_destroy(vp_ctx_t ctx);
+/* Use an existing cudaStream_t (NULL = the context's own stream). */
+int vp_ctx_set_stream(vp_ctx_t ctx, void* stream);
+void* vp_ctx_get_stream(vp_ctx_t ctx);
+/* Wait for the stream; report deferred device-side argument errors. */
+int vp_ctx_sync(vp_ctx_t ctx);
+/* Pre-size the workspace for up to n_tok tokens, hidden h, p exchange parts. */
+int vp_ctx_reserve(vp_ctx_t ctx, int64_t n_tok, int64_t h, int p);
+/* Options: "cta_group" (1 or 2, default 2), "gemm_sms" (SMs used by GEMMs). */
+int vp_ctx_set_option(vp_ctx_t ctx, const char* key, int64_t value);
+/* Number of kernels this context has launched (evidence counter). */
+int64_t vp_ctx_launch_count(vp_ctx_t ctx);
+
+/* NCCL group: rank 0 creates the id, every rank calls comm_init with it. */
+int vp_comm_unique_id(void* id128);
+int vp_ctx_comm_init(vp_ctx_t ctx, int nranks, int rank, const void* id128);
+int vp_ctx_comm_info(vp_ctx_t ctx, int* nranks, int* rank);
+
+/* ---- shard state (ShardState, VM.hpp:34-43) ----------------------------- */
+/* Device buffers for one shard: P = exp(Y - m_tile) in bf16 [n_tok x rows]
+ * (never the fp32 logits), per-256-column tile stats, m'/sum', the label
+ * logit y[i, g_i] of owned rows, A [n_tok x h] fp32 (alg2). */
+int vp_state_create(vp_ctx_t ctx, int64_t n_tok, int64_t h, int64_t rows, vp_state_t* out);
+int vp_state_destroy(vp_state_t st);
+/* m_local / sum_local (VM.hpp:36-37), device fp32 [n_tok]. */
+int vp_state_local_stats(vp_state_t st, const float** m_local, const float** sum_local);
+/* A = softmax'(Y) W_k (VM.hpp:40), device fp32 [n_tok x h], alg2 only. */
+int vp_state_grad_terms(vp_state_t st, const float** A, int64_t* lda);
+
+/* Copies into caller-owned device buffers (async on the context stream). */
+int vp_state_copy_local_stats(vp_ctx_t ctx, vp_state_t st, float* m_out, float* sum_out);
+int vp_state_copy_grad_terms(vp_ctx_t ctx, vp_state_t st, float* A_out, int64_t ldo);
+
+/* ---- output layer ------------------------------------------------------- */
+/* alg1_pass_S (VM.cpp:151-162): logits GEMM with the fused stats epilogue.
+ * batch->labels (may be NULL here, as in the reference's signature) are
+ * used to capture y[i, g_i] for the loss. */
+int vp_alg1_pass_S(vp_ctx_t ctx, const vp_batch_t* batch, const vp_shard_t* shard, vp_state_t st);
+/* alg2_pass_S (VM.cpp:181-191): alg1_pass_S + A = softmax'·W_k
+ * (B = G_k·W_k is a sparse row gather done in C1). */
+int vp_alg2_pass_S(vp_ctx_t ctx, const vp_batch_t* batch, const vp_shard_t* shard, vp_state_t st);
+/* merge_max_sum (VM.cpp:82-101), C1 of alg1: one NCCL all-gather of the
+ * [2 x n_tok] stats + a fixed-order merge; sum *= fault_scale (VM.cpp:314). */
+int vp_merge_max_sum(vp_ctx_t ctx, const vp_state_t* states, int n, double fault_scale, vp_stats_t out);
+/* merge_max_sum over raw device parts m/sum laid out [p x ld] (k-th part at
+ * offset k*ld), merged in k order — the host API's LocalStats entry point. */
+int vp_merge_stats_raw(vp_ctx_t ctx, const float* m_parts, const float* sum_parts, int p, int64_t n, int64_t ld,
+                       double fault_scale, vp_stats_t out);
+/* alg1_pass_T (VM.cpp:164-179): rescale + dX and dW GEMMs of this shard. */
+int vp_alg1_pass_T(vp_ctx_t ctx, vp_state_t st, vp_stats_t stats, const vp_batch_t* batch,
+                   const vp_shard_t* shard, float* grad_x_partial, int64_t ldgx, float* grad_w, int64_t ldgw);
+/* C2 of alg1 (VM.cpp:322): grad_x = sum_k partial_k (NCCL all-reduce, or k-ordered sum). */
+int vp_reduce_grad_x(vp_ctx_t ctx, float* const* partials, int n, int64_t n_tok, int64_t h, int64_t ld,
+                     float* grad_x, int64_t ldgx);
+/* alg2_barrier_C1 (VM.cpp:193-211; fault path :337-350): stats merge and
+ * grad_x = sum_k (A_k (.) scale_k - B_k); the only barrier of alg2. */
+int vp_alg2_barrier_C1(vp_ctx_t ctx, const vp_state_t* states, const vp_shard_t* shards, int n,
+                       const vp_batch_t* batch, double fault_scale, vp_stats_t out, float* grad_x, int64_t ldgx);
+/* alg2_pass_T (VM.cpp:213-225): dW_k = (softmax'·scale - G_k)^T X. */
+int vp_alg2_pass_T(vp_ctx_t ctx, vp_state_t st, vp_stats_t stats, const vp_batch_t* batch,
+                   const vp_shard_t* shard, float* grad_w, int64_t ldgw);
+/* loss_i = m_i + log(sum_i) - Y[i, g_i] at the owning shard (VM.cpp:287-292). */
+int vp_output_loss(vp_ctx_t ctx, const vp_state_t* states, const vp_shard_t* shards, int n, vp_stats_t stats,
+                   const vp_batch_t* batch, float* loss);
+/* softmax columns of one shard (assemble_forward, VM.cpp:281-286), fp32
+ * [n_tok x rows] — parity/debug materialisation only. */
+int vp_shard_softmax(vp_ctx_t ctx, vp_state_t st, vp_stats_t stats, float* out, int64_t ldo);
+/* naive_partitioned_output (VM.cpp:103-149): 3 barriers, stores and
+ * re-reads fp32 logits. grad_w[k] is shard k's [rows_k x h] block. */
+int vp_naive_partitioned_output(vp_ctx_t ctx, const vp_batch_t* batch, const vp_shard_t* shards,
+                                const vp_state_t* states, int n, vp_stats_t out, float* loss, float* grad_x,
+                                int64_t ldgx, float* const* grad_w, int64_t ldgw);
+/* Drivers run_alg1 / run_alg2 (VM.cpp:303-361) minus the [n_tok x V]
+ * softmax assembly (use vp_shard_softmax for that). */
+int vp_run_alg1(vp_ctx_t ctx, const vp_batch_t* batch, const vp_shard_t* shards, const vp_state_t* states, int n,
+                double fault_scale, vp_stats_t out, float* loss, float* grad_x, int64_t ldgx, float* const* grad_w,
+                int64_t ldgw);
+int vp_run_alg2(vp_ctx_t ctx, const vp_batch_t* batch, const vp_shard_t* shards, const vp_state_t* states, int n,
+                double fault_scale, vp_stats_t out, float* loss, float* grad_x, int64_t ldgx, float* const* grad_w,
+                int64_t ldgw);
+
+/* ---- input layer -------------------------------------------------------- */
+/* input_forward (VM.cpp:227-236): out[i] = W_k[tok_i - row_begin] if owned,
+ * else 0 (accumulate=0), or out[i] += owned row (accumulate=1).  bf16. */
+int vp_input_forward(vp_ctx_t ctx, const int64_t* tokens, int64_t n_tok, int64_t h, const vp_shard_t* shard,
+                     void* out, int64_t ldo, int accumulate);
+/* input_backward (VM.cpp:238-251): dE_k[t - row_begin] += grad_out[i] for
+ * owned tokens in ascending i (deterministic sort + segmented sum); dE_k
+ * zeroed first unless accumulate.  grad_out bf16 (grad_is_f32=0) or fp32. */
+int vp_input_backward(vp_ctx_t ctx, const void* grad_out, int64_t ldg, int grad_is_f32, const int64_t* tokens,
+                      int64_t n_tok, int64_t h, const vp_shard_t* shard, float* grad_w, int64_t ldgw,
+                      int accumulate);
+/* In-place sum all-reduce over the context's NCCL group (the input layer's
+ * post-forward all-reduce, R/PAPER.md:582).  dtype 0 = fp32, 1 = bf16. */
+int vp_allreduce_sum(vp_ctx_t ctx, void* buf, int64_t count, int dtype);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VPIPE_B200_H_ */

@@ -228,8 +228,9 @@ struct EpiStoreF32 {
   struct Params {
     float* out;
     int64_t ldo;
-    float* tile_max;     // optional [tiles_n x ld_stats]
+    float* tile_max;         // optional [tiles_n x ld_stats]
     int64_t ld_stats;
+    const float* row_scale;  // optional per-row factor applied on store
   };
   __device__ static void apply(const Params& p, const GemmGeom& g, uint32_t taddr, int row, int col0, int nb) {
     const bool row_ok = row < g.M;
@@ -237,6 +238,7 @@ struct EpiStoreF32 {
     float* dst = p.out + int64_t(row) * p.ldo + col0;
     const bool vec = ((p.ldo & 3) == 0) && ((reinterpret_cast<uintptr_t>(p.out) & 15) == 0);
     float mx = -INFINITY;
+    const float rs = (p.row_scale && row_ok) ? p.row_scale[row] : 1.f;
 #pragma unroll 1
     for (int c = 0; c < 8; ++c) {
       if (c * 32 >= nvalid) break;  // warp-uniform
@@ -244,6 +246,10 @@ struct EpiStoreF32 {
       ptx::tmem_ld32(taddr + c * 32, r);
       ptx::tmem_ld_wait();
       const int nv = nvalid - c * 32;
+      if (p.row_scale) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) * rs);
+      }
       if (p.tile_max) {
 #pragma unroll
         for (int j = 0; j < 32; ++j)

@@ -1,0 +1,978 @@
+// C-ABI implementation of include/vpipe_b200.h: contexts, shard states,
+// NCCL exchanges and the orchestration of the sm_100a kernels for the
+// naive / Algorithm-1 / Algorithm-2 output layer and the input layer.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/vpipe_b200.h"
+#include "gemm_host.cuh"
+#include "vocab_kernels.cuh"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct NcclError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+#define VP_CUDA(x)                                                                                   \
+  do {                                                                                               \
+    cudaError_t e_ = (x);                                                                            \
+    if (e_ != cudaSuccess) throw CudaError(std::string(#x) + ": " + cudaGetErrorString(e_));        \
+  } while (0)
+#define VP_NCCL(x)                                                                                   \
+  do {                                                                                               \
+    ncclResult_t r_ = (x);                                                                           \
+    if (r_ != ncclSuccess) throw NcclError(std::string(#x) + ": " + ncclGetErrorString(r_));        \
+  } while (0)
+#define VP_KCHECK() VP_CUDA(cudaGetLastError())
+
+inline void require(bool cond, const char* msg) {
+  if (!cond) throw std::invalid_argument(msg);
+}
+
+template <class F>
+int api(F&& f) {
+  try {
+    f();
+    return VP_OK;
+  } catch (const std::invalid_argument& e) {
+    g_last_error = e.what();
+    return VP_EINVAL;
+  } catch (const NcclError& e) {
+    g_last_error = e.what();
+    return VP_ENCCL;
+  } catch (const CudaError& e) {
+    g_last_error = e.what();
+    return VP_ECUDA;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return VP_EINTERNAL;
+  }
+}
+
+// Grow-only device buffer.
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  void* get(size_t need) {
+    if (need > bytes) {
+      if (p) VP_CUDA(cudaFree(p));
+      p = nullptr;
+      VP_CUDA(cudaMalloc(&p, need));
+      bytes = need;
+    }
+    return p;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+};
+
+constexpr int kErrInputFwd = 1, kErrInputBwd = 2;
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+enum PForm { kRaw = 0, kLocal = 1, kGlobal = 2 };
+
+}  // namespace
+
+struct vp_ctx_s {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cudaStream_t own_stream = nullptr;
+  int num_sms = 148;
+  int gemm_sms = 148;
+  int cg = 2;
+  ncclComm_t comm = nullptr;
+  int nranks = 1, rank = 0;
+  int* d_err = nullptr;
+  int64_t launches = 0;
+  // workspace
+  DevBuf inv, scale, xs, keys, gathered, packed, tmp_m, tmp_s;
+
+  void activate() const { VP_CUDA(cudaSetDevice(device)); }
+  bool distributed() const { return comm != nullptr && nranks > 1; }
+  template <class T>
+  T* buf(DevBuf& b, size_t count) {
+    return static_cast<T*>(b.get(count * sizeof(T)));
+  }
+  int grid_for(int64_t work, int per_block) const {
+    const int64_t blocks = ceil_div(work, per_block);
+    const int64_t cap = int64_t(num_sms) * 8;
+    return int(std::max<int64_t>(1, std::min(blocks, cap)));
+  }
+};
+
+struct vp_state_s {
+  vp_ctx_s* ctx = nullptr;
+  int64_t n_tok = 0, h = 0, rows = 0, ldp = 0, ntiles = 0;
+  __nv_bfloat16* P = nullptr;
+  float *tile_m = nullptr, *tile_s = nullptr, *m_loc = nullptr, *s_loc = nullptr, *ytgt = nullptr;
+  float* A = nullptr;  // [n_tok x h] fp32: alg2 A, or per-shard dX partial (alg1/naive local mode)
+  float* Y = nullptr;  // naive only: fp32 logits [n_tok x rows]
+  int form = kRaw;
+  bool has_grad_terms = false;
+  bool has_S = false;
+};
+
+namespace {
+
+void check_batch(const vp_batch_t* b, bool need_labels = true) {
+  require(b != nullptr && b->X != nullptr, "TokenBatch: null batch");
+  require(b->n_tok >= 1, "TokenBatch: empty X");
+  require(!need_labels || b->labels != nullptr, "TokenBatch: labels/X row mismatch");
+  require(b->h >= 1 && b->h % 8 == 0, "TokenBatch: h must be a positive multiple of 8 (pad the hidden dim)");
+  require(b->ldx >= b->h && b->ldx % 8 == 0, "TokenBatch: ldx must be >= h and a multiple of 8");
+  require(aligned16(b->X), "TokenBatch: X must be 16-byte aligned");
+}
+
+void check_shard(const vp_shard_t* s, int64_t h) {
+  require(s != nullptr && s->W != nullptr, "EmbeddingShard: null shard");
+  require(s->row_end > s->row_begin && s->row_begin >= 0, "EmbeddingShard: empty row range");
+  require(s->ldw >= h && s->ldw % 8 == 0, "EmbeddingShard: ldw must be >= h and a multiple of 8");
+  require(aligned16(s->W), "EmbeddingShard: W must be 16-byte aligned");
+}
+
+void check_state(const vp_state_s* st, const vp_batch_t* b, const vp_shard_t* s) {
+  require(st != nullptr, "ShardState: null state");
+  require(st->n_tok == b->n_tok, "ShardState: n_tok mismatch");
+  require(st->h == b->h, "alg1_pass_S: hidden dim mismatch");
+  if (s) require(st->rows == s->row_end - s->row_begin, "ShardState: shard rows mismatch");
+}
+
+// ---- GEMM wrappers ---------------------------------------------------------
+void gemm_logits(vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* s, vp_state_s* st) {
+  vp::EpiLogitStats::Params ep{st->P, st->ldp, st->tile_m, st->tile_s, st->n_tok, b->labels, s->row_begin,
+                               s->row_end, st->ytgt};
+  vp::launch_gemm<vp::EpiLogitStats>(c->cg, {b->X, b->ldx, false}, {s->W, s->ldw, false}, int(b->n_tok),
+                                     int(st->rows), int(b->h), 0, ep, c->gemm_sms, c->stream);
+  ++c->launches;
+}
+
+void gemm_logits_f32(vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* s, vp_state_s* st) {
+  vp::EpiStoreF32::Params ep{st->Y, st->rows, st->tile_m, st->n_tok, nullptr};
+  vp::launch_gemm<vp::EpiStoreF32>(c->cg, {b->X, b->ldx, false}, {s->W, s->ldw, false}, int(b->n_tok),
+                                   int(st->rows), int(b->h), 0, ep, c->gemm_sms, c->stream);
+  ++c->launches;
+}
+
+// out[T x h] = diag(row_scale) . P[T x rows] . W_k[rows x h]
+void gemm_dx(vp_ctx_s* c, vp_state_s* st, const vp_shard_t* s, float* out, int64_t ldo,
+             const float* row_scale = nullptr) {
+  vp::EpiStoreF32::Params ep{out, ldo, nullptr, 0, row_scale};
+  vp::launch_gemm<vp::EpiStoreF32>(c->cg, {st->P, st->ldp, false}, {s->W, s->ldw, true}, int(st->n_tok),
+                                   int(st->h), int(st->rows), 8, ep, c->gemm_sms, c->stream);
+  ++c->launches;
+}
+
+// out[rows x h] = P^T . Xop   (Xop [T x h] bf16)
+void gemm_dw(vp_ctx_s* c, vp_state_s* st, const void* Xop, int64_t ldx, float* out, int64_t ldo) {
+  vp::EpiStoreF32::Params ep{out, ldo, nullptr, 0, nullptr};
+  const int tiles_n = int(ceil_div(st->h, 256));
+  vp::launch_gemm<vp::EpiStoreF32>(c->cg, {st->P, st->ldp, true}, {Xop, ldx, true}, int(st->rows), int(st->h),
+                                   int(st->n_tok), -tiles_n, ep, c->gemm_sms, c->stream);
+  ++c->launches;
+}
+
+// ---- small kernel wrappers ---------------------------------------------------
+void stats_reduce(vp_ctx_s* c, vp_state_s* st, bool with_sum) {
+  vp::k_stats_reduce<<<unsigned(ceil_div(st->n_tok, 32)), 256, 0, c->stream>>>(
+      st->tile_m, with_sum ? st->tile_s : nullptr, int(st->ntiles), st->n_tok, int(st->n_tok), st->m_loc,
+      with_sum ? st->s_loc : nullptr);
+  VP_KCHECK();
+  ++c->launches;
+}
+
+void rescale_P(vp_ctx_s* c, vp_state_s* st, const float* tile_m, const float* mref, const float* inv) {
+  const int64_t work = st->n_tok * ceil_div(st->rows, 8);
+  vp::k_rescale_P<<<c->grid_for(work, 256), 256, 0, c->stream>>>(st->P, st->ldp, int(st->n_tok), int(st->rows),
+                                                                 tile_m, st->n_tok, mref, inv);
+  VP_KCHECK();
+  ++c->launches;
+}
+
+float* inv_of(vp_ctx_s* c, const float* s, int64_t n) {
+  float* inv = c->buf<float>(c->inv, size_t(n));
+  vp::k_inv<<<unsigned(ceil_div(n, 256)), 256, 0, c->stream>>>(s, int(n), inv);
+  VP_KCHECK();
+  ++c->launches;
+  return inv;
+}
+
+float* global_scale(vp_ctx_s* c, const vp_state_s* st, vp_stats_t g) {
+  float* sc = c->buf<float>(c->scale, size_t(st->n_tok));
+  vp::k_global_scale<<<unsigned(ceil_div(st->n_tok, 256)), 256, 0, c->stream>>>(st->m_loc, st->s_loc, g.m, g.sum,
+                                                                                int(st->n_tok), sc);
+  VP_KCHECK();
+  ++c->launches;
+  return sc;
+}
+
+// Sorted keys of the owned tokens of one shard (deterministic segments).
+unsigned long long* sorted_keys(vp_ctx_s* c, const int64_t* tok, int64_t n, int64_t rb, int64_t re, int* n_pad_out,
+                                int err_bit = 0) {
+  int n_pad = 1;
+  while (n_pad < n) n_pad <<= 1;
+  n_pad = std::max(n_pad, 2);
+  auto* keys = c->buf<unsigned long long>(c->keys, size_t(n_pad));
+  vp::k_make_keys<<<unsigned(ceil_div(n_pad, 256)), 256, 0, c->stream>>>(tok, int(n), n_pad, rb, re, keys,
+                                                                         c->d_err, err_bit);
+  VP_KCHECK();
+  const unsigned chunks = unsigned(ceil_div(n_pad, 2048));
+  vp::k_bitonic_shared<<<chunks, 1024, 0, c->stream>>>(keys, n_pad, 0, 1);
+  VP_KCHECK();
+  c->launches += 2;
+  for (int k = 4096; k <= n_pad; k <<= 1) {
+    for (int j = k >> 1; j >= 2048; j >>= 1) {
+      vp::k_bitonic_global<<<unsigned(ceil_div(n_pad, 256)), 256, 0, c->stream>>>(keys, n_pad, j, k);
+      VP_KCHECK();
+      ++c->launches;
+    }
+    vp::k_bitonic_shared<<<chunks, 1024, 0, c->stream>>>(keys, n_pad, k, 0);
+    VP_KCHECK();
+    ++c->launches;
+  }
+  *n_pad_out = n_pad;
+  return keys;
+}
+
+// dst[row] (+)= sign * src[i] over owned tokens, ascending i per row.
+template <typename Src>
+void segment_scatter(vp_ctx_s* c, const int64_t* tok, int64_t n, int64_t rb, int64_t re, const Src* src, int64_t lds,
+                     int64_t h, float sign, float* dst, int64_t ldd, int accumulate) {
+  int n_pad = 0;
+  unsigned long long* keys = sorted_keys(c, tok, n, rb, re, &n_pad);
+  vp::k_segment_scatter<Src><<<unsigned(n_pad), 256, 0, c->stream>>>(keys, n_pad, src, lds, int(h), sign, dst, ldd,
+                                                                      accumulate);
+  VP_KCHECK();
+  ++c->launches;
+}
+
+// alg1_pass_S (VM.cpp:151-162): Y = X W_k^T with the fused stats epilogue
+// (P = e^{Y - m_tile} in bf16, tile m/sum, y[i, g_i]); per-row merge of the
+// tile stats into m', sum'; then P <- softmax' = P e^{m_tile - m'} / sum'
+// (VM.cpp:158-160) in place.  P stays softmax' from here on: the T passes
+// apply the Eq. 5 factor per row (dX epilogue / scaled X), so they never
+// rewrite P and remain pure.
+void pass_S_common(vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* s, vp_state_s* st) {
+  check_batch(b, false);
+  check_shard(s, b->h);
+  check_state(st, b, s);
+  gemm_logits(c, b, s, st);
+  stats_reduce(c, st, true);
+  rescale_P(c, st, st->tile_m, st->m_loc, inv_of(c, st->s_loc, st->n_tok));
+  st->form = kLocal;
+  st->has_grad_terms = false;
+  st->has_S = true;
+}
+
+void alg2_S(vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* s, vp_state_s* st) {
+  pass_S_common(c, b, s, st);
+  gemm_dx(c, st, s, st->A, st->h);  // A = softmax' W_k (VM.cpp:183)
+  st->has_grad_terms = true;
+}
+
+// Xs = c (.) X in bf16, c = global_scale (the dW operand of both T passes)
+const __nv_bfloat16* scaled_x(vp_ctx_s* c, const vp_batch_t* b, const float* sc) {
+  auto* xs = c->buf<__nv_bfloat16>(c->xs, size_t(b->n_tok * b->h));
+  vp::k_scale_rows_bf16<<<c->grid_for(b->n_tok * b->h / 8, 256), 256, 0, c->stream>>>(
+      static_cast<const __nv_bfloat16*>(b->X), b->ldx, sc, int(b->n_tok), int(b->h), xs, b->h);
+  VP_KCHECK();
+  ++c->launches;
+  return xs;
+}
+
+void merge_stats(vp_ctx_s* c, const vp_state_t* states, int n, double fault_scale, vp_stats_t out) {
+  require(n >= 1 && states != nullptr, "merge_max_sum: empty input");
+  require(out.m != nullptr && out.sum != nullptr, "merge_max_sum: null output");
+  const int64_t T = states[0]->n_tok;
+  for (int k = 0; k < n; ++k) {
+    require(states[k] != nullptr && states[k]->has_S, "merge_max_sum: state has no pass-S stats");
+    require(states[k]->n_tok == T, "merge_max_sum: length mismatch");
+  }
+  if (c->distributed()) {
+    require(n == 1, "merge_max_sum: one state per rank in an NCCL group");
+    float* packed = c->buf<float>(c->packed, size_t(2 * T));
+    float* gathered = c->buf<float>(c->gathered, size_t(2 * T * c->nranks));
+    vp::k_pack_stats<<<unsigned(ceil_div(T, 256)), 256, 0, c->stream>>>(states[0]->m_loc, states[0]->s_loc, int(T),
+                                                                        packed);
+    VP_KCHECK();
+    VP_NCCL(ncclAllGather(packed, gathered, size_t(2 * T), ncclFloat32, c->comm, c->stream));
+    vp::k_merge_stats<<<unsigned(ceil_div(T, 256)), 256, 0, c->stream>>>(
+        gathered, gathered + T, c->nranks, 2 * T, int(T), float(fault_scale), out.m, out.sum);
+    VP_KCHECK();
+    c->launches += 2;
+  } else {
+    require(n <= vp::kMaxLocalShards, "merge_max_sum: too many local shards");
+    vp::StatsParts parts{};
+    parts.p = n;
+    for (int k = 0; k < n; ++k) {
+      parts.m[k] = states[k]->m_loc;
+      parts.s[k] = states[k]->s_loc;
+    }
+    vp::k_merge_stats_ptrs<<<unsigned(ceil_div(T, 256)), 256, 0, c->stream>>>(parts, int(T), float(fault_scale),
+                                                                             out.m, out.sum);
+    VP_KCHECK();
+    ++c->launches;
+  }
+}
+
+// alg1_pass_T (VM.cpp:164-179):  grad_y = softmax' (.) c - G_k,
+//   dX_k = grad_y W_k = diag(c) (softmax' W_k) - G_k W_k   (row scale in the epilogue, row gather)
+//   dW_k = grad_y^T X = softmax'^T (c (.) X) - G_k^T X     (scaled X operand, ordered scatter)
+void alg1_T(vp_ctx_s* c, vp_state_s* st, vp_stats_t g, const vp_batch_t* b, const vp_shard_t* s, float* gx,
+            int64_t ldgx, float* gw, int64_t ldgw) {
+  check_batch(b);
+  check_shard(s, b->h);
+  check_state(st, b, s);
+  require(st->has_S && st->form == kLocal, "alg1_pass_T: state/stats length mismatch");
+  require(g.m && g.sum, "alg1_pass_T: null stats");
+  const float* sc = global_scale(c, st, g);
+  gemm_dx(c, st, s, gx, ldgx, sc);
+  vp::k_sub_label_rows<<<c->grid_for(st->n_tok * st->h / 2, 256), 256, 0, c->stream>>>(
+      gx, ldgx, static_cast<const __nv_bfloat16*>(s->W), s->ldw, s->row_begin, s->row_end, b->labels,
+      int(st->n_tok), int(st->h));
+  VP_KCHECK();
+  ++c->launches;
+  gemm_dw(c, st, scaled_x(c, b, sc), b->h, gw, ldgw);
+  segment_scatter(c, b->labels, b->n_tok, s->row_begin, s->row_end, static_cast<const __nv_bfloat16*>(b->X), b->ldx,
+                  b->h, -1.f, gw, ldgw, 1);
+}
+
+// alg2_pass_T (VM.cpp:213-225): dW_k = softmax'^T (c (.) X) - G_k^T X
+void alg2_T(vp_ctx_s* c, vp_state_s* st, vp_stats_t g, const vp_batch_t* b, const vp_shard_t* s, float* gw,
+            int64_t ldgw) {
+  check_batch(b);
+  check_shard(s, b->h);
+  check_state(st, b, s);
+  require(st->has_S && st->form == kLocal, "alg2_pass_T: state/stats length mismatch");
+  require(g.m && g.sum, "alg2_pass_T: null stats");
+  const float* sc = global_scale(c, st, g);
+  gemm_dw(c, st, scaled_x(c, b, sc), b->h, gw, ldgw);
+  segment_scatter(c, b->labels, b->n_tok, s->row_begin, s->row_end, static_cast<const __nv_bfloat16*>(b->X), b->ldx,
+                  b->h, -1.f, gw, ldgw, 1);
+}
+
+void alg2_C1(vp_ctx_s* c, const vp_state_t* states, const vp_shard_t* shards, int n, const vp_batch_t* b,
+             double fault_scale, vp_stats_t out, float* gx, int64_t ldgx) {
+  require(n >= 1 && states != nullptr, "alg2_barrier_C1: no states");
+  check_batch(b);
+  for (int k = 0; k < n; ++k) {
+    require(states[k] != nullptr && states[k]->has_grad_terms && states[k]->form == kLocal,
+            "alg2_barrier_C1: A/B terms missing");
+    check_shard(&shards[k], b->h);
+    check_state(states[k], b, &shards[k]);
+  }
+  require(gx != nullptr && ldgx >= b->h && ldgx % 4 == 0, "alg2_barrier_C1: bad grad_x buffer");
+  merge_stats(c, states, n, fault_scale, out);
+  vp::CombineShards S{};
+  S.p = n;
+  S.lda = b->h;
+  for (int k = 0; k < n; ++k) {
+    S.A[k] = states[k]->A;
+    S.W[k] = static_cast<const __nv_bfloat16*>(shards[k].W);
+    S.ldw[k] = shards[k].ldw;
+    S.rb[k] = shards[k].row_begin;
+    S.re[k] = shards[k].row_end;
+    S.ml[k] = states[k]->m_loc;
+    S.sl[k] = states[k]->s_loc;
+  }
+  vp::k_alg2_combine<<<c->grid_for(b->n_tok * b->h / 4, 256), 256, 0, c->stream>>>(
+      S, out.m, out.sum, b->labels, int(b->n_tok), int(b->h), gx, ldgx);
+  VP_KCHECK();
+  ++c->launches;
+  if (c->distributed()) {
+    require(ldgx == b->h, "alg2_barrier_C1: grad_x must be dense (ldgx == h) for the all-reduce");
+    VP_NCCL(ncclAllReduce(gx, gx, size_t(b->n_tok * b->h), ncclFloat32, ncclSum, c->comm, c->stream));
+  }
+}
+
+void loss_of(vp_ctx_s* c, const vp_state_t* states, const vp_shard_t* shards, int n, vp_stats_t g,
+             const vp_batch_t* b, float* loss) {
+  require(n >= 1 && n <= vp::kMaxLocalShards, "loss: bad shard count");
+  require(loss != nullptr, "loss: null output");
+  vp::LossShards S{};
+  S.p = n;
+  for (int k = 0; k < n; ++k) {
+    S.yt[k] = states[k]->ytgt;
+    S.rb[k] = shards[k].row_begin;
+    S.re[k] = shards[k].row_end;
+  }
+  vp::k_loss<<<unsigned(ceil_div(b->n_tok, 256)), 256, 0, c->stream>>>(S, g.m, g.sum, b->labels, int(b->n_tok),
+                                                                       loss);
+  VP_KCHECK();
+  ++c->launches;
+  if (c->distributed())
+    VP_NCCL(ncclAllReduce(loss, loss, size_t(b->n_tok), ncclFloat32, ncclSum, c->comm, c->stream));
+}
+
+void reduce_partials(vp_ctx_s* c, float* const* partials, int n, int64_t T, int64_t h, int64_t ld, float* gx,
+                     int64_t ldgx) {
+  require(n >= 1, "reduce_grad_x: no partials");
+  require(ld == h && ldgx == h, "reduce_grad_x: partials and grad_x must be dense [n_tok x h]");
+  if (c->distributed()) {
+    require(n == 1, "reduce_grad_x: one partial per rank in an NCCL group");
+    VP_NCCL(ncclAllReduce(partials[0], gx, size_t(T * h), ncclFloat32, ncclSum, c->comm, c->stream));
+    return;
+  }
+  require(n <= vp::kMaxLocalShards, "reduce_grad_x: too many partials");
+  vp::PartialPtrs S{};
+  S.p = n;
+  for (int k = 0; k < n; ++k) S.P[k] = partials[k];
+  vp::k_sum_partials<<<c->grid_for(T * h, 256), 256, 0, c->stream>>>(S, T * h, gx);
+  VP_KCHECK();
+  ++c->launches;
+}
+
+void run_alg(int alg, vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* shards, const vp_state_t* states, int n,
+             double fault_scale, vp_stats_t out, float* loss, float* gx, int64_t ldgx, float* const* gw,
+             int64_t ldgw) {
+  require(n >= 1 && n <= vp::kMaxLocalShards, "run: bad shard count");
+  require(!c->distributed() || n == 1, "run: one shard per rank in an NCCL group");
+  if (alg == 2) {
+    for (int k = 0; k < n; ++k) alg2_S(c, b, &shards[k], states[k]);
+    alg2_C1(c, states, shards, n, b, fault_scale, out, gx, ldgx);
+    loss_of(c, states, shards, n, out, b, loss);
+    for (int k = 0; k < n; ++k) alg2_T(c, states[k], out, b, &shards[k], gw[k], ldgw);
+  } else {
+    for (int k = 0; k < n; ++k) pass_S_common(c, b, &shards[k], states[k]);
+    merge_stats(c, states, n, fault_scale, out);
+    loss_of(c, states, shards, n, out, b, loss);
+    std::vector<float*> partials(static_cast<size_t>(n));
+    for (int k = 0; k < n; ++k) {
+      // local mode: each shard's dX partial lives in its state's A buffer;
+      // NCCL mode: the partial is written straight into grad_x and all-reduced.
+      partials[size_t(k)] = c->distributed() ? gx : states[k]->A;
+      alg1_T(c, states[k], out, b, &shards[k], partials[size_t(k)], c->distributed() ? ldgx : b->h, gw[k], ldgw);
+    }
+    if (c->distributed()) {
+      require(ldgx == b->h, "run_alg1: grad_x must be dense for the all-reduce");
+      VP_NCCL(ncclAllReduce(gx, gx, size_t(b->n_tok * b->h), ncclFloat32, ncclSum, c->comm, c->stream));
+    } else {
+      reduce_partials(c, partials.data(), n, b->n_tok, b->h, b->h, gx, ldgx);
+    }
+  }
+}
+
+void naive(vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* shards, const vp_state_t* states, int n,
+           vp_stats_t out, float* loss, float* gx, int64_t ldgx, float* const* gw, int64_t ldgw) {
+  require(n >= 1 && shards != nullptr, "naive: no shards");
+  require(n <= vp::kMaxLocalShards, "naive: too many local shards");
+  require(!c->distributed() || n == 1, "naive: one shard per rank in an NCCL group");
+  check_batch(b);
+  const int64_t T = b->n_tok;
+  for (int k = 0; k < n; ++k) {
+    check_shard(&shards[k], b->h);
+    check_state(states[k], b, &shards[k]);
+    vp_state_s* st = states[k];
+    if (!st->Y) VP_CUDA(cudaMalloc(&st->Y, size_t(T * st->rows) * sizeof(float)));
+  }
+  // F1: local logits + local max, then the max all-reduce (VM.cpp:111-117)
+  for (int k = 0; k < n; ++k) {
+    vp_state_s* st = states[k];
+    gemm_logits_f32(c, b, &shards[k], st);
+    stats_reduce(c, st, false);
+    vp::k_gather_target<<<unsigned(ceil_div(T, 256)), 256, 0, c->stream>>>(
+        st->Y, st->rows, b->labels, shards[k].row_begin, shards[k].row_end, int(T), st->ytgt);
+    VP_KCHECK();
+    ++c->launches;
+  }
+  if (c->distributed()) {
+    VP_NCCL(ncclAllReduce(states[0]->m_loc, out.m, size_t(T), ncclFloat32, ncclMax, c->comm, c->stream));
+  } else {
+    vp::StatsParts parts{};
+    parts.p = n;
+    for (int k = 0; k < n; ++k) parts.m[k] = parts.s[k] = states[k]->m_loc;
+    // max over shards: merge with s = m is not meaningful; use the max-only path
+    float* dummy = c->buf<float>(c->tmp_s, size_t(T));
+    vp::k_merge_stats_ptrs<<<unsigned(ceil_div(T, 256)), 256, 0, c->stream>>>(parts, int(T), 1.f, out.m, dummy);
+    VP_KCHECK();
+    ++c->launches;
+  }
+  // F2: exp-sums against the global max, re-reading the logits, then the sum all-reduce
+  for (int k = 0; k < n; ++k) {
+    vp_state_s* st = states[k];
+    vp::k_naive_exp_sum<<<unsigned(T), 256, 0, c->stream>>>(st->Y, st->rows, int(st->rows), out.m, st->P, st->ldp,
+                                                             st->s_loc);
+    VP_KCHECK();
+    ++c->launches;
+  }
+  if (c->distributed()) {
+    VP_NCCL(ncclAllReduce(states[0]->s_loc, out.sum, size_t(T), ncclFloat32, ncclSum, c->comm, c->stream));
+  } else {
+    vp::PartialPtrs S{};
+    S.p = n;
+    for (int k = 0; k < n; ++k) S.P[k] = states[k]->s_loc;
+    vp::k_sum_partials<<<c->grid_for(T, 256), 256, 0, c->stream>>>(S, T, out.sum);
+    VP_KCHECK();
+    ++c->launches;
+  }
+  // B: softmax, loss at the owner, -1 at the label, dX partials, dW rows
+  const float* inv = inv_of(c, out.sum, T);
+  std::vector<float*> partials(static_cast<size_t>(n));
+  for (int k = 0; k < n; ++k) {
+    vp_state_s* st = states[k];
+    rescale_P(c, st, nullptr, nullptr, inv);
+    st->form = kGlobal;
+    st->has_S = true;
+    partials[size_t(k)] = c->distributed() ? gx : st->A;
+    const int64_t ld = c->distributed() ? ldgx : b->h;
+    gemm_dx(c, st, &shards[k], partials[size_t(k)], ld);
+    vp::k_sub_label_rows<<<c->grid_for(T * b->h / 2, 256), 256, 0, c->stream>>>(
+        partials[size_t(k)], ld, static_cast<const __nv_bfloat16*>(shards[k].W), shards[k].ldw, shards[k].row_begin,
+        shards[k].row_end, b->labels, int(T), int(b->h));
+    VP_KCHECK();
+    ++c->launches;
+    gemm_dw(c, st, b->X, b->ldx, gw[k], ldgw);
+    segment_scatter(c, b->labels, T, shards[k].row_begin, shards[k].row_end,
+                    static_cast<const __nv_bfloat16*>(b->X), b->ldx, b->h, -1.f, gw[k], ldgw, 1);
+  }
+  loss_of(c, states, shards, n, out, b, loss);
+  if (c->distributed()) {
+    VP_NCCL(ncclAllReduce(gx, gx, size_t(T * b->h), ncclFloat32, ncclSum, c->comm, c->stream));
+  } else {
+    reduce_partials(c, partials.data(), n, T, b->h, b->h, gx, ldgx);
+  }
+}
+
+}  // namespace
+
+// =============================================================================
+extern "C" {
+
+int vp_abi_version(void) { return VP_ABI_VERSION; }
+const char* vp_last_error(void) { return g_last_error.c_str(); }
+
+int vp_ctx_create(int device, vp_ctx_t* out) {
+  return api([&] {
+    require(out != nullptr, "vp_ctx_create: null output");
+    int ndev = 0;
+    VP_CUDA(cudaGetDeviceCount(&ndev));
+    require(device >= 0 && device < ndev, "vp_ctx_create: bad device");
+    auto* c = new vp_ctx_s();
+    c->device = device;
+    try {
+      c->activate();
+      cudaDeviceProp prop;
+      VP_CUDA(cudaGetDeviceProperties(&prop, device));
+      if (prop.major != 10) throw std::invalid_argument("vp_ctx_create: this library targets sm_100a (B200)");
+      c->num_sms = prop.multiProcessorCount;
+      c->gemm_sms = c->num_sms;
+      VP_CUDA(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
+      c->stream = c->own_stream;
+      VP_CUDA(cudaMalloc(&c->d_err, sizeof(int)));
+      VP_CUDA(cudaMemset(c->d_err, 0, sizeof(int)));
+    } catch (...) {
+      delete c;
+      throw;
+    }
+    *out = c;
+  });
+}
+
+int vp_ctx_destroy(vp_ctx_t c) {
+  return api([&] {
+    if (!c) return;
+    c->activate();
+    cudaStreamSynchronize(c->stream);
+    if (c->comm) ncclCommDestroy(c->comm);
+    for (DevBuf* b : {&c->inv, &c->scale, &c->xs, &c->keys, &c->gathered, &c->packed, &c->tmp_m, &c->tmp_s})
+      b->release();
+    if (c->d_err) cudaFree(c->d_err);
+    if (c->own_stream) cudaStreamDestroy(c->own_stream);
+    delete c;
+  });
+}
+
+int vp_ctx_set_stream(vp_ctx_t c, void* stream) {
+  return api([&] {
+    require(c != nullptr, "vp_ctx_set_stream: null context");
+    c->stream = stream ? static_cast<cudaStream_t>(stream) : c->own_stream;
+  });
+}
+
+void* vp_ctx_get_stream(vp_ctx_t c) { return c ? static_cast<void*>(c->stream) : nullptr; }
+
+int vp_ctx_sync(vp_ctx_t c) {
+  return api([&] {
+    require(c != nullptr, "vp_ctx_sync: null context");
+    c->activate();
+    VP_CUDA(cudaStreamSynchronize(c->stream));
+    int err = 0;
+    VP_CUDA(cudaMemcpy(&err, c->d_err, sizeof(int), cudaMemcpyDeviceToHost));
+    if (err) {
+      VP_CUDA(cudaMemset(c->d_err, 0, sizeof(int)));
+      if (err & kErrInputFwd) throw std::invalid_argument("input_forward: token out of range");
+      throw std::invalid_argument("input_backward: token out of range");
+    }
+  });
+}
+
+int vp_ctx_reserve(vp_ctx_t c, int64_t n_tok, int64_t h, int p) {
+  return api([&] {
+    require(c != nullptr && n_tok >= 1 && h >= 1 && p >= 1, "vp_ctx_reserve: bad arguments");
+    c->activate();
+    int n_pad = 2;
+    while (n_pad < n_tok) n_pad <<= 1;
+    c->buf<float>(c->inv, size_t(n_tok));
+    c->buf<float>(c->scale, size_t(n_tok));
+    c->buf<float>(c->tmp_m, size_t(n_tok));
+    c->buf<float>(c->tmp_s, size_t(n_tok));
+    c->buf<__nv_bfloat16>(c->xs, size_t(n_tok * h));
+    c->buf<unsigned long long>(c->keys, size_t(n_pad));
+    c->buf<float>(c->packed, size_t(2 * n_tok));
+    c->buf<float>(c->gathered, size_t(2 * n_tok * std::max(p, c->nranks)));
+  });
+}
+
+int vp_ctx_set_option(vp_ctx_t c, const char* key, int64_t value) {
+  return api([&] {
+    require(c != nullptr && key != nullptr, "vp_ctx_set_option: null argument");
+    const std::string k(key);
+    if (k == "cta_group") {
+      require(value == 1 || value == 2, "vp_ctx_set_option: cta_group must be 1 or 2");
+      c->cg = int(value);
+    } else if (k == "gemm_sms") {
+      require(value >= 2 && value <= c->num_sms, "vp_ctx_set_option: gemm_sms out of range");
+      c->gemm_sms = int(value);
+    } else {
+      throw std::invalid_argument("vp_ctx_set_option: unknown option " + k);
+    }
+  });
+}
+
+int64_t vp_ctx_launch_count(vp_ctx_t c) { return c ? c->launches : -1; }
+
+int vp_comm_unique_id(void* id128) {
+  return api([&] {
+    require(id128 != nullptr, "vp_comm_unique_id: null output");
+    ncclUniqueId id;
+    VP_NCCL(ncclGetUniqueId(&id));
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    std::memcpy(id128, &id, sizeof(id));
+  });
+}
+
+int vp_ctx_comm_init(vp_ctx_t c, int nranks, int rank, const void* id128) {
+  return api([&] {
+    require(c != nullptr && id128 != nullptr, "vp_ctx_comm_init: null argument");
+    require(nranks >= 1 && rank >= 0 && rank < nranks, "vp_ctx_comm_init: bad rank");
+    require(c->comm == nullptr, "vp_ctx_comm_init: already initialised");
+    c->activate();
+    ncclUniqueId id;
+    std::memcpy(&id, id128, sizeof(id));
+    VP_NCCL(ncclCommInitRank(&c->comm, nranks, id, rank));
+    c->nranks = nranks;
+    c->rank = rank;
+  });
+}
+
+int vp_ctx_comm_info(vp_ctx_t c, int* nranks, int* rank) {
+  return api([&] {
+    require(c != nullptr, "vp_ctx_comm_info: null context");
+    if (nranks) *nranks = c->nranks;
+    if (rank) *rank = c->rank;
+  });
+}
+
+int vp_state_create(vp_ctx_t c, int64_t n_tok, int64_t h, int64_t rows, vp_state_t* out) {
+  return api([&] {
+    require(c != nullptr && out != nullptr, "vp_state_create: null argument");
+    require(n_tok >= 1 && h >= 1 && rows >= 1, "vp_state_create: empty shape");
+    require(h % 8 == 0, "vp_state_create: h must be a multiple of 8");
+    c->activate();
+    auto* st = new vp_state_s();
+    st->ctx = c;
+    st->n_tok = n_tok;
+    st->h = h;
+    st->rows = rows;
+    st->ldp = round_up(rows, 64);
+    st->ntiles = ceil_div(rows, vp::kTileN);
+    try {
+      VP_CUDA(cudaMalloc(&st->P, size_t(n_tok * st->ldp) * sizeof(__nv_bfloat16)));
+      VP_CUDA(cudaMalloc(&st->tile_m, size_t(st->ntiles * n_tok) * sizeof(float)));
+      VP_CUDA(cudaMalloc(&st->tile_s, size_t(st->ntiles * n_tok) * sizeof(float)));
+      VP_CUDA(cudaMalloc(&st->m_loc, size_t(n_tok) * sizeof(float)));
+      VP_CUDA(cudaMalloc(&st->s_loc, size_t(n_tok) * sizeof(float)));
+      VP_CUDA(cudaMalloc(&st->ytgt, size_t(n_tok) * sizeof(float)));
+      VP_CUDA(cudaMalloc(&st->A, size_t(n_tok * h) * sizeof(float)));
+      VP_CUDA(cudaMemset(st->ytgt, 0, size_t(n_tok) * sizeof(float)));
+    } catch (...) {
+      for (void* p : {static_cast<void*>(st->P), static_cast<void*>(st->tile_m), static_cast<void*>(st->tile_s),
+                      static_cast<void*>(st->m_loc), static_cast<void*>(st->s_loc), static_cast<void*>(st->ytgt),
+                      static_cast<void*>(st->A)})
+        if (p) cudaFree(p);
+      delete st;
+      throw;
+    }
+    *out = st;
+  });
+}
+
+int vp_state_destroy(vp_state_t st) {
+  return api([&] {
+    if (!st) return;
+    st->ctx->activate();
+    cudaStreamSynchronize(st->ctx->stream);
+    for (void* p : {static_cast<void*>(st->P), static_cast<void*>(st->tile_m), static_cast<void*>(st->tile_s),
+                    static_cast<void*>(st->m_loc), static_cast<void*>(st->s_loc), static_cast<void*>(st->ytgt),
+                    static_cast<void*>(st->A), static_cast<void*>(st->Y)})
+      if (p) cudaFree(p);
+    delete st;
+  });
+}
+
+int vp_state_local_stats(vp_state_t st, const float** m_local, const float** sum_local) {
+  return api([&] {
+    require(st != nullptr, "vp_state_local_stats: null state");
+    if (m_local) *m_local = st->m_loc;
+    if (sum_local) *sum_local = st->s_loc;
+  });
+}
+
+int vp_state_grad_terms(vp_state_t st, const float** A, int64_t* lda) {
+  return api([&] {
+    require(st != nullptr, "vp_state_grad_terms: null state");
+    require(st->has_grad_terms, "alg2_barrier_C1: A/B terms missing");
+    if (A) *A = st->A;
+    if (lda) *lda = st->h;
+  });
+}
+
+int vp_state_copy_local_stats(vp_ctx_t c, vp_state_t st, float* m_out, float* sum_out) {
+  return api([&] {
+    require(c != nullptr && st != nullptr, "vp_state_copy_local_stats: null argument");
+    require(st->has_S, "vp_state_copy_local_stats: state has no pass-S output");
+    c->activate();
+    const size_t bytes = size_t(st->n_tok) * sizeof(float);
+    if (m_out) VP_CUDA(cudaMemcpyAsync(m_out, st->m_loc, bytes, cudaMemcpyDeviceToDevice, c->stream));
+    if (sum_out) VP_CUDA(cudaMemcpyAsync(sum_out, st->s_loc, bytes, cudaMemcpyDeviceToDevice, c->stream));
+  });
+}
+
+int vp_state_copy_grad_terms(vp_ctx_t c, vp_state_t st, float* A_out, int64_t ldo) {
+  return api([&] {
+    require(c != nullptr && st != nullptr && A_out != nullptr, "vp_state_copy_grad_terms: null argument");
+    require(st->has_grad_terms, "alg2_barrier_C1: A/B terms missing");
+    require(ldo >= st->h, "vp_state_copy_grad_terms: ldo < h");
+    c->activate();
+    VP_CUDA(cudaMemcpy2DAsync(A_out, size_t(ldo) * sizeof(float), st->A, size_t(st->h) * sizeof(float),
+                              size_t(st->h) * sizeof(float), size_t(st->n_tok), cudaMemcpyDeviceToDevice, c->stream));
+  });
+}
+
+int vp_alg1_pass_S(vp_ctx_t c, const vp_batch_t* b, const vp_shard_t* s, vp_state_t st) {
+  return api([&] {
+    require(c != nullptr, "alg1_pass_S: null context");
+    c->activate();
+    pass_S_common(c, b, s, st);
+  });
+}
+
+int vp_alg2_pass_S(vp_ctx_t c, const vp_batch_t* b, const vp_shard_t* s, vp_state_t st) {
+  return api([&] {
+    require(c != nullptr, "alg2_pass_S: null context");
+    c->activate();
+    alg2_S(c, b, s, st);
+  });
+}
+
+int vp_merge_max_sum(vp_ctx_t c, const vp_state_t* states, int n, double fault_scale, vp_stats_t out) {
+  return api([&] {
+    require(c != nullptr, "merge_max_sum: null context");
+    c->activate();
+    merge_stats(c, states, n, fault_scale, out);
+  });
+}
+
+int vp_merge_stats_raw(vp_ctx_t c, const float* m_parts, const float* s_parts, int p, int64_t n, int64_t ld,
+                       double fault_scale, vp_stats_t out) {
+  return api([&] {
+    require(c != nullptr, "merge_max_sum: null context");
+    require(p >= 1 && m_parts != nullptr && s_parts != nullptr, "merge_max_sum: empty input");
+    require(n >= 1 && ld >= n, "merge_max_sum: length mismatch");
+    require(out.m != nullptr && out.sum != nullptr, "merge_max_sum: null output");
+    c->activate();
+    vp::k_merge_stats<<<unsigned(ceil_div(n, 256)), 256, 0, c->stream>>>(m_parts, s_parts, p, ld, int(n),
+                                                                        float(fault_scale), out.m, out.sum);
+    VP_KCHECK();
+    ++c->launches;
+  });
+}
+
+int vp_alg1_pass_T(vp_ctx_t c, vp_state_t st, vp_stats_t stats, const vp_batch_t* b, const vp_shard_t* s,
+                   float* gx, int64_t ldgx, float* gw, int64_t ldgw) {
+  return api([&] {
+    require(c != nullptr, "alg1_pass_T: null context");
+    require(gx != nullptr && gw != nullptr, "alg1_pass_T: null gradient buffer");
+    c->activate();
+    alg1_T(c, st, stats, b, s, gx, ldgx, gw, ldgw);
+  });
+}
+
+int vp_reduce_grad_x(vp_ctx_t c, float* const* partials, int n, int64_t n_tok, int64_t h, int64_t ld, float* gx,
+                     int64_t ldgx) {
+  return api([&] {
+    require(c != nullptr && partials != nullptr && gx != nullptr, "reduce_grad_x: null argument");
+    c->activate();
+    reduce_partials(c, partials, n, n_tok, h, ld, gx, ldgx);
+  });
+}
+
+int vp_alg2_barrier_C1(vp_ctx_t c, const vp_state_t* states, const vp_shard_t* shards, int n, const vp_batch_t* b,
+                       double fault_scale, vp_stats_t out, float* gx, int64_t ldgx) {
+  return api([&] {
+    require(c != nullptr, "alg2_barrier_C1: null context");
+    require(n <= vp::kMaxLocalShards, "alg2_barrier_C1: too many local shards");
+    require(!c->distributed() || n == 1, "alg2_barrier_C1: one state per rank in an NCCL group");
+    c->activate();
+    alg2_C1(c, states, shards, n, b, fault_scale, out, gx, ldgx);
+  });
+}
+
+int vp_alg2_pass_T(vp_ctx_t c, vp_state_t st, vp_stats_t stats, const vp_batch_t* b, const vp_shard_t* s,
+                   float* gw, int64_t ldgw) {
+  return api([&] {
+    require(c != nullptr && gw != nullptr, "alg2_pass_T: null argument");
+    c->activate();
+    alg2_T(c, st, stats, b, s, gw, ldgw);
+  });
+}
+
+int vp_output_loss(vp_ctx_t c, const vp_state_t* states, const vp_shard_t* shards, int n, vp_stats_t stats,
+                   const vp_batch_t* b, float* loss) {
+  return api([&] {
+    require(c != nullptr && states != nullptr && shards != nullptr, "loss: null argument");
+    c->activate();
+    check_batch(b);
+    loss_of(c, states, shards, n, stats, b, loss);
+  });
+}
+
+int vp_shard_softmax(vp_ctx_t c, vp_state_t st, vp_stats_t g, float* out, int64_t ldo) {
+  return api([&] {
+    require(c != nullptr && st != nullptr && out != nullptr, "softmax: null argument");
+    require(st->has_S, "softmax: state has no pass-S output");
+    require(ldo >= st->rows, "softmax: ldo < rows");
+    c->activate();
+    const float* tile_m = nullptr;
+    const float* mref = nullptr;
+    const float* mul = nullptr;
+    if (st->form == kLocal) {  // P = softmax':  softmax = P * global_scale
+      mul = global_scale(c, st, g);
+    } else {  // kGlobal: P already is the softmax
+      float* ones = c->buf<float>(c->tmp_m, size_t(st->n_tok));
+      std::vector<float> h(size_t(st->n_tok), 1.f);
+      VP_CUDA(cudaMemcpyAsync(ones, h.data(), h.size() * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+      VP_CUDA(cudaStreamSynchronize(c->stream));
+      mul = ones;
+    }
+    vp::k_materialize<<<c->grid_for(st->n_tok * st->rows, 256), 256, 0, c->stream>>>(
+        st->P, st->ldp, int(st->n_tok), int(st->rows), tile_m, st->n_tok, mref, mul, out, ldo);
+    VP_KCHECK();
+    ++c->launches;
+  });
+}
+
+int vp_naive_partitioned_output(vp_ctx_t c, const vp_batch_t* b, const vp_shard_t* shards, const vp_state_t* states,
+                                int n, vp_stats_t out, float* loss, float* gx, int64_t ldgx, float* const* gw,
+                                int64_t ldgw) {
+  return api([&] {
+    require(c != nullptr && gx != nullptr && gw != nullptr && loss != nullptr, "naive: null argument");
+    c->activate();
+    naive(c, b, shards, states, n, out, loss, gx, ldgx, gw, ldgw);
+  });
+}
+
+int vp_run_alg1(vp_ctx_t c, const vp_batch_t* b, const vp_shard_t* shards, const vp_state_t* states, int n,
+                double fault_scale, vp_stats_t out, float* loss, float* gx, int64_t ldgx, float* const* gw,
+                int64_t ldgw) {
+  return api([&] {
+    require(c != nullptr && gx != nullptr && gw != nullptr && loss != nullptr, "run_alg1: null argument");
+    c->activate();
+    run_alg(1, c, b, shards, states, n, fault_scale, out, loss, gx, ldgx, gw, ldgw);
+  });
+}
+
+int vp_run_alg2(vp_ctx_t c, const vp_batch_t* b, const vp_shard_t* shards, const vp_state_t* states, int n,
+                double fault_scale, vp_stats_t out, float* loss, float* gx, int64_t ldgx, float* const* gw,
+                int64_t ldgw) {
+  return api([&] {
+    require(c != nullptr && gx != nullptr && gw != nullptr && loss != nullptr, "run_alg2: null argument");
+    c->activate();
+    run_alg(2, c, b, shards, states, n, fault_scale, out, loss, gx, ldgx, gw, ldgw);
+  });
+}
+
+int vp_input_forward(vp_ctx_t c, const int64_t* tokens, int64_t n_tok, int64_t h, const vp_shard_t* s, void* out,
+                     int64_t ldo, int accumulate) {
+  return api([&] {
+    require(c != nullptr && out != nullptr && tokens != nullptr, "input_forward: null argument");
+    require(n_tok >= 0, "input_forward: negative token count");
+    check_shard(s, h);
+    require(h % 8 == 0 && ldo >= h && ldo % 8 == 0 && aligned16(out), "input_forward: h/ldo must be multiples of 8");
+    if (n_tok == 0) return;
+    c->activate();
+    vp::k_input_forward<<<c->grid_for(n_tok, 8), 256, 0, c->stream>>>(
+        tokens, int(n_tok), static_cast<const __nv_bfloat16*>(s->W), s->ldw, s->row_begin, s->row_end, int(h),
+        static_cast<__nv_bfloat16*>(out), ldo, accumulate, c->d_err);
+    VP_KCHECK();
+    ++c->launches;
+  });
+}
+
+int vp_input_backward(vp_ctx_t c, const void* grad, int64_t ldg, int grad_is_f32, const int64_t* tokens,
+                      int64_t n_tok, int64_t h, const vp_shard_t* s, float* gw, int64_t ldgw, int accumulate) {
+  return api([&] {
+    require(c != nullptr && gw != nullptr && tokens != nullptr && grad != nullptr, "input_backward: null argument");
+    require(n_tok >= 0, "input_backward: grad/token length mismatch");
+    check_shard(s, h);
+    require(h % 8 == 0 && ldg >= h && ldg % 8 == 0 && ldgw >= h && ldgw % 4 == 0,
+            "input_backward: h/ld must be multiples of 8");
+    c->activate();
+    const int64_t rows = s->row_end - s->row_begin;
+    if (!accumulate) {
+      VP_CUDA(cudaMemset2DAsync(gw, size_t(ldgw) * sizeof(float), 0, size_t(h) * sizeof(float), size_t(rows),
+                                c->stream));
+    }
+    if (n_tok == 0) return;
+    int n_pad = 0;
+    unsigned long long* keys = sorted_keys(c, tokens, n_tok, s->row_begin, s->row_end, &n_pad, kErrInputBwd);
+    if (grad_is_f32)
+      vp::k_segment_scatter<float><<<unsigned(n_pad), 256, 0, c->stream>>>(
+          keys, n_pad, static_cast<const float*>(grad), ldg, int(h), 1.f, gw, ldgw, 1);
+    else
+      vp::k_segment_scatter<__nv_bfloat16><<<unsigned(n_pad), 256, 0, c->stream>>>(
+          keys, n_pad, static_cast<const __nv_bfloat16*>(grad), ldg, int(h), 1.f, gw, ldgw, 1);
+    VP_KCHECK();
+    ++c->launches;
+  });
+}
+
+int vp_allreduce_sum(vp_ctx_t c, void* buf, int64_t count, int dtype) {
+  return api([&] {
+    require(c != nullptr && buf != nullptr, "allreduce: null argument");
+    require(dtype == 0 || dtype == 1, "allreduce: dtype must be 0 (fp32) or 1 (bf16)");
+    if (!c->distributed()) return;
+    c->activate();
+    VP_NCCL(ncclAllReduce(buf, buf, size_t(count), dtype == 0 ? ncclFloat32 : ncclBfloat16, ncclSum, c->comm,
+                          c->stream));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,456 @@
+// Vocabulary-layer kernels around the tcgen05 GEMMs: stats reductions and
+// merges, softmax normalisation of the stored P tiles, the alg2 C1 combine,
+// loss, one-hot corrections, the input-layer masked gather and the
+// deterministic sort-based scatter-add.  All HBM-bound: 16-byte vector
+// accesses, grids sized in multiples of the SM count.
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace vp {
+
+constexpr int kTileN = 256;          // K1 vocab tile width (stats granularity)
+constexpr int kMaxLocalShards = 16;  // shards simulated on one device
+constexpr float kLog2e = 1.4426950408889634f;
+
+__device__ __forceinline__ float fast_exp(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x * kLog2e));
+  return y;
+}
+
+// ---------------------------------------------------------------------------
+// Per-row reduction of the K1 per-tile stats (m_ij, s_ij), tiles merged in
+// ascending j (fixed order: deterministic).  One warp-column per row group:
+// block = 256 threads = 8 warps x 32 rows; warp w takes tiles j = w, w+8, ...
+// then the 8 partials merge in w order.  s may be null (max only: naive F1).
+// ---------------------------------------------------------------------------
+__global__ void k_stats_reduce(const float* __restrict__ tile_m, const float* __restrict__ tile_s, int ntiles,
+                               int64_t ld, int n, float* __restrict__ m_out, float* __restrict__ s_out) {
+  __shared__ float sm[8][32], ss[8][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int row = blockIdx.x * 32 + lane;
+  float m = -INFINITY, s = 0.f;
+  if (row < n) {
+    for (int j = w; j < ntiles; j += 8) {
+      const float mj = tile_m[int64_t(j) * ld + row];
+      if (tile_s) {
+        const float sj = tile_s[int64_t(j) * ld + row];
+        const float nm = fmaxf(m, mj);
+        s = s * fast_exp(m - nm) + sj * fast_exp(mj - nm);
+        m = nm;
+      } else {
+        m = fmaxf(m, mj);
+      }
+    }
+  }
+  sm[w][lane] = m;
+  ss[w][lane] = s;
+  __syncthreads();
+  if (w == 0 && row < n) {
+    float M = sm[0][lane], S = ss[0][lane];
+    for (int q = 1; q < 8; ++q) {
+      const float mq = sm[q][lane];
+      if (mq == -INFINITY) continue;
+      const float nm = fmaxf(M, mq);
+      S = S * fast_exp(M - nm) + ss[q][lane] * fast_exp(mq - nm);
+      M = nm;
+    }
+    m_out[row] = M;
+    if (s_out) s_out[row] = S;
+  }
+}
+
+// merge_max_sum (VM.cpp:82-101) over p parts laid out [p x n]: m starts at
+// part 0 and takes the max in k order; sum accumulates sum_k e^{m_k - m} in
+// k order; then sum *= fault_scale (VM.cpp:314).
+__global__ void k_merge_stats(const float* __restrict__ mparts, const float* __restrict__ sparts, int p, int64_t ld,
+                              int n, float fault_scale, float* __restrict__ m_out, float* __restrict__ s_out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float m = mparts[i];
+  for (int k = 1; k < p; ++k) m = fmaxf(m, mparts[int64_t(k) * ld + i]);
+  float s = 0.f;
+  for (int k = 0; k < p; ++k) s += sparts[int64_t(k) * ld + i] * expf(mparts[int64_t(k) * ld + i] - m);
+  m_out[i] = m;
+  s_out[i] = s * fault_scale;
+}
+
+// Same merge with the parts given as pointer arrays (shards on one device).
+struct StatsParts {
+  const float* m[kMaxLocalShards];
+  const float* s[kMaxLocalShards];
+  int p;
+};
+__global__ void k_merge_stats_ptrs(StatsParts parts, int n, float fault_scale, float* __restrict__ m_out,
+                                   float* __restrict__ s_out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float m = parts.m[0][i];
+  for (int k = 1; k < parts.p; ++k) m = fmaxf(m, parts.m[k][i]);
+  float s = 0.f;
+  for (int k = 0; k < parts.p; ++k) s += parts.s[k][i] * expf(parts.m[k][i] - m);
+  m_out[i] = m;
+  s_out[i] = s * fault_scale;
+}
+
+// Pack (m_loc, s_loc) into one [2 x n] buffer for the stats all-gather.
+__global__ void k_pack_stats(const float* __restrict__ m, const float* __restrict__ s, int n, float* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  out[i] = m[i];
+  out[n + i] = s[i];
+}
+
+// ---------------------------------------------------------------------------
+// In-place rescale of the stored P (bf16 [n x ldp], valid cols < cols):
+//   P[i,v] <- P[i,v] * exp(tile_m[v/256][i] - mref[i]) * inv[i]
+// tile_m == null drops the tile factor (P already relative to mref).
+// 8 bf16 per thread (16-byte vectors); grid-stride.
+// ---------------------------------------------------------------------------
+__global__ void k_rescale_P(__nv_bfloat16* __restrict__ P, int64_t ldp, int n, int cols,
+                            const float* __restrict__ tile_m, int64_t ld_stats, const float* __restrict__ mref,
+                            const float* __restrict__ inv) {
+  const int vec_per_row = (cols + 7) / 8;
+  const int64_t total = int64_t(n) * vec_per_row;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < total; t += int64_t(gridDim.x) * blockDim.x) {
+    const int i = int(t / vec_per_row);
+    const int v0 = int(t - int64_t(i) * vec_per_row) * 8;
+    float f = inv[i];
+    if (tile_m) f *= fast_exp(tile_m[int64_t(v0 / kTileN) * ld_stats + i] - mref[i]);
+    uint4* ptr = reinterpret_cast<uint4*>(P + int64_t(i) * ldp + v0);
+    uint4 u = *ptr;
+    __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      float2 x = __bfloat1622float2(h2[q]);
+      x.x *= f;
+      x.y *= f;
+      h2[q] = __floats2bfloat162_rn(x.x, x.y);
+    }
+    // columns >= cols inside the last vector are padding: keep them zero
+    if (v0 + 8 > cols) {
+      __nv_bfloat16* e = reinterpret_cast<__nv_bfloat16*>(&u);
+      for (int q = cols - v0; q < 8; ++q) e[q] = __float2bfloat16(0.f);
+    }
+    *ptr = u;
+  }
+}
+
+// Per-row factor tables for the rescale:  inv = 1/s  (alg2 local softmax'),
+// inv = 1/sum_g (alg1 global), with mref = m_loc or m_global.
+__global__ void k_inv(const float* __restrict__ s, int n, float* __restrict__ inv) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) inv[i] = 1.f / s[i];
+}
+
+// global_scale (VM.cpp:22-27): c_i = sum'_i e^{m'_i - m_i} / sum_i
+__global__ void k_global_scale(const float* __restrict__ ml, const float* __restrict__ sl,
+                               const float* __restrict__ mg, const float* __restrict__ sg, int n,
+                               float* __restrict__ c) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) c[i] = sl[i] * expf(ml[i] - mg[i]) / sg[i];
+}
+
+// ---------------------------------------------------------------------------
+// alg2 C1 combine (VM.cpp:205-209): grad_x[i,:] = sum_k ( c_k[i] A_k[i,:] - B_k[i,:] )
+// with B_k[i,:] = W_k[g_i - rb_k,:] if shard k owns g_i (sparse row gather,
+// SPEC.md:231).  Shards summed in k order.  4 columns per thread.
+// ---------------------------------------------------------------------------
+struct CombineShards {
+  const float* A[kMaxLocalShards];
+  int64_t lda;
+  const __nv_bfloat16* W[kMaxLocalShards];
+  int64_t ldw[kMaxLocalShards];
+  int64_t rb[kMaxLocalShards], re[kMaxLocalShards];
+  const float* ml[kMaxLocalShards];
+  const float* sl[kMaxLocalShards];
+  int p;
+};
+__global__ void k_alg2_combine(CombineShards S, const float* __restrict__ mg, const float* __restrict__ sg,
+                               const int64_t* __restrict__ labels, int n, int h, float* __restrict__ gx,
+                               int64_t ldgx) {
+  const int hv = h / 4;
+  const int64_t total = int64_t(n) * hv;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < total; t += int64_t(gridDim.x) * blockDim.x) {
+    const int i = int(t / hv), c = int(t - int64_t(i) * hv) * 4;
+    const int64_t g = labels[i];
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int k = 0; k < S.p; ++k) {
+      const float sc = S.sl[k][i] * expf(S.ml[k][i] - mg[i]) / sg[i];
+      const float4 a = *reinterpret_cast<const float4*>(S.A[k] + int64_t(i) * S.lda + c);
+      float4 b = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (g >= S.rb[k] && g < S.re[k]) {
+        const __nv_bfloat16* w = S.W[k] + (g - S.rb[k]) * S.ldw[k] + c;
+        const float2 w0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(w));
+        const float2 w1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(w + 2));
+        b = make_float4(w0.x, w0.y, w1.x, w1.y);
+      }
+      acc.x += a.x * sc - b.x;
+      acc.y += a.y * sc - b.y;
+      acc.z += a.z * sc - b.z;
+      acc.w += a.w * sc - b.w;
+    }
+    *reinterpret_cast<float4*>(gx + int64_t(i) * ldgx + c) = acc;
+  }
+}
+
+// Sum of p partials in k order (alg1/naive C2 on one device).
+struct PartialPtrs {
+  const float* P[kMaxLocalShards];
+  int p;
+};
+__global__ void k_sum_partials(PartialPtrs S, int64_t count, float* __restrict__ out) {
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < count; t += int64_t(gridDim.x) * blockDim.x) {
+    float acc = 0.f;
+    for (int k = 0; k < S.p; ++k) acc += S.P[k][t];
+    out[t] = acc;
+  }
+}
+
+// dX correction for alg1/naive: gx[i,:] -= W_k[g_i - rb,:] for owned rows.
+__global__ void k_sub_label_rows(float* __restrict__ gx, int64_t ldgx, const __nv_bfloat16* __restrict__ W,
+                                 int64_t ldw, int64_t rb, int64_t re, const int64_t* __restrict__ labels, int n,
+                                 int h) {
+  const int hv = h / 2;
+  const int64_t total = int64_t(n) * hv;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < total; t += int64_t(gridDim.x) * blockDim.x) {
+    const int i = int(t / hv), c = int(t - int64_t(i) * hv) * 2;
+    const int64_t g = labels[i];
+    if (g < rb || g >= re) continue;
+    const float2 w = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(W + (g - rb) * ldw + c));
+    float* d = gx + int64_t(i) * ldgx + c;
+    d[0] -= w.x;
+    d[1] -= w.y;
+  }
+}
+
+// loss_i = m_i + log(sum_i) - y_tgt_i at the shard owning g_i (VM.cpp:287-292);
+// rows owned by none of the given shards get 0 (summed across ranks).
+struct LossShards {
+  const float* yt[kMaxLocalShards];
+  int64_t rb[kMaxLocalShards], re[kMaxLocalShards];
+  int p;
+};
+__global__ void k_loss(LossShards S, const float* __restrict__ mg, const float* __restrict__ sg,
+                       const int64_t* __restrict__ labels, int n, float* __restrict__ loss) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t g = labels[i];
+  float out = 0.f;
+  for (int k = 0; k < S.p; ++k)
+    if (g >= S.rb[k] && g < S.re[k]) out = mg[i] + logf(sg[i]) - S.yt[k][i];
+  loss[i] = out;
+}
+
+// Xs[i,:] = bf16(c_i * X[i,:])   (alg2 pass T: dW = P'^T diag(c) X)
+__global__ void k_scale_rows_bf16(const __nv_bfloat16* __restrict__ X, int64_t ldx, const float* __restrict__ c,
+                                  int n, int h, __nv_bfloat16* __restrict__ out, int64_t ldo) {
+  const int hv = h / 8;
+  const int64_t total = int64_t(n) * hv;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < total; t += int64_t(gridDim.x) * blockDim.x) {
+    const int i = int(t / hv), j = int(t - int64_t(i) * hv) * 8;
+    uint4 u = *reinterpret_cast<const uint4*>(X + int64_t(i) * ldx + j);
+    __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u);
+    const float f = c[i];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      float2 x = __bfloat1622float2(h2[q]);
+      h2[q] = __floats2bfloat162_rn(x.x * f, x.y * f);
+    }
+    *reinterpret_cast<uint4*>(out + int64_t(i) * ldo + j) = u;
+  }
+}
+
+// naive F2: e = exp(Y - m) from the stored fp32 logits (re-read, VM.cpp:119-125),
+// written as bf16 P, plus the per-row local exp-sum.  One block per row.
+__global__ void k_naive_exp_sum(const float* __restrict__ Y, int64_t ldy, int cols, const float* __restrict__ m,
+                                __nv_bfloat16* __restrict__ P, int64_t ldp, float* __restrict__ s_out) {
+  const int i = blockIdx.x;
+  const float mi = m[i];
+  float acc = 0.f;
+  for (int v = threadIdx.x * 4; v < cols; v += blockDim.x * 4) {
+    float e[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) e[q] = (v + q < cols) ? fast_exp(Y[int64_t(i) * ldy + v + q] - mi) : 0.f;
+    acc += (e[0] + e[1]) + (e[2] + e[3]);
+    __nv_bfloat162* d = reinterpret_cast<__nv_bfloat162*>(P + int64_t(i) * ldp + v);
+    if (v + 4 <= cols) {
+      d[0] = __floats2bfloat162_rn(e[0], e[1]);
+      d[1] = __floats2bfloat162_rn(e[2], e[3]);
+    } else {
+      for (int q = 0; q < 4 && v + q < cols; ++q) P[int64_t(i) * ldp + v + q] = __float2bfloat16(e[q]);
+    }
+  }
+  __shared__ float red[32];
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float s = 0.f;
+    for (int w = 0; w < int(blockDim.x >> 5); ++w) s += red[w];
+    s_out[i] = s;
+  }
+}
+
+// naive: y_tgt[i] = Y[i, g_i - rb] for owned rows (VM.cpp:139-140)
+__global__ void k_gather_target(const float* __restrict__ Y, int64_t ldy, const int64_t* __restrict__ labels,
+                                int64_t rb, int64_t re, int n, float* __restrict__ yt) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t g = labels[i];
+  if (g >= rb && g < re) yt[i] = Y[int64_t(i) * ldy + (g - rb)];
+}
+
+// Debug/parity materialisation (assemble_forward softmax, VM.cpp:281-286):
+// out[i, v] = P[i,v] * f(i, v) in fp32 (same factor as k_rescale_P).
+__global__ void k_materialize(const __nv_bfloat16* __restrict__ P, int64_t ldp, int n, int cols,
+                              const float* __restrict__ tile_m, int64_t ld_stats, const float* __restrict__ mref,
+                              const float* __restrict__ mul, float* __restrict__ out, int64_t ldo) {
+  const int64_t total = int64_t(n) * cols;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < total; t += int64_t(gridDim.x) * blockDim.x) {
+    const int i = int(t / cols), v = int(t - int64_t(i) * cols);
+    float f = mul[i];
+    if (tile_m) f *= fast_exp(tile_m[int64_t(v / kTileN) * ld_stats + i] - mref[i]);
+    out[int64_t(i) * ldo + v] = __bfloat162float(P[int64_t(i) * ldp + v]) * f;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Input layer.
+// K7 input_forward (VM.cpp:227-236): out[i,:] = W_k[t_i - rb,:] if owned else 0.
+// One warp per token row, 16-byte vectors.  t_i < 0 raises the context's
+// error flag (the reference throws invalid_argument); t_i >= V is "not owned".
+// accumulate != 0 adds the owned rows onto out instead (fused all-reduce
+// target for shards simulated on one device).
+// ---------------------------------------------------------------------------
+__global__ void k_input_forward(const int64_t* __restrict__ tok, int n, const __nv_bfloat16* __restrict__ W,
+                                int64_t ldw, int64_t rb, int64_t re, int h, __nv_bfloat16* __restrict__ out,
+                                int64_t ldo, int accumulate, int* __restrict__ err) {
+  const int warps = (blockDim.x >> 5);
+  const int lane = threadIdx.x & 31;
+  for (int i = blockIdx.x * warps + (threadIdx.x >> 5); i < n; i += gridDim.x * warps) {
+    const int64_t t = tok[i];
+    if (t < 0 && lane == 0) atomicOr(err, 1);
+    const bool own = t >= rb && t < re;
+    uint4* d = reinterpret_cast<uint4*>(out + int64_t(i) * ldo);
+    const uint4* s = reinterpret_cast<const uint4*>(W + (own ? (t - rb) : 0) * ldw);
+    const int hv = h / 8;
+    if (!accumulate) {
+      for (int j = lane; j < hv; j += 32) d[j] = own ? __ldg(s + j) : make_uint4(0u, 0u, 0u, 0u);
+    } else if (own) {
+      for (int j = lane; j < hv; j += 32) {
+        uint4 a = d[j];
+        const uint4 b = __ldg(s + j);
+        __nv_bfloat162* a2 = reinterpret_cast<__nv_bfloat162*>(&a);
+        const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&b);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) a2[q] = __hadd2(a2[q], b2[q]);
+        d[j] = a;
+      }
+    }
+  }
+}
+
+// Sort keys for the deterministic scatter-add: key = (local_row << 32) | i for
+// owned tokens, UINT64_MAX otherwise; n_pad = next power of two.
+__global__ void k_make_keys(const int64_t* __restrict__ tok, int n, int n_pad, int64_t rb, int64_t re,
+                            unsigned long long* __restrict__ keys, int* __restrict__ err, int err_bit) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_pad) return;
+  unsigned long long k = ~0ull;
+  if (i < n) {
+    const int64_t t = tok[i];
+    if (t < 0 && err_bit) atomicOr(err, err_bit);
+    if (t >= rb && t < re) k = (static_cast<unsigned long long>(t - rb) << 32) | static_cast<unsigned>(i);
+  }
+  keys[i] = k;
+}
+
+// Bitonic sort building blocks (ascending, n_pad power of two).
+__global__ void k_bitonic_global(unsigned long long* __restrict__ keys, int n_pad, int j, int k) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_pad) return;
+  const int l = i ^ j;
+  if (l > i) {
+    const unsigned long long a = keys[i], b = keys[l];
+    const bool up = (i & k) == 0;
+    if ((a > b) == up) {
+      keys[i] = b;
+      keys[l] = a;
+    }
+  }
+}
+// Sorts/merges 2048-key chunks in shared memory.  full != 0: complete
+// bitonic sort of each chunk (k = 2..kmax); else only the j < 2048 steps of
+// stage k.
+__global__ void k_bitonic_shared(unsigned long long* __restrict__ keys, int n_pad, int k_stage, int full) {
+  __shared__ unsigned long long s[2048];
+  const int base = blockIdx.x * 2048;
+  for (int q = threadIdx.x; q < 2048; q += blockDim.x) s[q] = base + q < n_pad ? keys[base + q] : ~0ull;
+  __syncthreads();
+  auto step = [&](int j, int k) {
+    for (int q = threadIdx.x; q < 2048; q += blockDim.x) {
+      const int i = base + q, l = i ^ j;
+      if (l > i && (l - base) < 2048) {
+        const unsigned long long a = s[q], b = s[l - base];
+        const bool up = (i & k) == 0;
+        if ((a > b) == up) {
+          s[q] = b;
+          s[l - base] = a;
+        }
+      }
+    }
+    __syncthreads();
+  };
+  if (full) {
+    const int kmax = n_pad < 2048 ? n_pad : 2048;
+    for (int k = 2; k <= kmax; k <<= 1)
+      for (int j = k >> 1; j > 0; j >>= 1) step(j, k);
+  } else {
+    for (int j = 1024; j > 0; j >>= 1) step(j, k_stage);
+  }
+  for (int q = threadIdx.x; q < 2048; q += blockDim.x)
+    if (base + q < n_pad) keys[base + q] = s[q];
+}
+
+// Segmented, ordered scatter-add over sorted keys (K8 and the dW one-hot
+// correction).  One block per sorted position; only segment heads work:
+//   dst[row,:] = (accumulate ? dst[row,:] : 0) + sign*src[i1,:] + sign*src[i2,:] + ...
+// with i1 < i2 < ... (ascending-i order of VM.cpp:245-249), fp32.
+template <typename Src>
+__global__ void k_segment_scatter(const unsigned long long* __restrict__ keys, int n_pad,
+                                  const Src* __restrict__ src, int64_t lds, int h, float sign,
+                                  float* __restrict__ dst, int64_t ldd, int accumulate) {
+  const int s0 = blockIdx.x;
+  const unsigned long long k0 = keys[s0];
+  if (k0 == ~0ull) return;
+  const unsigned row = unsigned(k0 >> 32);
+  if (s0 > 0 && unsigned(keys[s0 - 1] >> 32) == row) return;  // not a head
+  int e = s0 + 1;
+  while (e < n_pad && keys[e] != ~0ull && unsigned(keys[e] >> 32) == row) ++e;
+  float* d = dst + int64_t(row) * ldd;
+  for (int c = threadIdx.x * 4; c < h; c += blockDim.x * 4) {
+    float4 acc = accumulate ? *reinterpret_cast<const float4*>(d + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int q = s0; q < e; ++q) {
+      const unsigned i = unsigned(keys[q] & 0xffffffffu);
+      float4 v;
+      if constexpr (sizeof(Src) == 2) {
+        const __nv_bfloat162* p = reinterpret_cast<const __nv_bfloat162*>(src + int64_t(i) * lds + c);
+        const float2 a = __bfloat1622float2(p[0]), b = __bfloat1622float2(p[1]);
+        v = make_float4(a.x, a.y, b.x, b.y);
+      } else {
+        v = *reinterpret_cast<const float4*>(src + int64_t(i) * lds + c);
+      }
+      acc.x += sign * v.x;
+      acc.y += sign * v.y;
+      acc.z += sign * v.z;
+      acc.w += sign * v.w;
+    }
+    *reinterpret_cast<float4*>(d + c) = acc;
+  }
+}
+
+}  // namespace vp
