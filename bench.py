@@ -1,0 +1,367 @@
+#!/usr/bin/env python3
+"""Benchmark of the vocabulary-parallel output layer (fwd+bwd) on B200.
+
+Metric (BASELINE.json): vocab-layer fwd+bwd tokens/s at V=256k, h=4096 on
+1/2/4/8 B200s.  One step = one Algorithm-2 (reduced-barrier) forward +
+backward of the output layer over one microbatch of T=8192 synthetic tokens:
+pass S (logits GEMM + fused stats epilogue, softmax', A = softmax' W_k), the
+single C1 barrier (stats all-gather + merge, dX combine + all-reduce), the
+loss and pass T (dW GEMM + ordered one-hot correction).  The vocabulary is
+sharded over the N ranks (one process per GPU, NCCL over NVLink between
+them); total work is fixed as N grows ("strong" scaling).
+
+  python bench.py [--gpus N --steps K --warmup W]          # our sm_100a path
+  python bench.py --impl reference [...]                    # reference CPU path
+  torchrun --nproc-per-node N bench.py --gpus N [...]       # N > 1
+
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "vocab-layer fwd+bwd tokens/s at V=256k,h=4096 @1/2/4/8 B200; % BF16 TC peak"
+WORKLOAD = "vocab-parallel output layer fwd+bwd, Algorithm 2 (reduced barrier), vocab sharded over N GPUs"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--alg", choices=["alg2", "alg1", "naive"], default="alg2")
+    ap.add_argument("--tokens", type=int, default=8192)
+    ap.add_argument("--hidden", type=int, default=4096)
+    ap.add_argument("--vocab", type=int, default=256000)
+    ap.add_argument("--cta-group", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-tokens", type=int, default=64)
+    ap.add_argument("--cpu-sample-vocab", type=int, default=64000)
+    return ap.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(
+        os.environ.get("LOCAL_RANK", "0"))
+
+
+def measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled DURING the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+                out = ""
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                smax = float(f[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": smax, "reasons": sorted(reasons), "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU side: the reference's own algorithm (oracle restatement), bounded sample
+# ---------------------------------------------------------------------------
+def cpu_reference_sample(T_s: int, h: int, V_s: int, p: int, reps: int = 1):
+    """Times run_alg2 (VM.cpp:328-361, fp64, incl. the [T x V] softmax assembly)
+    of the CPU oracle on a [T_s tokens x V_s vocab rows] slice; returns seconds."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import numpy as np
+
+    import oracle
+    rng = np.random.default_rng(1234)
+    X = rng.standard_normal((T_s, h))
+    W = rng.standard_normal((V_s, h)) * 0.02
+    g = rng.integers(0, V_s, T_s)
+    times = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        oracle.run("alg2", X, g, W, p)
+        times.append(time.perf_counter() - t0)
+    return times, oracle.num_threads()
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return  # rank 0 alone runs the CPU reference
+    T, h, V = args.tokens, args.hidden, args.vocab
+    T_s, V_s = 16, min(args.cpu_sample_vocab, V)
+    p = max(1, args.gpus)
+    while V_s % p:
+        V_s -= 1
+    times, cores = cpu_reference_sample(T_s, h, V_s, p, reps=args.warmup + args.steps)
+    timed = times[args.warmup:]
+    t = sum(timed) / len(timed)
+    scale = V / V_s  # cost is linear in V (three T x h x V GEMMs + T x V elementwise)
+    value = T_s / (t * scale)
+    sample = (f"run_alg2 (fp64 CPU oracle restating VM.cpp:328-361) on {T_s} tokens x {V_s} of {V} vocab rows, "
+              f"h={h}, p={p}; tokens/s scaled by {V_s}/{V} (cost linear in V)")
+    line = {
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+        "config": {"workload": "reference CPU path: " + WORKLOAD, "tokens": T, "hidden": h, "vocab": V,
+                   "shards": p},
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU side: our sm_100a path through the C ABI
+# ---------------------------------------------------------------------------
+class Step:
+    """Pre-marshalled call of vp_run_alg{1,2} / vp_naive_partitioned_output for
+    one rank's shard (no per-step Python allocation or argument building)."""
+
+    def __init__(self, ctx, alg, batch, shard, state, outs):
+        from paper_2411_05288_b200._lib import vp_shard_t
+        self.ctx = ctx
+        loss, gx, gw, stats = outs
+        self.batch_c = batch.c()
+        self.shards_c = (vp_shard_t * 1)(shard.c())
+        self.states_c = (ctypes.c_void_p * 1)(state.handle.value)
+        self.gw_c = (ctypes.c_void_p * 1)(gw.data_ptr())
+        lib = ctx.lib
+        common_tail = [stats.c(), ctypes.c_void_p(loss.data_ptr()), ctypes.c_void_p(gx.data_ptr()), gx.stride(0),
+                       self.gw_c, gw.stride(0)]
+        head = [ctx.handle, ctypes.byref(self.batch_c), self.shards_c, self.states_c, 1]
+        if alg == "naive":
+            self.fn, self.args = lib.vp_naive_partitioned_output, head + common_tail
+        else:
+            fn = lib.vp_run_alg2 if alg == "alg2" else lib.vp_run_alg1
+            self.fn, self.args = fn, head + [1.0] + common_tail
+
+    def __call__(self):
+        rc = self.fn(*self.args)
+        if rc:
+            from paper_2411_05288_b200._lib import check
+            check(rc)
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2411_05288_b200 import vocab_math as vm
+
+    rank, world, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    T, h, V = args.tokens, args.hidden, args.vocab
+    if V % world:
+        raise SystemExit("vocab must divide by the number of GPUs (pad_vocab_size)")
+    rows = V // world
+    ctx = vm.Context(local, cta_group=args.cta_group)
+    if world > 1:
+        uid = [vm.Context.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        ctx.comm_init(world, rank, uid[0])
+    ctx.reserve(T, h, world)
+
+    # synthetic inputs of the named shape (X~N(0,1), W~N(0,0.02^2), seed 1234)
+    gen = torch.Generator(device="cuda").manual_seed(1234)
+    X = torch.randn(T, h, device="cuda", generator=gen).to(torch.bfloat16)
+    labels = torch.randint(0, V, (T,), device="cuda", generator=gen)
+    gen.manual_seed(1234 + 1 + rank)
+    W_k = (torch.randn(rows, h, device="cuda", generator=gen) * 0.02).to(torch.bfloat16)
+    shard = vm.EmbeddingShard(W_k, rank, rank * rows, (rank + 1) * rows)
+    batch = vm.TokenBatch(X, labels)
+    state = vm.ShardState(ctx, T, h, rows)
+    outs = (torch.empty(T, dtype=torch.float32, device="cuda"), torch.empty(T, h, dtype=torch.float32, device="cuda"),
+            torch.empty(rows, h, dtype=torch.float32, device="cuda"), vm.GlobalStats.empty(T, "cuda"))
+    step = Step(ctx, args.alg, batch, shard, state, outs)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- device-resident throughput (value) ----
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    ctx.gemm_timing(True)
+    launches0 = ctx.launches
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        barrier()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    launches = ctx.launches - launches0
+    gemm = ctx.gemm_timing(False)
+    ms = max_over_ranks(ms)
+    value = T / (ms / 1e3)
+
+    # ---- end-to-end through the public API with host buffers (e2e) ----
+    e2e = None
+    if not args.no_e2e:
+        Xh = X.cpu().pin_memory()
+        Lh = labels.cpu().pin_memory()
+        loss_h = torch.empty(T, dtype=torch.float32).pin_memory()
+        Xd, Ld = torch.empty_like(X), torch.empty_like(labels)
+        step_e2e = Step(ctx, args.alg, vm.TokenBatch(Xd, Ld), shard, state, outs)
+
+        def e2e_step():
+            Xd.copy_(Xh, non_blocking=True)
+            Ld.copy_(Lh, non_blocking=True)
+            step_e2e()
+            loss_h.copy_(outs[0], non_blocking=True)
+
+        for _ in range(args.warmup):
+            e2e_step()
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        ev1.record(stream)
+        barrier()
+        ms_e2e = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
+        e2e = {"value": T / (ms_e2e / 1e3), "unit": "tokens/s", "ms_per_step": ms_e2e,
+               "h2d_bytes_per_step": Xh.numel() * 2 + Lh.numel() * 8, "d2h_bytes_per_step": loss_h.numel() * 4,
+               "path": "vp_run_%s via ctypes (C ABI), pinned host X/labels -> HBM, loss -> host" % args.alg}
+
+    if rank != 0:
+        ctx.close()
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel (tensor-bound GEMMs) ----
+    peaks = measured_peaks()
+    peak = peaks.get("bf16_tflops_sustained") if peaks else 1400.0
+    peak_src = "MEASURED_PEAKS.json bf16_tflops_sustained (kernel timed inside a long step)" if peaks else \
+        "fallback (B200_PROFILING.md)"
+    flops_launch = 2.0 * T * h * rows  # each of K1 (logits), K3 (dX / A), K4 (dW)
+    kern = {}
+    for name, (kms, n) in gemm.items():
+        if n:
+            kern[name] = {"launches": n, "avg_ms": kms / n, "tflops": flops_launch / (kms / n / 1e3) / 1e12}
+    dom = max(kern, key=lambda k: kern[k]["avg_ms"] * kern[k]["launches"]) if kern else None
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if dom and os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(f"{dom}:{T}x{h}x{rows}")
+        except Exception:
+            traffic = None
+    achieved = kern[dom]["tflops"] if dom else None
+    roofline = {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                "peak_source": peak_src, "flops_per_launch": flops_launch, "gemms": kern,
+                "step_frac_of_peak": (6.0 * T * h * V / (ms / 1e3) / 1e12) / (world * peak),
+                "step_frac_of_nominal_2250": (6.0 * T * h * V / (ms / 1e3) / 1e12) / (world * 2250.0)}
+
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        T_s, V_s = args.cpu_sample_tokens, min(args.cpu_sample_vocab, V)
+        times, cores = cpu_reference_sample(T_s, h, V_s, 1)
+        cpu = {"value": T_s / (times[0] * V / V_s), "unit": "tokens/s", "cores": cores, "kind": "port",
+               "sample": (f"CPU oracle run_alg2 (fp64, restates VM.cpp:328-361) on {T_s} tokens x {V_s} of {V} "
+                          f"vocab rows, h={h}, {times[0]:.1f} s; tokens/s scaled by {V_s}/{V}")}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (X~N(0,1), W~N(0,0.02^2), uniform labels, seed 1234)",
+        "config": {"workload": WORKLOAD.replace("Algorithm 2 (reduced barrier)", {
+            "alg2": "Algorithm 2 (reduced barrier)", "alg1": "Algorithm 1 (2 barriers)",
+            "naive": "naive 3-barrier"}[args.alg]),
+            "alg": args.alg, "tokens": T, "hidden": h, "vocab": V, "vocab_rows_per_gpu": rows,
+            "parallelism": f"vocab{world}", "operands": "bf16", "accum_and_stats": "fp32",
+            "cta_group": args.cta_group,
+            "l2": "inputs larger than L2 every step (W_k %.0f MB, P %.0f MB per GPU)" % (
+                rows * h * 2 / 1e6, T * rows * 2 / 1e6)},
+        "e2e": e2e, "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -78,7 +78,8 @@ const char* vp_last_error(void);
 
 int vp_ctx_create(int device, vp_ctx_t* out);
 int vp_ctx_destroy(vp_ctx_t ctx);
-/* Use an existing cudaStream_t (NULL = the context's own stream). */
+/* Run on an existing cudaStream_t (NULL = the legacy default stream).  A new
+ * context runs on its own non-blocking stream until this is called. */
 int vp_ctx_set_stream(vp_ctx_t ctx, void* stream);
 void* vp_ctx_get_stream(vp_ctx_t ctx);
 /* Wait for the stream; report deferred device-side argument errors. */
@@ -89,6 +90,11 @@ int vp_ctx_reserve(vp_ctx_t ctx, int64_t n_tok, int64_t h, int p);
 int vp_ctx_set_option(vp_ctx_t ctx, const char* key, int64_t value);
 /* Number of kernels this context has launched (evidence counter). */
 int64_t vp_ctx_launch_count(vp_ctx_t ctx);
+/* Per-GEMM CUDA-event timing on the launching stream.  Returns (and resets)
+ * the accumulated milliseconds / launch counts per GEMM kind since the last
+ * call — [0] logits+stats (K1), [1] fp32 logits (naive F1), [2] dX (K3),
+ * [3] dW (K4) — then enables (enable=1) or disables timing.  Synchronises. */
+int vp_ctx_gemm_timing(vp_ctx_t ctx, int enable, double* ms_out4, int64_t* count_out4);
 
 /* NCCL group: rank 0 creates the id, every rank calls comm_init with it. */
 int vp_comm_unique_id(void* id128);
@@ -100,6 +106,7 @@ int vp_ctx_comm_info(vp_ctx_t ctx, int* nranks, int* rank);
  * (never the fp32 logits), per-256-column tile stats, m'/sum', the label
  * logit y[i, g_i] of owned rows, A [n_tok x h] fp32 (alg2). */
 int vp_state_create(vp_ctx_t ctx, int64_t n_tok, int64_t h, int64_t rows, vp_state_t* out);
+/* States belong to their context: destroy them before vp_ctx_destroy. */
 int vp_state_destroy(vp_state_t st);
 /* m_local / sum_local (VM.hpp:36-37), device fp32 [n_tok]. */
 int vp_state_local_stats(vp_state_t st, const float** m_local, const float** sum_local);

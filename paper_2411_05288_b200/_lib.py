@@ -40,6 +40,7 @@ SIGNATURES = {
     "vp_ctx_reserve": (c_int, [c_void_p, c_int64, c_int64, c_int]),
     "vp_ctx_set_option": (c_int, [c_void_p, c_char_p, c_int64]),
     "vp_ctx_launch_count": (c_int64, [c_void_p]),
+    "vp_ctx_gemm_timing": (c_int, [c_void_p, c_int, POINTER(ctypes.c_double), POINTER(c_int64)]),
     "vp_comm_unique_id": (c_int, [c_void_p]),
     "vp_ctx_comm_init": (c_int, [c_void_p, c_int, c_int, c_void_p]),
     "vp_ctx_comm_info": (c_int, [c_void_p, POINTER(c_int), POINTER(c_int)]),
@@ -94,6 +95,13 @@ def load() -> ctypes.CDLL:
         raise ImportError(
             f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
             "(there is no CPU fallback for the product path)")
+    # libvpipe_b200.so needs libnccl.so.2.  torch bundles a newer NCCL under
+    # the same soname; whichever loads first wins process-wide, and torch
+    # needs its own, so let torch load it first (ours is ABI-compatible).
+    try:
+        import torch  # noqa: F401
+    except ImportError:
+        pass
     lib = ctypes.CDLL(LIB_PATH)
     for name, (res, args) in SIGNATURES.items():
         fn = getattr(lib, name)

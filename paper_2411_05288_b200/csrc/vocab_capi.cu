@@ -102,10 +102,20 @@ struct vp_ctx_s {
   int nranks = 1, rank = 0;
   int* d_err = nullptr;
   int64_t launches = 0;
+  // optional per-GEMM event timing (bench instrumentation): kind -> events
+  bool timing = false;
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_pending;
+  size_t ev_next = 0;
+  double gemm_ms[4] = {0, 0, 0, 0};
+  int64_t gemm_n[4] = {0, 0, 0, 0};
   // workspace
   DevBuf inv, scale, xs, keys, gathered, packed, tmp_m, tmp_s;
 
-  void activate() const { VP_CUDA(cudaSetDevice(device)); }
+  void activate() const {
+    VP_CUDA(cudaSetDevice(device));
+    (void)cudaGetLastError();  // drop stale non-sticky errors left by other code
+  }
   bool distributed() const { return comm != nullptr && nranks > 1; }
   template <class T>
   T* buf(DevBuf& b, size_t count) {
@@ -155,19 +165,46 @@ void check_state(const vp_state_s* st, const vp_batch_t* b, const vp_shard_t* s)
   if (s) require(st->rows == s->row_end - s->row_begin, "ShardState: shard rows mismatch");
 }
 
+// ---- GEMM timing (kinds: 0 logits+stats K1, 1 logits fp32 (naive), 2 dX K3, 3 dW K4) --
+cudaEvent_t next_event(vp_ctx_s* c) {
+  if (c->ev_next == c->ev_pool.size()) {
+    cudaEvent_t e;
+    VP_CUDA(cudaEventCreate(&e));
+    c->ev_pool.push_back(e);
+  }
+  return c->ev_pool[c->ev_next++];
+}
+
+template <class F>
+void timed_gemm(vp_ctx_s* c, int kind, F&& launch) {
+  if (!c->timing) {
+    launch();
+    return;
+  }
+  cudaEvent_t a = next_event(c), b = next_event(c);
+  VP_CUDA(cudaEventRecord(a, c->stream));
+  launch();
+  VP_CUDA(cudaEventRecord(b, c->stream));
+  c->ev_pending.push_back({kind, {a, b}});
+}
+
 // ---- GEMM wrappers ---------------------------------------------------------
 void gemm_logits(vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* s, vp_state_s* st) {
   vp::EpiLogitStats::Params ep{st->P, st->ldp, st->tile_m, st->tile_s, st->n_tok, b->labels, s->row_begin,
                                s->row_end, st->ytgt};
-  vp::launch_gemm<vp::EpiLogitStats>(c->cg, {b->X, b->ldx, false}, {s->W, s->ldw, false}, int(b->n_tok),
-                                     int(st->rows), int(b->h), 0, ep, c->gemm_sms, c->stream);
+  timed_gemm(c, 0, [&] {
+    vp::launch_gemm<vp::EpiLogitStats>(c->cg, {b->X, b->ldx, false}, {s->W, s->ldw, false}, int(b->n_tok),
+                                       int(st->rows), int(b->h), 0, ep, c->gemm_sms, c->stream);
+  });
   ++c->launches;
 }
 
 void gemm_logits_f32(vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* s, vp_state_s* st) {
   vp::EpiStoreF32::Params ep{st->Y, st->rows, st->tile_m, st->n_tok, nullptr};
-  vp::launch_gemm<vp::EpiStoreF32>(c->cg, {b->X, b->ldx, false}, {s->W, s->ldw, false}, int(b->n_tok),
-                                   int(st->rows), int(b->h), 0, ep, c->gemm_sms, c->stream);
+  timed_gemm(c, 1, [&] {
+    vp::launch_gemm<vp::EpiStoreF32>(c->cg, {b->X, b->ldx, false}, {s->W, s->ldw, false}, int(b->n_tok),
+                                     int(st->rows), int(b->h), 0, ep, c->gemm_sms, c->stream);
+  });
   ++c->launches;
 }
 
@@ -175,8 +212,10 @@ void gemm_logits_f32(vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* s, vp_s
 void gemm_dx(vp_ctx_s* c, vp_state_s* st, const vp_shard_t* s, float* out, int64_t ldo,
              const float* row_scale = nullptr) {
   vp::EpiStoreF32::Params ep{out, ldo, nullptr, 0, row_scale};
-  vp::launch_gemm<vp::EpiStoreF32>(c->cg, {st->P, st->ldp, false}, {s->W, s->ldw, true}, int(st->n_tok),
-                                   int(st->h), int(st->rows), 8, ep, c->gemm_sms, c->stream);
+  timed_gemm(c, 2, [&] {
+    vp::launch_gemm<vp::EpiStoreF32>(c->cg, {st->P, st->ldp, false}, {s->W, s->ldw, true}, int(st->n_tok),
+                                     int(st->h), int(st->rows), 8, ep, c->gemm_sms, c->stream);
+  });
   ++c->launches;
 }
 
@@ -184,8 +223,10 @@ void gemm_dx(vp_ctx_s* c, vp_state_s* st, const vp_shard_t* s, float* out, int64
 void gemm_dw(vp_ctx_s* c, vp_state_s* st, const void* Xop, int64_t ldx, float* out, int64_t ldo) {
   vp::EpiStoreF32::Params ep{out, ldo, nullptr, 0, nullptr};
   const int tiles_n = int(ceil_div(st->h, 256));
-  vp::launch_gemm<vp::EpiStoreF32>(c->cg, {st->P, st->ldp, true}, {Xop, ldx, true}, int(st->rows), int(st->h),
-                                   int(st->n_tok), -tiles_n, ep, c->gemm_sms, c->stream);
+  timed_gemm(c, 3, [&] {
+    vp::launch_gemm<vp::EpiStoreF32>(c->cg, {st->P, st->ldp, true}, {Xop, ldx, true}, int(st->rows), int(st->h),
+                                     int(st->n_tok), -tiles_n, ep, c->gemm_sms, c->stream);
+  });
   ++c->launches;
 }
 
@@ -591,6 +632,7 @@ int vp_ctx_destroy(vp_ctx_t c) {
     c->activate();
     cudaStreamSynchronize(c->stream);
     if (c->comm) ncclCommDestroy(c->comm);
+    for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
     for (DevBuf* b : {&c->inv, &c->scale, &c->xs, &c->keys, &c->gathered, &c->packed, &c->tmp_m, &c->tmp_s})
       b->release();
     if (c->d_err) cudaFree(c->d_err);
@@ -602,7 +644,7 @@ int vp_ctx_destroy(vp_ctx_t c) {
 int vp_ctx_set_stream(vp_ctx_t c, void* stream) {
   return api([&] {
     require(c != nullptr, "vp_ctx_set_stream: null context");
-    c->stream = stream ? static_cast<cudaStream_t>(stream) : c->own_stream;
+    c->stream = static_cast<cudaStream_t>(stream);  // NULL = the legacy default stream
   });
 }
 
@@ -657,6 +699,31 @@ int vp_ctx_set_option(vp_ctx_t c, const char* key, int64_t value) {
 }
 
 int64_t vp_ctx_launch_count(vp_ctx_t c) { return c ? c->launches : -1; }
+
+int vp_ctx_gemm_timing(vp_ctx_t c, int enable, double* ms_out, int64_t* count_out) {
+  return api([&] {
+    require(c != nullptr, "vp_ctx_gemm_timing: null context");
+    c->activate();
+    if (!c->ev_pending.empty()) {
+      VP_CUDA(cudaStreamSynchronize(c->stream));
+      for (auto& p : c->ev_pending) {
+        float ms = 0.f;
+        VP_CUDA(cudaEventElapsedTime(&ms, p.second.first, p.second.second));
+        c->gemm_ms[p.first] += ms;
+        c->gemm_n[p.first] += 1;
+      }
+      c->ev_pending.clear();
+    }
+    c->ev_next = 0;
+    for (int k = 0; k < 4; ++k) {
+      if (ms_out) ms_out[k] = c->gemm_ms[k];
+      if (count_out) count_out[k] = c->gemm_n[k];
+      c->gemm_ms[k] = 0.0;
+      c->gemm_n[k] = 0;
+    }
+    c->timing = enable != 0;
+  });
+}
 
 int vp_comm_unique_id(void* id128) {
   return api([&] {

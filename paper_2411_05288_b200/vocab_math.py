@@ -18,6 +18,7 @@ std::invalid_argument in the reference maps to ValueError here.
 from __future__ import annotations
 
 import ctypes
+import weakref
 from dataclasses import dataclass, field
 from typing import List, Optional, Sequence
 
@@ -45,6 +46,7 @@ class Context:
     def __init__(self, device: int = 0, cta_group: int = 2):
         self.lib = _lib.load()
         self.device = int(device)
+        self._states = weakref.WeakSet()  # states must die before the context
         h = ctypes.c_void_p()
         check(self.lib.vp_ctx_create(self.device, ctypes.byref(h)))
         self.handle = h
@@ -70,6 +72,15 @@ class Context:
     def launches(self) -> int:
         return int(self.lib.vp_ctx_launch_count(self.handle))
 
+    def gemm_timing(self, enable: bool):
+        """Accumulated (ms, launches) per GEMM kind since the last call
+        (logits, logits_f32, dx, dw), then switches event timing on/off."""
+        ms = (ctypes.c_double * 4)()
+        n = (ctypes.c_int64 * 4)()
+        check(self.lib.vp_ctx_gemm_timing(self.handle, int(enable), ms, n))
+        names = ("logits", "logits_f32", "dx", "dw")
+        return {k: (ms[i], n[i]) for i, k in enumerate(names)}
+
     @staticmethod
     def unique_id() -> bytes:
         buf = ctypes.create_string_buffer(128)
@@ -87,6 +98,8 @@ class Context:
 
     def close(self) -> None:
         if getattr(self, "handle", None):
+            for st in list(self._states):
+                st.close()
             check(self.lib.vp_ctx_destroy(self.handle))
             self.handle = None
 
@@ -164,6 +177,7 @@ class ShardState:
         check(ctx.lib.vp_state_create(ctx.handle, self.n_tok, self.h, self.rows, ctypes.byref(hdl)))
         self.handle = hdl
         self.has_grad_terms = False
+        ctx._states.add(self)
 
     def local_stats(self) -> LocalStats:
         dev = torch.device("cuda", self.ctx.device)
@@ -196,9 +210,9 @@ class ShardState:
         return self.softmax(self.local_stats())
 
     def close(self) -> None:
-        if getattr(self, "handle", None):
+        if getattr(self, "handle", None) and getattr(self.ctx, "handle", None):
             check(self.ctx.lib.vp_state_destroy(self.handle))
-            self.handle = None
+        self.handle = None
 
     def __del__(self):
         try:
