@@ -86,7 +86,9 @@ void* vp_ctx_get_stream(vp_ctx_t ctx);
 int vp_ctx_sync(vp_ctx_t ctx);
 /* Pre-size the workspace for up to n_tok tokens, hidden h, p exchange parts. */
 int vp_ctx_reserve(vp_ctx_t ctx, int64_t n_tok, int64_t h, int p);
-/* Options: "cta_group" (1 or 2, default 2), "gemm_sms" (SMs used by GEMMs). */
+/* Options: "cta_group" (1 or 2, default 2), "gemm_sms" (SMs used by GEMMs),
+ * "raster_{logits,dx,dw}" (tile order, see GemmGeom::raster),
+ * "policy_{logits,dx,dw}" (TMA L2 policy: -1 default, 0 normal, 1 first, 2 last). */
 int vp_ctx_set_option(vp_ctx_t ctx, const char* key, int64_t value);
 /* Number of kernels this context has launched (evidence counter). */
 int64_t vp_ctx_launch_count(vp_ctx_t ctx);

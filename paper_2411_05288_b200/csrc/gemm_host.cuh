@@ -59,7 +59,8 @@ struct Operand {
 
 template <int CG, bool A_MN, bool B_MN, class Epi>
 inline void launch_gemm_t(const Operand& A, const Operand& B, int M, int N, int K, int raster,
-                          const typename Epi::Params& ep, int num_sms, cudaStream_t st) {
+                          const typename Epi::Params& ep, int num_sms, cudaStream_t st, int pol_a = -1,
+                          int pol_b = -1) {
   using C = GemmCfg<CG>;
   const CUtensorMap ta = A_MN ? make_tmap_bf16(A.ptr, uint64_t(M), uint64_t(K), uint64_t(A.ld), 64, 64)
                               : make_tmap_bf16(A.ptr, uint64_t(K), uint64_t(M), uint64_t(A.ld), 64, C::BM_CTA);
@@ -73,6 +74,8 @@ inline void launch_gemm_t(const Operand& A, const Operand& B, int M, int N, int 
   g.tiles_n = (N + C::BN - 1) / C::BN;
   g.num_kb = (K + C::BK - 1) / C::BK;
   g.raster = raster;
+  g.pol_a = pol_a;
+  g.pol_b = pol_b;
   auto kern = gemm_sm100_kernel<CG, A_MN, B_MN, Epi>;
   static bool attr_done = false;
   if (!attr_done) {
@@ -101,11 +104,12 @@ inline void launch_gemm_t(const Operand& A, const Operand& B, int M, int N, int 
 // Runtime dispatch over (cta_group, operand majors).
 template <class Epi>
 inline void launch_gemm(int cg, const Operand& A, const Operand& B, int M, int N, int K, int raster,
-                        const typename Epi::Params& ep, int num_sms, cudaStream_t st) {
-#define VP_GEMM_CASE(CGV, AM, BM_)                                                     \
-  if (cg == CGV && A.mn_major == AM && B.mn_major == BM_) {                            \
-    launch_gemm_t<CGV, AM, BM_, Epi>(A, B, M, N, K, raster, ep, num_sms, st);           \
-    return;                                                                            \
+                        const typename Epi::Params& ep, int num_sms, cudaStream_t st, int pol_a = -1,
+                        int pol_b = -1) {
+#define VP_GEMM_CASE(CGV, AM, BM_)                                                         \
+  if (cg == CGV && A.mn_major == AM && B.mn_major == BM_) {                                \
+    launch_gemm_t<CGV, AM, BM_, Epi>(A, B, M, N, K, raster, ep, num_sms, st, pol_a, pol_b); \
+    return;                                                                                \
   }
   VP_GEMM_CASE(2, false, false)
   VP_GEMM_CASE(2, false, true)

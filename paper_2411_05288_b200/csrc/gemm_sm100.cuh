@@ -36,7 +36,15 @@ struct GemmGeom {
   // n-tiles.  Picks which operand band stays L2-resident while the
   // concurrently running tiles sweep the other.
   int raster;
+  // L2 policies of the A / B TMA loads: 0 evict_normal, 1 evict_first,
+  // 2 evict_last, -1 = the epilogue's default (see Epi::kAStreams).
+  int pol_a = -1, pol_b = -1;
 };
+
+__device__ __forceinline__ uint64_t make_policy(int p, bool dflt_first) {
+  if (p < 0) p = dflt_first ? 1 : 2;
+  return p == 1 ? ptx::policy_evict_first() : p == 2 ? ptx::policy_evict_last() : ptx::policy_evict_normal();
+}
 
 template <int CG>
 struct GemmCfg {
@@ -120,8 +128,8 @@ __global__ void __launch_bounds__(256, 1)
 
   if (warp == 0 && lane == 0) {
     // ===== TMA producer =====
-    const uint64_t polA = Epi::kAStreams ? ptx::policy_evict_first() : ptx::policy_evict_last();
-    const uint64_t polB = Epi::kAStreams ? ptx::policy_evict_last() : ptx::policy_evict_first();
+    const uint64_t polA = make_policy(g.pol_a, Epi::kAStreams);
+    const uint64_t polB = make_policy(g.pol_b, !Epi::kAStreams);
     uint32_t it = 0;
     for (int t = cluster; t < num_tiles; t += nclusters) {
       int mb, nb;
@@ -275,25 +283,43 @@ struct EpiStoreF32 {
 
 // K1 fused stats epilogue (forward of the output layer).  For row i and
 // vocab tile j (256 columns of this shard):
-//   m_ij = max_v Y[i,v];  s_ij = sum_v exp(Y[i,v] - m_ij)
-//   P[i,v] = bf16(exp(Y[i,v] - m_ij))          (never the raw logits)
-//   y_tgt[i] = Y[i, g_i - row_begin]  when the label falls in this tile.
-// Full-vocab logits are never written to or re-read from HBM.
+//   m_ij = max_v Y[i,v];  y_tgt[i] = Y[i, g_i - row_begin] when the label falls here;
+//   P[i,v] = bf16(exp(Y[i,v] - q_ij)),  s_ij = sum_v exp(Y[i,v] - q_ij),
+// where the reference q_ij is ONE value per row, r_i = m_i0 (the max of the
+// row's first vocab tile), published by the j = 0 tiles (first wave) through
+// a release flag per 128-row block.  A per-row reference makes
+// softmax' = P * cfac_i (one factor per row), which the dX epilogue and the
+// scaled-X operand of dW absorb: no pass over P is needed after K1.
+// Tiles that run before r_i is published (part of the first wave) use their
+// own max (q_ij = m_ij) and log their 32-row group in fix_list; rows whose
+// logits exceed r_i + kMaxRefGap (exp would overflow) are marked in row_bad
+// and re-referenced to the row max after the stats merge.  Full-vocab
+// logits are never written to or re-read from HBM.
 struct EpiLogitStats {
   static constexpr bool kAStreams = false;  // A = X is reused by every vocab tile
+  static constexpr float kMaxRefGap = 64.f;
   struct Params {
     __nv_bfloat16* P;
     int64_t ldp;
-    float* tile_m;        // [tiles_n x ld_stats]
-    float* tile_s;        // [tiles_n x ld_stats]
+    float* tile_m;          // [tiles_n x ld_stats] tile max
+    float* tile_s;          // [tiles_n x ld_stats] exp-sum relative to tile_q
     int64_t ld_stats;
     const int64_t* labels;  // [M] global vocab ids (may be null)
     int64_t row_begin, row_end;
-    float* y_tgt;         // [M]
+    float* y_tgt;           // [M]
+    float* tile_q;          // [tiles_n x ld_stats] reference of P / s for (row, tile)
+    float* row_ref;         // [M] r_i
+    int* ref_flag;          // [ceil(M/128)] 1 once r of that 128-row block is visible
+    int* row_bad;           // [M]
+    int* bad_count;         // bad rows appended to bad_list (once each)
+    int* bad_list;          // [M]
+    int* fix_count;         // (32-row group, tile) pairs stored relative to their own max
+    int2* fix_list;         // [ceil(M/32) x tiles_n]
   };
   __device__ static void apply(const Params& p, const GemmGeom& g, uint32_t taddr, int row, int col0, int nb) {
     constexpr float kLog2e = 1.4426950408889634f;
     const bool row_ok = row < g.M;
+    const int lane = threadIdx.x & 31;
     const int nvalid = min(GemmCfg<1>::BN, g.N - col0);
     int lb = -1;
     if (row_ok && p.labels) {
@@ -320,7 +346,31 @@ struct EpiLogitStats {
         has_t = true;
       }
     }
-    const float mxs = mx * kLog2e;
+    // ---- choose the reference q for this (row, tile) ----
+    const int blk = row >> 7;
+    float ref = mx;
+    bool own = false, bad = false;
+    if (nb == 0) {
+      if (row_ok) p.row_ref[row] = mx;
+      asm volatile("bar.sync 1, 128;" ::: "memory");  // the 4 epilogue warps of this CTA
+      if (threadIdx.x == 128) {
+        __threadfence();
+        atomicExch(p.ref_flag + blk, 1);
+      }
+    } else {
+      int f;
+      asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(f) : "l"(p.ref_flag + blk) : "memory");
+      if (f) {
+        if (row_ok) {
+          const float r = p.row_ref[row];
+          if (mx - r > kMaxRefGap) bad = true;  // exp(y - r) could overflow: keep own max
+          else ref = r;
+        }
+      } else {
+        own = true;
+      }
+    }
+    const float refs = ref * kLog2e;
     float sum = 0.f;
     __nv_bfloat16* dst = p.P + int64_t(row) * p.ldp + col0;
     const bool vec = ((p.ldp & 7) == 0) && ((reinterpret_cast<uintptr_t>(p.P) & 15) == 0);
@@ -334,8 +384,8 @@ struct EpiLogitStats {
       uint32_t pk[16];
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
-        const float e0 = (2 * j < nv) ? ptx::ex2(fmaf(__uint_as_float(r[2 * j]), kLog2e, -mxs)) : 0.f;
-        const float e1 = (2 * j + 1 < nv) ? ptx::ex2(fmaf(__uint_as_float(r[2 * j + 1]), kLog2e, -mxs)) : 0.f;
+        const float e0 = (2 * j < nv) ? ptx::ex2(fmaf(__uint_as_float(r[2 * j]), kLog2e, -refs)) : 0.f;
+        const float e1 = (2 * j + 1 < nv) ? ptx::ex2(fmaf(__uint_as_float(r[2 * j + 1]), kLog2e, -refs)) : 0.f;
         sum += e0 + e1;
         pk[j] = ptx::pack_bf16(e0, e1);
       }
@@ -353,10 +403,15 @@ struct EpiLogitStats {
       }
     }
     if (row_ok) {
-      p.tile_m[int64_t(nb) * p.ld_stats + row] = mx;
-      p.tile_s[int64_t(nb) * p.ld_stats + row] = sum;
+      const int64_t o = int64_t(nb) * p.ld_stats + row;
+      p.tile_m[o] = mx;
+      p.tile_s[o] = sum;
+      p.tile_q[o] = ref;
       if (has_t) p.y_tgt[row] = yt;
+      if (bad && atomicExch(p.row_bad + row, 1) == 0) p.bad_list[atomicAdd(p.bad_count, 1)] = row;
     }
+    if (__ballot_sync(0xffffffffu, own && row_ok) && lane == 0)
+      p.fix_list[atomicAdd(p.fix_count, 1)] = make_int2(row >> 5, nb);
   }
 };
 

@@ -98,6 +98,10 @@ struct vp_ctx_s {
   int num_sms = 148;
   int gemm_sms = 148;
   int cg = 2;
+  // GEMM tile rasterisation and TMA L2 policy per GEMM [logits, dX, dW]
+  // (measured: evict_normal on both operands beats first/last hints)
+  int raster[3] = {0, 16, 0};
+  int pol[3] = {0, 0, 0};
   ncclComm_t comm = nullptr;
   int nranks = 1, rank = 0;
   int* d_err = nullptr;
@@ -133,6 +137,11 @@ struct vp_state_s {
   int64_t n_tok = 0, h = 0, rows = 0, ldp = 0, ntiles = 0;
   __nv_bfloat16* P = nullptr;
   float *tile_m = nullptr, *tile_s = nullptr, *m_loc = nullptr, *s_loc = nullptr, *ytgt = nullptr;
+  // per-row reference machinery of the K1 epilogue (see EpiLogitStats)
+  float *tile_q = nullptr, *row_ref = nullptr, *cfac = nullptr;
+  int *ref_flag = nullptr, *row_bad = nullptr, *bad_list = nullptr, *counters = nullptr;  // counters: bad, fix
+  int2* fix_list = nullptr;
+  int64_t nblk128 = 0;
   float* A = nullptr;  // [n_tok x h] fp32: alg2 A, or per-shard dX partial (alg1/naive local mode)
   float* Y = nullptr;  // naive only: fp32 logits [n_tok x rows]
   int form = kRaw;
@@ -141,6 +150,16 @@ struct vp_state_s {
 };
 
 namespace {
+
+void free_state_buffers(vp_state_s* st) {
+  for (void* p : {static_cast<void*>(st->P), static_cast<void*>(st->tile_m), static_cast<void*>(st->tile_s),
+                  static_cast<void*>(st->m_loc), static_cast<void*>(st->s_loc), static_cast<void*>(st->ytgt),
+                  static_cast<void*>(st->A), static_cast<void*>(st->Y), static_cast<void*>(st->tile_q),
+                  static_cast<void*>(st->row_ref), static_cast<void*>(st->cfac), static_cast<void*>(st->ref_flag),
+                  static_cast<void*>(st->row_bad), static_cast<void*>(st->bad_list),
+                  static_cast<void*>(st->counters), static_cast<void*>(st->fix_list)})
+    if (p) cudaFree(p);
+}
 
 void check_batch(const vp_batch_t* b, bool need_labels = true) {
   require(b != nullptr && b->X != nullptr, "TokenBatch: null batch");
@@ -190,11 +209,17 @@ void timed_gemm(vp_ctx_s* c, int kind, F&& launch) {
 
 // ---- GEMM wrappers ---------------------------------------------------------
 void gemm_logits(vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* s, vp_state_s* st) {
-  vp::EpiLogitStats::Params ep{st->P, st->ldp, st->tile_m, st->tile_s, st->n_tok, b->labels, s->row_begin,
-                               s->row_end, st->ytgt};
+  VP_CUDA(cudaMemsetAsync(st->ref_flag, 0, size_t(st->nblk128) * sizeof(int), c->stream));
+  VP_CUDA(cudaMemsetAsync(st->row_bad, 0, size_t(st->n_tok) * sizeof(int), c->stream));
+  VP_CUDA(cudaMemsetAsync(st->counters, 0, 2 * sizeof(int), c->stream));
+  vp::EpiLogitStats::Params ep{st->P,       st->ldp,      st->tile_m,   st->tile_s,       st->n_tok,
+                               b->labels,   s->row_begin, s->row_end,   st->ytgt,         st->tile_q,
+                               st->row_ref, st->ref_flag, st->row_bad,  st->counters,     st->bad_list,
+                               st->counters + 1, st->fix_list};
   timed_gemm(c, 0, [&] {
     vp::launch_gemm<vp::EpiLogitStats>(c->cg, {b->X, b->ldx, false}, {s->W, s->ldw, false}, int(b->n_tok),
-                                       int(st->rows), int(b->h), 0, ep, c->gemm_sms, c->stream);
+                                       int(st->rows), int(b->h), c->raster[0], ep, c->gemm_sms, c->stream,
+                                       c->pol[0], c->pol[0]);
   });
   ++c->launches;
 }
@@ -203,7 +228,8 @@ void gemm_logits_f32(vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* s, vp_s
   vp::EpiStoreF32::Params ep{st->Y, st->rows, st->tile_m, st->n_tok, nullptr};
   timed_gemm(c, 1, [&] {
     vp::launch_gemm<vp::EpiStoreF32>(c->cg, {b->X, b->ldx, false}, {s->W, s->ldw, false}, int(b->n_tok),
-                                     int(st->rows), int(b->h), 0, ep, c->gemm_sms, c->stream);
+                                     int(st->rows), int(b->h), c->raster[0], ep, c->gemm_sms, c->stream, c->pol[0],
+                                     c->pol[0]);
   });
   ++c->launches;
 }
@@ -214,7 +240,8 @@ void gemm_dx(vp_ctx_s* c, vp_state_s* st, const vp_shard_t* s, float* out, int64
   vp::EpiStoreF32::Params ep{out, ldo, nullptr, 0, row_scale};
   timed_gemm(c, 2, [&] {
     vp::launch_gemm<vp::EpiStoreF32>(c->cg, {st->P, st->ldp, false}, {s->W, s->ldw, true}, int(st->n_tok),
-                                     int(st->h), int(st->rows), 8, ep, c->gemm_sms, c->stream);
+                                     int(st->h), int(st->rows), c->raster[1], ep, c->gemm_sms, c->stream, c->pol[1],
+                                     c->pol[1]);
   });
   ++c->launches;
 }
@@ -223,9 +250,10 @@ void gemm_dx(vp_ctx_s* c, vp_state_s* st, const vp_shard_t* s, float* out, int64
 void gemm_dw(vp_ctx_s* c, vp_state_s* st, const void* Xop, int64_t ldx, float* out, int64_t ldo) {
   vp::EpiStoreF32::Params ep{out, ldo, nullptr, 0, nullptr};
   const int tiles_n = int(ceil_div(st->h, 256));
+  const int raster = c->raster[2] == 0 ? -tiles_n : c->raster[2];
   timed_gemm(c, 3, [&] {
     vp::launch_gemm<vp::EpiStoreF32>(c->cg, {st->P, st->ldp, true}, {Xop, ldx, true}, int(st->rows), int(st->h),
-                                     int(st->n_tok), -tiles_n, ep, c->gemm_sms, c->stream);
+                                     int(st->n_tok), raster, ep, c->gemm_sms, c->stream, c->pol[2], c->pol[2]);
   });
   ++c->launches;
 }
@@ -255,10 +283,12 @@ float* inv_of(vp_ctx_s* c, const float* s, int64_t n) {
   return inv;
 }
 
+// c_i = global_scale (VM.cpp:22-27) times cfac_i: the per-row factor that
+// turns the state's stored P into the global softmax.
 float* global_scale(vp_ctx_s* c, const vp_state_s* st, vp_stats_t g) {
   float* sc = c->buf<float>(c->scale, size_t(st->n_tok));
-  vp::k_global_scale<<<unsigned(ceil_div(st->n_tok, 256)), 256, 0, c->stream>>>(st->m_loc, st->s_loc, g.m, g.sum,
-                                                                                int(st->n_tok), sc);
+  vp::k_global_scale<<<unsigned(ceil_div(st->n_tok, 256)), 256, 0, c->stream>>>(
+      st->m_loc, st->s_loc, g.m, g.sum, st->form == kLocal ? st->cfac : nullptr, int(st->n_tok), sc);
   VP_KCHECK();
   ++c->launches;
   return sc;
@@ -315,16 +345,31 @@ void pass_S_common(vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* s, vp_sta
   check_shard(s, b->h);
   check_state(st, b, s);
   gemm_logits(c, b, s, st);
-  stats_reduce(c, st, true);
-  rescale_P(c, st, st->tile_m, st->m_loc, inv_of(c, st->s_loc, st->n_tok));
-  st->form = kLocal;
+  const int T = int(st->n_tok);
+  const int fix_grid = c->num_sms;
+  vp::k_fix_check<<<fix_grid, 256, 0, c->stream>>>(st->fix_list, st->counters + 1, st->tile_q, st->n_tok, T,
+                                                   st->row_ref, vp::EpiLogitStats::kMaxRefGap, st->row_bad,
+                                                   st->counters, st->bad_list);
+  VP_KCHECK();
+  vp::k_stats_reduce_ref<<<unsigned(ceil_div(T, 32)), 256, 0, c->stream>>>(
+      st->tile_m, st->tile_s, st->tile_q, int(st->ntiles), st->n_tok, T, st->row_ref, st->row_bad, st->m_loc,
+      st->s_loc, st->cfac);
+  VP_KCHECK();
+  vp::k_fix_apply<<<fix_grid, 256, 0, c->stream>>>(st->fix_list, st->counters + 1, st->P, st->ldp, int(st->rows),
+                                                   st->tile_q, st->n_tok, T, st->row_ref, st->row_bad);
+  VP_KCHECK();
+  vp::k_fix_bad<<<fix_grid, 256, 0, c->stream>>>(st->bad_list, st->counters, st->P, st->ldp, int(st->rows),
+                                                 st->tile_q, st->n_tok, st->m_loc);
+  VP_KCHECK();
+  c->launches += 4;
+  st->form = kLocal;  // softmax' = P * cfac (per row)
   st->has_grad_terms = false;
   st->has_S = true;
 }
 
 void alg2_S(vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* s, vp_state_s* st) {
   pass_S_common(c, b, s, st);
-  gemm_dx(c, st, s, st->A, st->h);  // A = softmax' W_k (VM.cpp:183)
+  gemm_dx(c, st, s, st->A, st->h, st->cfac);  // A = softmax' W_k = diag(cfac) P W_k (VM.cpp:183)
   st->has_grad_terms = true;
 }
 
@@ -689,6 +734,15 @@ int vp_ctx_set_option(vp_ctx_t c, const char* key, int64_t value) {
     if (k == "cta_group") {
       require(value == 1 || value == 2, "vp_ctx_set_option: cta_group must be 1 or 2");
       c->cg = int(value);
+    } else if (k.rfind("raster_", 0) == 0 || k.rfind("policy_", 0) == 0) {
+      const std::string which = k.substr(7);
+      const int idx = which == "logits" ? 0 : which == "dx" ? 1 : which == "dw" ? 2 : -1;
+      require(idx >= 0, "vp_ctx_set_option: raster_/policy_ suffix must be logits, dx or dw");
+      if (k[0] == 'r') c->raster[idx] = int(value);
+      else {
+        require(value >= -1 && value <= 2, "vp_ctx_set_option: policy must be -1..2");
+        c->pol[idx] = int(value);
+      }
     } else if (k == "gemm_sms") {
       require(value >= 2 && value <= c->num_sms, "vp_ctx_set_option: gemm_sms out of range");
       c->gemm_sms = int(value);
@@ -778,12 +832,18 @@ int vp_state_create(vp_ctx_t c, int64_t n_tok, int64_t h, int64_t rows, vp_state
       VP_CUDA(cudaMalloc(&st->s_loc, size_t(n_tok) * sizeof(float)));
       VP_CUDA(cudaMalloc(&st->ytgt, size_t(n_tok) * sizeof(float)));
       VP_CUDA(cudaMalloc(&st->A, size_t(n_tok * h) * sizeof(float)));
+      st->nblk128 = ceil_div(n_tok, 128) + 2;
+      VP_CUDA(cudaMalloc(&st->tile_q, size_t(st->ntiles * n_tok) * sizeof(float)));
+      VP_CUDA(cudaMalloc(&st->row_ref, size_t(n_tok) * sizeof(float)));
+      VP_CUDA(cudaMalloc(&st->cfac, size_t(n_tok) * sizeof(float)));
+      VP_CUDA(cudaMalloc(&st->ref_flag, size_t(st->nblk128) * sizeof(int)));
+      VP_CUDA(cudaMalloc(&st->row_bad, size_t(n_tok) * sizeof(int)));
+      VP_CUDA(cudaMalloc(&st->bad_list, size_t(n_tok) * sizeof(int)));
+      VP_CUDA(cudaMalloc(&st->counters, 2 * sizeof(int)));
+      VP_CUDA(cudaMalloc(&st->fix_list, size_t(ceil_div(n_tok, 32) * st->ntiles) * sizeof(int2)));
       VP_CUDA(cudaMemset(st->ytgt, 0, size_t(n_tok) * sizeof(float)));
     } catch (...) {
-      for (void* p : {static_cast<void*>(st->P), static_cast<void*>(st->tile_m), static_cast<void*>(st->tile_s),
-                      static_cast<void*>(st->m_loc), static_cast<void*>(st->s_loc), static_cast<void*>(st->ytgt),
-                      static_cast<void*>(st->A)})
-        if (p) cudaFree(p);
+      free_state_buffers(st);
       delete st;
       throw;
     }
@@ -796,10 +856,7 @@ int vp_state_destroy(vp_state_t st) {
     if (!st) return;
     st->ctx->activate();
     cudaStreamSynchronize(st->ctx->stream);
-    for (void* p : {static_cast<void*>(st->P), static_cast<void*>(st->tile_m), static_cast<void*>(st->tile_s),
-                    static_cast<void*>(st->m_loc), static_cast<void*>(st->s_loc), static_cast<void*>(st->ytgt),
-                    static_cast<void*>(st->A), static_cast<void*>(st->Y)})
-      if (p) cudaFree(p);
+    free_state_buffers(st);
     delete st;
   });
 }

@@ -63,6 +63,119 @@ __global__ void k_stats_reduce(const float* __restrict__ tile_m, const float* __
   }
 }
 
+// Per-row merge of the K1 tile stats when each tile's exp-sum s_ij is
+// relative to its own reference q_ij (see EpiLogitStats):
+//   m' = max_j m_ij,  s' = sum_j s_ij e^{q_ij - m'}      (tiles in ascending j)
+// and the per-row factor that turns the stored P into softmax':
+//   cfac_i = e^{ref_i - m'_i} / s'_i,  ref_i = row_bad ? m'_i : r_i.
+__global__ void k_stats_reduce_ref(const float* __restrict__ tile_m, const float* __restrict__ tile_s,
+                                   const float* __restrict__ tile_q, int ntiles, int64_t ld, int n,
+                                   const float* __restrict__ row_ref, const int* __restrict__ row_bad,
+                                   float* __restrict__ m_out, float* __restrict__ s_out, float* __restrict__ cfac) {
+  __shared__ float sm[8][32], ss[8][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int row = blockIdx.x * 32 + lane;
+  float m = -INFINITY, s = 0.f;
+  if (row < n) {
+    for (int j = w; j < ntiles; j += 8) {
+      const int64_t o = int64_t(j) * ld + row;
+      const float mj = tile_m[o];
+      const float sj = tile_s[o] * fast_exp(tile_q[o] - mj);  // relative to the tile max
+      const float nm = fmaxf(m, mj);
+      s = s * fast_exp(m - nm) + sj * fast_exp(mj - nm);
+      m = nm;
+    }
+  }
+  sm[w][lane] = m;
+  ss[w][lane] = s;
+  __syncthreads();
+  if (w == 0 && row < n) {
+    float M = sm[0][lane], S = ss[0][lane];
+    for (int q = 1; q < 8; ++q) {
+      const float mq = sm[q][lane];
+      if (mq == -INFINITY) continue;
+      const float nm = fmaxf(M, mq);
+      S = S * fast_exp(M - nm) + ss[q][lane] * fast_exp(mq - nm);
+      M = nm;
+    }
+    m_out[row] = M;
+    s_out[row] = S;
+    const float ref = row_bad[row] ? M : row_ref[row];
+    cfac[row] = expf(ref - M) / S;
+  }
+}
+
+// Fixup 1/3: a tile stored against its own max (ran before r_i was
+// published) whose max exceeds r_i + gap cannot be re-referenced to r_i:
+// its row joins the bad rows (re-referenced to the row max instead).
+__global__ void k_fix_check(const int2* __restrict__ fix_list, const int* __restrict__ fix_count,
+                            const float* __restrict__ tile_q, int64_t ld, int n, const float* __restrict__ row_ref,
+                            float gap, int* __restrict__ row_bad, int* __restrict__ bad_count,
+                            int* __restrict__ bad_list) {
+  const int cnt = *fix_count;
+  const int lane = threadIdx.x & 31;
+  for (int e = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); e < cnt; e += gridDim.x * (blockDim.x >> 5)) {
+    const int2 f = fix_list[e];
+    const int row = f.x * 32 + lane;
+    if (row >= n) continue;
+    if (tile_q[int64_t(f.y) * ld + row] - row_ref[row] > gap && atomicExch(row_bad + row, 1) == 0)
+      bad_list[atomicAdd(bad_count, 1)] = row;
+  }
+}
+
+// Rescale P[row, tile j] by e^{q - ref} (8 bf16 per thread-step).
+__device__ __forceinline__ void rescale_segment(__nv_bfloat16* p, int cols, float f, int t0, int tstep) {
+  for (int v = t0 * 8; v < cols; v += tstep * 8) {
+    if (v + 8 <= cols) {
+      uint4 u = *reinterpret_cast<uint4*>(p + v);
+      __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        float2 x = __bfloat1622float2(h2[q]);
+        h2[q] = __floats2bfloat162_rn(x.x * f, x.y * f);
+      }
+      *reinterpret_cast<uint4*>(p + v) = u;
+    } else {
+      for (int q = v; q < cols; ++q) p[q] = __float2bfloat16(__bfloat162float(p[q]) * f);
+    }
+  }
+}
+
+// Fixup 2/3: listed (32-row group, tile) pairs of good rows -> reference r_i.
+__global__ void k_fix_apply(const int2* __restrict__ fix_list, const int* __restrict__ fix_count,
+                            __nv_bfloat16* __restrict__ P, int64_t ldp, int cols, const float* __restrict__ tile_q,
+                            int64_t ld, int n, const float* __restrict__ row_ref, const int* __restrict__ row_bad) {
+  const int cnt = *fix_count;
+  for (int e = blockIdx.x; e < cnt; e += gridDim.x) {
+    const int2 f = fix_list[e];
+    const int c0 = f.y * kTileN, cw = min(kTileN, cols - c0);
+    for (int rr = threadIdx.x >> 5; rr < 32; rr += blockDim.x >> 5) {
+      const int row = f.x * 32 + rr;
+      if (row >= n || row_bad[row]) continue;
+      const float fac = fast_exp(tile_q[int64_t(f.y) * ld + row] - row_ref[row]);
+      rescale_segment(P + int64_t(row) * ldp + c0, cw, fac, threadIdx.x & 31, 32);
+    }
+  }
+}
+
+// Fixup 3/3: bad rows -> every tile re-referenced to the row max m'.
+__global__ void k_fix_bad(const int* __restrict__ bad_list, const int* __restrict__ bad_count,
+                          __nv_bfloat16* __restrict__ P, int64_t ldp, int cols, const float* __restrict__ tile_q,
+                          int64_t ld, const float* __restrict__ m_row) {
+  const int cnt = *bad_count;
+  const int ntiles = (cols + kTileN - 1) / kTileN;
+  for (int e = blockIdx.x; e < cnt; e += gridDim.x) {
+    const int row = bad_list[e];
+    for (int j = threadIdx.x >> 5; j < ntiles; j += blockDim.x >> 5) {
+      const float q = tile_q[int64_t(j) * ld + row];
+      if (q == m_row[row]) continue;
+      const int c0 = j * kTileN;
+      rescale_segment(P + int64_t(row) * ldp + c0, min(kTileN, cols - c0), fast_exp(q - m_row[row]),
+                      threadIdx.x & 31, 32);
+    }
+  }
+}
+
 // merge_max_sum (VM.cpp:82-101) over p parts laid out [p x n]: m starts at
 // part 0 and takes the max in k order; sum accumulates sum_k e^{m_k - m} in
 // k order; then sum *= fault_scale (VM.cpp:314).
@@ -146,12 +259,13 @@ __global__ void k_inv(const float* __restrict__ s, int n, float* __restrict__ in
   if (i < n) inv[i] = 1.f / s[i];
 }
 
-// global_scale (VM.cpp:22-27): c_i = sum'_i e^{m'_i - m_i} / sum_i
+// global_scale (VM.cpp:22-27): c_i = sum'_i e^{m'_i - m_i} / sum_i, times the
+// per-row factor cfac_i that maps the stored P to softmax' (null: 1).
 __global__ void k_global_scale(const float* __restrict__ ml, const float* __restrict__ sl,
-                               const float* __restrict__ mg, const float* __restrict__ sg, int n,
-                               float* __restrict__ c) {
+                               const float* __restrict__ mg, const float* __restrict__ sg,
+                               const float* __restrict__ cfac, int n, float* __restrict__ c) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) c[i] = sl[i] * expf(ml[i] - mg[i]) / sg[i];
+  if (i < n) c[i] = sl[i] * expf(ml[i] - mg[i]) / sg[i] * (cfac ? cfac[i] : 1.f);
 }
 
 // ---------------------------------------------------------------------------

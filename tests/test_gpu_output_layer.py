@@ -223,3 +223,25 @@ def test_headline_shape_properties_and_sampled_rows(ctx):
     gx_ref = G @ W.double()
     err = (out.grad_x[rows].double() - gx_ref).norm() / gx_ref.norm()
     assert err.item() <= GRAD_REL_L2
+
+
+def test_extreme_logit_gap_takes_the_overflow_path(ctx):
+    # a row whose first vocab tile is ~0 while a later column is 100 nats
+    # higher: exp(y - r_i) would overflow, so the row is re-referenced to its
+    # max (EpiLogitStats kMaxRefGap path); results must still match the oracle
+    T, h, V = 64, 64, 1024
+    rng = np.random.default_rng(5)
+    X = rng.standard_normal((T, h)) * 0.1
+    W = rng.standard_normal((V, h)) * 0.01
+    X[3, :] = 1.0
+    W[700, :] = 100.0 / h      # logit(3, 700) ~ 100, tile 0 of row 3 ~ 0
+    W[900, :] = -100.0 / h
+    X[7, :] = -1.0             # row 7: column 900 is the outlier
+    g = rng.integers(0, V, T)
+    g[3], g[7] = 5, 900
+    Xb, Wb, batch, Wd = device_case(X, W, g)
+    ref = oracle.oracle_output_layer(Xb, g, Wb)
+    for alg in ALGS:
+        for p in (1, 2):
+            res, _ = run_device(ctx, alg, batch, Wd, p, h)
+            assert_parity(res, ref, f"gap {alg} p={p}")

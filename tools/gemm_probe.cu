@@ -1,0 +1,95 @@
+// Developer probe: one vocab GEMM at the headline shape (T=8192, h=4096,
+// V=256000 by default) with a chosen tile rasterisation and L2 policies.
+//   gemm_probe <k1|dx|dw> <raster> <pol_a> <pol_b> [iters] [V]
+// pol: -1 default, 0 normal, 1 evict_first, 2 evict_last.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <string>
+
+#include "../paper_2411_05288_b200/csrc/gemm_host.cuh"
+
+#define CK(x)                                                                             \
+  do {                                                                                    \
+    cudaError_t e_ = (x);                                                                 \
+    if (e_ != cudaSuccess) {                                                              \
+      fprintf(stderr, "CUDA %s at %s:%d\n", cudaGetErrorString(e_), __FILE__, __LINE__); \
+      exit(2);                                                                            \
+    }                                                                                     \
+  } while (0)
+
+// N(0, s^2) via Box-Muller on hashed uniforms (power draw depends on the data)
+__device__ __forceinline__ uint32_t hash32(uint64_t x) {
+  x ^= x >> 33;
+  x *= 0xff51afd7ed558ccdull;
+  x ^= x >> 33;
+  x *= 0xc4ceb9fe1a85ec53ull;
+  x ^= x >> 33;
+  return uint32_t(x);
+}
+__global__ void fill(__nv_bfloat16* p, int64_t n, float s, uint64_t seed) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    const float u1 = (hash32(seed * 0x9E3779B97F4A7C15ull + 2 * i) + 1.f) * 2.3283064e-10f;
+    const float u2 = hash32(seed * 0x9E3779B97F4A7C15ull + 2 * i + 1) * 2.3283064e-10f;
+    p[i] = __float2bfloat16(s * sqrtf(-2.f * logf(u1)) * cospif(2.f * u2));
+  }
+}
+
+int main(int argc, char** argv) {
+  if (argc < 5) {
+    fprintf(stderr, "usage: gemm_probe <k1|dx|dw> <raster> <pol_a> <pol_b> [iters] [V]\n");
+    return 2;
+  }
+  const std::string kind = argv[1];
+  const int raster = atoi(argv[2]), pa = atoi(argv[3]), pb = atoi(argv[4]);
+  const int iters = argc > 5 ? atoi(argv[5]) : 10;
+  const int64_t T = 8192, h = 4096, V = argc > 6 ? atoll(argv[6]) : 256000;
+  int nsm = 0;
+  CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0));
+  __nv_bfloat16 *X, *W, *P;
+  float* out;
+  CK(cudaMalloc(&X, T * h * 2));
+  CK(cudaMalloc(&W, V * h * 2));
+  CK(cudaMalloc(&P, T * V * 2));
+  fill<<<1024, 256>>>(X, T * h, 1.f, 1);
+  fill<<<1024, 256>>>(W, V * h, 0.02f, 2);
+  fill<<<1024, 256>>>(P, T * V, 4e-6f, 3);  // softmax-like magnitudes
+  const int ntiles = int((V + 255) / 256);
+  float *tm, *ts, *yt;
+  CK(cudaMalloc(&tm, int64_t(ntiles) * T * 4));
+  CK(cudaMalloc(&ts, int64_t(ntiles) * T * 4));
+  CK(cudaMalloc(&yt, T * 4));
+  const int64_t out_elems = kind == "dw" ? V * h : T * h;
+  CK(cudaMalloc(&out, out_elems * 4));
+  auto run = [&] {
+    if (kind == "k1") {
+      vp::EpiLogitStats::Params ep{P, V, tm, ts, T, nullptr, 0, V, yt};
+      vp::launch_gemm<vp::EpiLogitStats>(2, {X, h, false}, {W, h, false}, int(T), int(V), int(h), raster, ep, nsm, 0,
+                                         pa, pb);
+    } else if (kind == "dx") {
+      vp::EpiStoreF32::Params ep{out, h, nullptr, 0, nullptr};
+      vp::launch_gemm<vp::EpiStoreF32>(2, {P, V, false}, {W, h, true}, int(T), int(h), int(V), raster, ep, nsm, 0, pa,
+                                       pb);
+    } else {
+      vp::EpiStoreF32::Params ep{out, h, nullptr, 0, nullptr};
+      vp::launch_gemm<vp::EpiStoreF32>(2, {P, V, true}, {X, h, true}, int(V), int(h), int(T), raster, ep, nsm, 0, pa,
+                                       pb);
+    }
+  };
+  run();
+  CK(cudaDeviceSynchronize());
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  cudaEventRecord(a);
+  for (int i = 0; i < iters; ++i) run();
+  cudaEventRecord(b);
+  CK(cudaEventSynchronize(b));
+  float ms;
+  cudaEventElapsedTime(&ms, a, b);
+  ms /= iters;
+  printf("probe %s raster=%d pol_a=%d pol_b=%d V=%lld: %.3f ms %.1f TFLOP/s\n", kind.c_str(), raster, pa, pb,
+         (long long)V, ms, 2.0 * T * h * double(V) / ms / 1e9);
+  return 0;
+}
