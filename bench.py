@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-tokens", type=int, default=64)
     ap.add_argument("--cpu-sample-vocab", type=int, default=64000)
+    ap.add_argument("--opt", action="append", default=[],
+                    help="library option key=value (vp_ctx_set_option), e.g. raster_dx=16")
     return ap.parse_args()
 
 
@@ -215,6 +217,9 @@ def run_ours(args):
         raise SystemExit("vocab must divide by the number of GPUs (pad_vocab_size)")
     rows = V // world
     ctx = vm.Context(local, cta_group=args.cta_group)
+    for kv in args.opt:
+        k, v = kv.split("=")
+        ctx.set_option(k, int(v))
     if world > 1:
         uid = [vm.Context.unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
@@ -343,7 +348,7 @@ def run_ours(args):
             "naive": "naive 3-barrier"}[args.alg]),
             "alg": args.alg, "tokens": T, "hidden": h, "vocab": V, "vocab_rows_per_gpu": rows,
             "parallelism": f"vocab{world}", "operands": "bf16", "accum_and_stats": "fp32",
-            "cta_group": args.cta_group,
+            "cta_group": args.cta_group, "options": args.opt,
             "l2": "inputs larger than L2 every step (W_k %.0f MB, P %.0f MB per GPU)" % (
                 rows * h * 2 / 1e6, T * rows * 2 / 1e6)},
         "e2e": e2e, "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu,

@@ -57,15 +57,17 @@ struct Operand {
   bool mn_major;
 };
 
-template <int CG, bool A_MN, bool B_MN, class Epi>
+template <int CG, bool A_MN, bool B_MN, class Epi, int MC = 1>
 inline void launch_gemm_t(const Operand& A, const Operand& B, int M, int N, int K, int raster,
                           const typename Epi::Params& ep, int num_sms, cudaStream_t st, int pol_a = -1,
                           int pol_b = -1) {
   using C = GemmCfg<CG>;
   const CUtensorMap ta = A_MN ? make_tmap_bf16(A.ptr, uint64_t(M), uint64_t(K), uint64_t(A.ld), 64, 64)
                               : make_tmap_bf16(A.ptr, uint64_t(K), uint64_t(M), uint64_t(A.ld), 64, C::BM_CTA);
+  // with multicast each CTA loads half of its B block (64 rows / one 64-col chunk)
   const CUtensorMap tb = B_MN ? make_tmap_bf16(B.ptr, uint64_t(N), uint64_t(K), uint64_t(B.ld), 64, 64)
-                              : make_tmap_bf16(B.ptr, uint64_t(K), uint64_t(N), uint64_t(B.ld), 64, C::B_ROWS);
+                              : make_tmap_bf16(B.ptr, uint64_t(K), uint64_t(N), uint64_t(B.ld), 64,
+                                               MC == 2 ? 64 : C::B_ROWS);
   GemmGeom g;
   g.M = M;
   g.N = N;
@@ -76,23 +78,47 @@ inline void launch_gemm_t(const Operand& A, const Operand& B, int M, int N, int 
   g.raster = raster;
   g.pol_a = pol_a;
   g.pol_b = pol_b;
-  auto kern = gemm_sm100_kernel<CG, A_MN, B_MN, Epi>;
+  auto kern = gemm_sm100_kernel<CG, A_MN, B_MN, Epi, MC>;
   static bool attr_done = false;
   if (!attr_done) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
     if (e != cudaSuccess) throw std::runtime_error(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
     attr_done = true;
   }
-  const int tiles = g.tiles_m * g.tiles_n;
-  const int clusters = tiles < num_sms / CG ? tiles : num_sms / CG;
+  constexpr int CL = CG * MC;
+  const int tiles = ((g.tiles_m + MC - 1) / MC) * g.tiles_n;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(unsigned(clusters * CG), 1, 1);
+  // persistent grid: no more clusters than can be co-resident (clusters of 4
+  // cannot tile all 148 SMs: GPC packing leaves some idle)
+  static int max_active = -1;
+  if (max_active < 0) {
+    cudaLaunchConfig_t q = {};
+    q.gridDim = dim3(unsigned(num_sms / CL * CL), 1, 1);
+    q.blockDim = dim3(C::THREADS, 1, 1);
+    q.dynamicSmemBytes = C::SMEM_BYTES;
+    cudaLaunchAttribute qa[1];
+    qa[0].id = cudaLaunchAttributeClusterDimension;
+    qa[0].val.clusterDim.x = CL;
+    qa[0].val.clusterDim.y = 1;
+    qa[0].val.clusterDim.z = 1;
+    q.attrs = qa;
+    q.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, kern, &q) != cudaSuccess || n <= 0) {
+      (void)cudaGetLastError();
+      n = num_sms / CL;
+    }
+    max_active = n;
+  }
+  int cap = num_sms / CL < max_active ? num_sms / CL : max_active;
+  const int clusters = tiles < cap ? tiles : cap;
+  cfg.gridDim = dim3(unsigned(clusters * CL), 1, 1);
   cfg.blockDim = dim3(C::THREADS, 1, 1);
   cfg.dynamicSmemBytes = C::SMEM_BYTES;
   cfg.stream = st;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = CG;
+  at[0].val.clusterDim.x = CL;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
@@ -105,18 +131,21 @@ inline void launch_gemm_t(const Operand& A, const Operand& B, int M, int N, int 
 template <class Epi>
 inline void launch_gemm(int cg, const Operand& A, const Operand& B, int M, int N, int K, int raster,
                         const typename Epi::Params& ep, int num_sms, cudaStream_t st, int pol_a = -1,
-                        int pol_b = -1) {
-#define VP_GEMM_CASE(CGV, AM, BM_)                                                         \
-  if (cg == CGV && A.mn_major == AM && B.mn_major == BM_) {                                \
-    launch_gemm_t<CGV, AM, BM_, Epi>(A, B, M, N, K, raster, ep, num_sms, st, pol_a, pol_b); \
-    return;                                                                                \
+                        int pol_b = -1, int mc = 1) {
+#define VP_GEMM_CASE(CGV, AM, BM_, MCV)                                                             \
+  if (cg == CGV && A.mn_major == AM && B.mn_major == BM_ && mc == MCV) {                            \
+    launch_gemm_t<CGV, AM, BM_, Epi, MCV>(A, B, M, N, K, raster, ep, num_sms, st, pol_a, pol_b);     \
+    return;                                                                                         \
   }
-  VP_GEMM_CASE(2, false, false)
-  VP_GEMM_CASE(2, false, true)
-  VP_GEMM_CASE(2, true, true)
-  VP_GEMM_CASE(1, false, false)
-  VP_GEMM_CASE(1, false, true)
-  VP_GEMM_CASE(1, true, true)
+  VP_GEMM_CASE(2, false, false, 2)
+  VP_GEMM_CASE(2, false, true, 2)
+  VP_GEMM_CASE(2, true, true, 2)
+  VP_GEMM_CASE(2, false, false, 1)
+  VP_GEMM_CASE(2, false, true, 1)
+  VP_GEMM_CASE(2, true, true, 1)
+  VP_GEMM_CASE(1, false, false, 1)
+  VP_GEMM_CASE(1, false, true, 1)
+  VP_GEMM_CASE(1, true, true, 1)
 #undef VP_GEMM_CASE
   throw std::invalid_argument("launch_gemm: unsupported operand layout combination");
 }

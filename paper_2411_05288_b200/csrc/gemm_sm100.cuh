@@ -84,11 +84,19 @@ __device__ __forceinline__ void tile_coords(const GemmGeom& g, int t, int& mb, i
   }
 }
 
-template <int CG, bool A_MN, bool B_MN, class Epi>
+// MC = CTA pairs per cluster along M (CG == 2 only).  MC == 2: a 4-CTA
+// cluster computes a 512 x 256 "cluster tile" as two pair tiles (m, n) and
+// (m+1, n) that need the same B rows; each CTA loads HALF of its B rows and
+// multicasts them to its counterpart in the other pair, halving B's L2
+// traffic.  A stage may then be refilled only after BOTH pairs consumed it,
+// so every empty barrier expects one commit from each pair leader.
+template <int CG, bool A_MN, bool B_MN, class Epi, int MC = 1>
 __global__ void __launch_bounds__(256, 1)
     gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       const GemmGeom g, const typename Epi::Params ep) {
   using C = GemmCfg<CG>;
+  static_assert(MC == 1 || (MC == 2 && CG == 2), "multicast clusters are built from CTA pairs");
+  constexpr int CL = CG * MC;  // CTAs per cluster
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t sbase = ptx::smem_u32(smem);
@@ -101,9 +109,16 @@ __global__ void __launch_bounds__(256, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::STAGES * C::STAGE_BYTES + 8 * (2 * C::STAGES + 4));
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t rank = CG == 2 ? ptx::cluster_ctarank() : 0u;
-  const int cluster = blockIdx.x / CG, nclusters = gridDim.x / CG;
-  const int num_tiles = g.tiles_m * g.tiles_n;
+  const uint32_t crank = CL > 1 ? ptx::cluster_ctarank() : 0u;  // rank in cluster
+  const uint32_t rank = crank % CG;                              // rank in the CTA pair
+  const uint32_t pair = crank / CG;                              // pair index along M
+  const uint32_t leader = crank - rank;                          // cluster rank of the pair leader
+  const uint16_t pair_mask = uint16_t(((1u << CG) - 1u) << leader);
+  const int cluster = blockIdx.x / CL, nclusters = gridDim.x / CL;
+  const int tiles_mc = (g.tiles_m + MC - 1) / MC;  // cluster tiles along M
+  GemmGeom gc = g;
+  gc.tiles_m = tiles_mc;
+  const int num_tiles = tiles_mc * g.tiles_n;
 
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&tmA);
@@ -111,8 +126,8 @@ __global__ void __launch_bounds__(256, 1)
   }
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
-      ptx::mbar_init(bar_full + 8 * s, 1);    // leader's expect_tx arrival (covers the pair)
-      ptx::mbar_init(bar_empty + 8 * s, 1);   // one tcgen05.commit
+      ptx::mbar_init(bar_full + 8 * s, 1);    // pair leader's expect_tx (covers the pair)
+      ptx::mbar_init(bar_empty + 8 * s, MC);  // one tcgen05.commit per consuming pair
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(bar_tfull + 8 * a, 1);        // one tcgen05.commit
@@ -122,7 +137,7 @@ __global__ void __launch_bounds__(256, 1)
   }
   if (warp == 2) ptx::tmem_alloc<CG>(ptx::smem_u32(tmem_slot), C::TMEM_COLS);
   ptx::tc_fence_before();
-  if constexpr (CG == 2) ptx::cluster_sync(); else __syncthreads();
+  if constexpr (CL > 1) ptx::cluster_sync(); else __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *reinterpret_cast<volatile uint32_t*>(tmem_slot);
 
@@ -132,23 +147,24 @@ __global__ void __launch_bounds__(256, 1)
     const uint64_t polB = make_policy(g.pol_b, !Epi::kAStreams);
     uint32_t it = 0;
     for (int t = cluster; t < num_tiles; t += nclusters) {
-      int mb, nb;
-      tile_coords(g, t, mb, nb);
+      int mc, nb;
+      tile_coords(gc, t, mc, nb);
+      const int mb = mc * MC + int(pair);
       const int m0 = mb * C::BM + int(rank) * C::BM_CTA;
       const int n0 = nb * C::BN + int(rank) * C::B_ROWS;
       for (int kb = 0; kb < g.num_kb; ++kb, ++it) {
         const uint32_t s = it % C::STAGES, ph = (it / C::STAGES) & 1u;
         ptx::mbar_wait(bar_empty + 8 * s, ph ^ 1u);
-        const uint32_t fb = CG == 1 ? bar_full + 8 * s : ptx::mapa(bar_full + 8 * s, 0);
-        // The leader's barrier expects the bytes of BOTH CTAs of the pair; the
-        // peer only issues its TMA (a remote arrive would cost a GPU-scope
+        // The leader's barrier expects the bytes landing in BOTH CTAs of its
+        // pair; the peer only issues TMA (a remote arrive costs a GPU-scope
         // membar per stage).
         if (rank == 0) ptx::mbar_arrive_expect_tx(bar_full + 8 * s, C::STAGE_BYTES * CG);
+        const uint32_t fb = bar_full + 8 * s;
         const uint32_t a_dst = sA + s * C::A_BYTES, b_dst = sB + s * C::B_BYTES;
         const int k0 = kb * C::BK;
         auto load = [&](const CUtensorMap* m, uint32_t dst, int c0, int c1, uint64_t pol) {
           if constexpr (CG == 1) ptx::tma_load_2d(m, fb, dst, c0, c1, pol);
-          else ptx::tma_load_2d_cg2(m, fb, dst, c0, c1, pol);
+          else ptx::tma_load_2d_cg2(m, fb & 0xFEFFFFFFu, dst, c0, c1, pol);
         };
         if constexpr (!A_MN) {
           load(&tmA, a_dst, k0, m0, polA);
@@ -156,7 +172,15 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
           for (int j = 0; j < C::BM_CTA / 64; ++j) load(&tmA, a_dst + j * 8192, m0 + 64 * j, k0, polA);
         }
-        if constexpr (!B_MN) {
+        if constexpr (MC == 2) {
+          // my half (64 rows / 64 cols) of this CTA's B block, multicast to the
+          // same-rank CTA of both pairs
+          const uint16_t mask = uint16_t((1u << rank) | (1u << (CG + rank)));
+          if constexpr (!B_MN)
+            ptx::tma_load_2d_cg2_mc(&tmB, fb, b_dst + pair * 8192, k0, n0 + int(pair) * 64, mask, polB);
+          else
+            ptx::tma_load_2d_cg2_mc(&tmB, fb, b_dst + pair * 8192, n0 + int(pair) * 64, k0, mask, polB);
+        } else if constexpr (!B_MN) {
           load(&tmB, b_dst, k0, n0, polB);
         } else {
 #pragma unroll
@@ -165,8 +189,9 @@ __global__ void __launch_bounds__(256, 1)
       }
     }
   } else if (warp == 1 && lane == 0 && rank == 0) {
-    // ===== MMA issuer (leader CTA, one thread) =====
+    // ===== MMA issuer (pair leader, one thread) =====
     constexpr uint32_t idesc = ptx::idesc_bf16_f32(C::BM, C::BN, A_MN, B_MN);
+    constexpr uint16_t all_mask = uint16_t((1u << CL) - 1u);
     uint32_t it = 0, tc = 0;
     for (int t = cluster; t < num_tiles; t += nclusters, ++tc) {
       const uint32_t acc = tc & 1u, aph = (tc >> 1) & 1u;
@@ -189,17 +214,20 @@ __global__ void __launch_bounds__(256, 1)
                                    : ptx::sdesc_sw128(b_base + kk * 32, 16, 1024);
           ptx::mma_bf16<CG>(d, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
         }
-        ptx::mma_commit<CG>(bar_empty + 8 * s);
+        // free the stage in every CTA whose smem this pair read (all CTAs of
+        // the cluster when B was multicast)
+        ptx::mma_commit<CG>(bar_empty + 8 * s, MC == 2 ? all_mask : pair_mask);
       }
-      ptx::mma_commit<CG>(bar_tfull + 8 * acc);
+      ptx::mma_commit<CG>(bar_tfull + 8 * acc, pair_mask);
     }
   } else if (warp >= 4) {
     // ===== epilogue =====
     const int ew = warp - 4;
     uint32_t tc = 0;
     for (int t = cluster; t < num_tiles; t += nclusters, ++tc) {
-      int mb, nb;
-      tile_coords(g, t, mb, nb);
+      int mc, nb;
+      tile_coords(gc, t, mc, nb);
+      const int mb = mc * MC + int(pair);
       const uint32_t acc = tc & 1u, aph = (tc >> 1) & 1u;
       ptx::mbar_wait(bar_tfull + 8 * acc, aph);
       ptx::tc_fence_after();
@@ -210,13 +238,13 @@ __global__ void __launch_bounds__(256, 1)
       __syncwarp();
       if (lane == 0) {
         if constexpr (CG == 1) ptx::mbar_arrive(bar_tempty + 8 * acc);
-        else ptx::mbar_arrive_remote(bar_tempty + 8 * acc, 0);
+        else ptx::mbar_arrive_remote(bar_tempty + 8 * acc, leader);
       }
     }
   }
   __syncwarp();
   ptx::tc_fence_before();
-  if constexpr (CG == 2) ptx::cluster_sync(); else __syncthreads();
+  if constexpr (CL > 1) ptx::cluster_sync(); else __syncthreads();
   if (warp == 2) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc<CG>(tmem_base, C::TMEM_COLS);

@@ -117,6 +117,17 @@ __device__ __forceinline__ void tma_load_2d_cg2(const CUtensorMap* m, uint32_t l
       "l"(m), "r"(c0), "r"(c1), "r"(leader_bar), "l"(policy)
       : "memory");
 }
+// 2-CTA form with multicast: the box lands at the same smem offset in every
+// CTA of `mask`, and each destination signals the barrier of ITS pair
+// leader (`bar` given with the peer bit cleared, CUTLASS's convention).
+__device__ __forceinline__ void tma_load_2d_cg2_mc(const CUtensorMap* m, uint32_t bar, uint32_t dst, int c0, int c1,
+                                                   uint16_t mask, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      ".L2::cache_hint [%0], [%1, {%3, %4}], [%2], %5, %6;" ::"r"(dst),
+      "l"(m), "r"(bar & 0xFEFFFFFFu), "r"(c0), "r"(c1), "h"(mask), "l"(policy)
+      : "memory");
+}
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
@@ -179,9 +190,10 @@ __device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t adesc, uint64
 }
 
 // Arrive (once) on `bar` when all previously issued MMAs of this thread
-// complete.  CG == 2 multicasts to the same offset in both CTAs of the pair.
+// complete.  CG == 2 multicasts to the same offset in every CTA of `mask`
+// (default: the pair, ranks 0 and 1).
 template <int CG>
-__device__ __forceinline__ void mma_commit(uint32_t bar) {
+__device__ __forceinline__ void mma_commit(uint32_t bar, uint16_t mask = 3) {
   if constexpr (CG == 1)
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
                  : "memory");
@@ -189,7 +201,7 @@ __device__ __forceinline__ void mma_commit(uint32_t bar) {
     asm volatile(
         "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
             bar),
-        "h"((uint16_t)3)
+        "h"(mask)
         : "memory");
 }
 

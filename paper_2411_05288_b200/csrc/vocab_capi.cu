@@ -102,6 +102,7 @@ struct vp_ctx_s {
   // (measured: evict_normal on both operands beats first/last hints)
   int raster[3] = {0, 16, 0};
   int pol[3] = {0, 0, 0};
+  int mc = 1;  // CTA pairs per cluster sharing B by TMA multicast (1 or 2)
   ncclComm_t comm = nullptr;
   int nranks = 1, rank = 0;
   int* d_err = nullptr;
@@ -219,7 +220,7 @@ void gemm_logits(vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* s, vp_state
   timed_gemm(c, 0, [&] {
     vp::launch_gemm<vp::EpiLogitStats>(c->cg, {b->X, b->ldx, false}, {s->W, s->ldw, false}, int(b->n_tok),
                                        int(st->rows), int(b->h), c->raster[0], ep, c->gemm_sms, c->stream,
-                                       c->pol[0], c->pol[0]);
+                                       c->pol[0], c->pol[0], c->mc);
   });
   ++c->launches;
 }
@@ -229,7 +230,7 @@ void gemm_logits_f32(vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* s, vp_s
   timed_gemm(c, 1, [&] {
     vp::launch_gemm<vp::EpiStoreF32>(c->cg, {b->X, b->ldx, false}, {s->W, s->ldw, false}, int(b->n_tok),
                                      int(st->rows), int(b->h), c->raster[0], ep, c->gemm_sms, c->stream, c->pol[0],
-                                     c->pol[0]);
+                                     c->pol[0], c->mc);
   });
   ++c->launches;
 }
@@ -241,7 +242,7 @@ void gemm_dx(vp_ctx_s* c, vp_state_s* st, const vp_shard_t* s, float* out, int64
   timed_gemm(c, 2, [&] {
     vp::launch_gemm<vp::EpiStoreF32>(c->cg, {st->P, st->ldp, false}, {s->W, s->ldw, true}, int(st->n_tok),
                                      int(st->h), int(st->rows), c->raster[1], ep, c->gemm_sms, c->stream, c->pol[1],
-                                     c->pol[1]);
+                                     c->pol[1], c->mc);
   });
   ++c->launches;
 }
@@ -253,7 +254,7 @@ void gemm_dw(vp_ctx_s* c, vp_state_s* st, const void* Xop, int64_t ldx, float* o
   const int raster = c->raster[2] == 0 ? -tiles_n : c->raster[2];
   timed_gemm(c, 3, [&] {
     vp::launch_gemm<vp::EpiStoreF32>(c->cg, {st->P, st->ldp, true}, {Xop, ldx, true}, int(st->rows), int(st->h),
-                                     int(st->n_tok), raster, ep, c->gemm_sms, c->stream, c->pol[2], c->pol[2]);
+                                     int(st->n_tok), raster, ep, c->gemm_sms, c->stream, c->pol[2], c->pol[2], c->mc);
   });
   ++c->launches;
 }
@@ -743,6 +744,10 @@ int vp_ctx_set_option(vp_ctx_t c, const char* key, int64_t value) {
         require(value >= -1 && value <= 2, "vp_ctx_set_option: policy must be -1..2");
         c->pol[idx] = int(value);
       }
+    } else if (k == "multicast") {
+      require(value == 1 || value == 2, "vp_ctx_set_option: multicast must be 1 or 2");
+      require(value == 1 || c->cg == 2, "vp_ctx_set_option: multicast needs cta_group 2");
+      c->mc = int(value);
     } else if (k == "gemm_sms") {
       require(value >= 2 && value <= c->num_sms, "vp_ctx_set_option: gemm_sms out of range");
       c->gemm_sms = int(value);

@@ -37,6 +37,7 @@ __global__ void fill(__nv_bfloat16* p, int64_t n, float s, uint64_t seed) {
 }
 
 int main(int argc, char** argv) {
+  const int mc = getenv("VP_MC") ? atoi(getenv("VP_MC")) : 1;
   if (argc < 5) {
     fprintf(stderr, "usage: gemm_probe <k1|dx|dw> <raster> <pol_a> <pol_b> [iters] [V]\n");
     return 2;
@@ -60,21 +61,39 @@ int main(int argc, char** argv) {
   CK(cudaMalloc(&tm, int64_t(ntiles) * T * 4));
   CK(cudaMalloc(&ts, int64_t(ntiles) * T * 4));
   CK(cudaMalloc(&yt, T * 4));
-  const int64_t out_elems = kind == "dw" ? V * h : T * h;
+  float *tq, *ref;
+  int *flg, *bad, *cnt, *bl;
+  int2* fl;
+  CK(cudaMalloc(&tq, int64_t(ntiles) * T * 4));
+  CK(cudaMalloc(&ref, T * 4));
+  CK(cudaMalloc(&flg, 4096 * 4));
+  CK(cudaMalloc(&bad, T * 4));
+  CK(cudaMalloc(&cnt, 8));
+  CK(cudaMalloc(&bl, T * 4));
+  CK(cudaMalloc(&fl, int64_t(T / 32 + 1) * ntiles * 8));
+  const int64_t out_elems = kind == "dw" ? V * h : kind == "sq8192" ? int64_t(8192) * 8192 : T * h;
   CK(cudaMalloc(&out, out_elems * 4));
   auto run = [&] {
     if (kind == "k1") {
-      vp::EpiLogitStats::Params ep{P, V, tm, ts, T, nullptr, 0, V, yt};
+      vp::EpiLogitStats::Params ep{P,   V,   tm,  ts,  T,   nullptr, 0,   V,   yt,  tq,
+                                   ref, flg, bad, cnt, bl,  cnt + 1, fl};
+      CK(cudaMemsetAsync(flg, 0, 4096 * 4));
+      CK(cudaMemsetAsync(bad, 0, T * 4));
+      CK(cudaMemsetAsync(cnt, 0, 8));
       vp::launch_gemm<vp::EpiLogitStats>(2, {X, h, false}, {W, h, false}, int(T), int(V), int(h), raster, ep, nsm, 0,
-                                         pa, pb);
+                                         pa, pb, mc);
     } else if (kind == "dx") {
       vp::EpiStoreF32::Params ep{out, h, nullptr, 0, nullptr};
       vp::launch_gemm<vp::EpiStoreF32>(2, {P, V, false}, {W, h, true}, int(T), int(h), int(V), raster, ep, nsm, 0, pa,
-                                       pb);
-    } else {
+                                       pb, mc);
+    } else if (kind == "dw") {
       vp::EpiStoreF32::Params ep{out, h, nullptr, 0, nullptr};
       vp::launch_gemm<vp::EpiStoreF32>(2, {P, V, true}, {X, h, true}, int(V), int(h), int(T), raster, ep, nsm, 0, pa,
-                                       pb);
+                                       pb, mc);
+    } else {  // sq8192: plain 8192^3 K-major GEMM (W as an 8192 x 8192 slice), fp32 out
+      vp::EpiStoreF32::Params ep{out, 8192, nullptr, 0, nullptr};
+      vp::launch_gemm<vp::EpiStoreF32>(2, {W, 8192, false}, {W + int64_t(8192) * 8192, 8192, false}, 8192, 8192,
+                                       8192, raster, ep, nsm, 0, pa, pb, mc);
     }
   };
   run();
@@ -89,7 +108,9 @@ int main(int argc, char** argv) {
   float ms;
   cudaEventElapsedTime(&ms, a, b);
   ms /= iters;
+  const double flops = kind == "sq8192" ? 2.0 * 8192.0 * 8192.0 * 8192.0 : 2.0 * T * h * double(V);
+  printf("mc=%d ", mc);
   printf("probe %s raster=%d pol_a=%d pol_b=%d V=%lld: %.3f ms %.1f TFLOP/s\n", kind.c_str(), raster, pa, pb,
-         (long long)V, ms, 2.0 * T * h * double(V) / ms / 1e9);
+         (long long)V, ms, flops / ms / 1e9);
   return 0;
 }

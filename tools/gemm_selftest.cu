@@ -47,7 +47,7 @@ __global__ void ref_gemm(const __nv_bfloat16* A, int64_t lda, bool amn, const __
 
 static int failures = 0;
 
-static void check_store(int cg, bool amn, bool bmn, int M, int N, int K, int nsm) {
+static void check_store(int cg, bool amn, bool bmn, int M, int N, int K, int nsm, int mc = 1) {
   const int64_t lda = amn ? ((M + 7) / 8 * 8) : ((K + 7) / 8 * 8);
   const int64_t ldb = bmn ? ((N + 7) / 8 * 8) : ((K + 7) / 8 * 8);
   const int64_t asz = amn ? int64_t(K) * lda : int64_t(M) * lda;
@@ -62,7 +62,7 @@ static void check_store(int cg, bool amn, bool bmn, int M, int N, int K, int nsm
   init_bf16<<<256, 256>>>(B, bsz, 91u, 1.f);
   CK(cudaMemset(D, 0xFF, int64_t(M) * N * 4));
   vp::EpiStoreF32::Params ep{D, N, nullptr, 0};
-  vp::launch_gemm<vp::EpiStoreF32>(cg, {A, lda, amn}, {B, ldb, bmn}, M, N, K, 0, ep, nsm, 0);
+  vp::launch_gemm<vp::EpiStoreF32>(cg, {A, lda, amn}, {B, ldb, bmn}, M, N, K, 0, ep, nsm, 0, -1, -1, mc);
   ref_gemm<<<dim3((N + 127) / 128, M), 128>>>(A, lda, amn, B, ldb, bmn, R, M, N, K);
   CK(cudaDeviceSynchronize());
   std::vector<float> d(size_t(M) * N), r(size_t(M) * N);
@@ -76,7 +76,7 @@ static void check_store(int cg, bool amn, bool bmn, int M, int N, int K, int nsm
     maxerr = std::max(maxerr, std::isnan(e) ? 1e30 : e);
     maxref = std::max(maxref, double(std::fabs(r[i])));
   }
-  printf("store cg=%d A_%s B_%s M=%d N=%d K=%d : max_abs_err=%.3e max_ref=%.3e bad=%zu %s\n", cg,
+  printf("store cg=%d mc=%d A_%s B_%s M=%d N=%d K=%d : max_abs_err=%.3e max_ref=%.3e bad=%zu %s\n", cg, mc,
          amn ? "MN" : "K", bmn ? "MN" : "K", M, N, K, maxerr, maxref, bad, bad ? "FAIL" : "ok");
   if (bad) ++failures;
   cudaFree(A);
@@ -85,7 +85,7 @@ static void check_store(int cg, bool amn, bool bmn, int M, int N, int K, int nsm
   cudaFree(R);
 }
 
-static void check_stats(int cg, int M, int N, int K, int nsm) {
+static void check_stats(int cg, int M, int N, int K, int nsm, int mc = 1) {
   const int64_t ld = (K + 7) / 8 * 8;
   const int64_t ldp = (N + 63) / 64 * 64;
   const int tiles = (N + 255) / 256;
@@ -106,8 +106,21 @@ static void check_stats(int cg, int M, int N, int K, int nsm) {
   const int64_t rb = 1000;
   for (int i = 0; i < M; ++i) hl[i] = (i % 3 == 0) ? 5 : rb + (int64_t(i) * 7919) % N;
   CK(cudaMemcpy(lab, hl.data(), M * 8, cudaMemcpyHostToDevice));
-  vp::EpiLogitStats::Params ep{P, ldp, tm, ts, M, lab, rb, rb + N, yt};
-  vp::launch_gemm<vp::EpiLogitStats>(cg, {A, ld, false}, {B, ld, false}, M, N, K, 0, ep, nsm, 0);
+  float *tq, *ref;
+  int *flg, *badr, *cnt, *bl;
+  int2* fl;
+  CK(cudaMalloc(&tq, int64_t(tiles) * M * 4));
+  CK(cudaMalloc(&ref, M * 4));
+  CK(cudaMalloc(&flg, 4096 * 4));
+  CK(cudaMalloc(&badr, M * 4));
+  CK(cudaMalloc(&cnt, 8));
+  CK(cudaMalloc(&bl, M * 4));
+  CK(cudaMalloc(&fl, int64_t(M / 32 + 1) * tiles * 8));
+  CK(cudaMemset(flg, 0, 4096 * 4));
+  CK(cudaMemset(badr, 0, M * 4));
+  CK(cudaMemset(cnt, 0, 8));
+  vp::EpiLogitStats::Params ep{P, ldp, tm, ts, M, lab, rb, rb + N, yt, tq, ref, flg, badr, cnt, bl, cnt + 1, fl};
+  vp::launch_gemm<vp::EpiLogitStats>(cg, {A, ld, false}, {B, ld, false}, M, N, K, 0, ep, nsm, 0, -1, -1, mc);
   ref_gemm<<<dim3((N + 127) / 128, M), 128>>>(A, ld, false, B, ld, false, R, M, N, K);
   CK(cudaDeviceSynchronize());
   std::vector<float> r(size_t(M) * N), htm(size_t(tiles) * M), hts(size_t(tiles) * M), hyt(M);
@@ -117,19 +130,22 @@ static void check_stats(int cg, int M, int N, int K, int nsm) {
   CK(cudaMemcpy(hts.data(), ts, hts.size() * 4, cudaMemcpyDeviceToHost));
   CK(cudaMemcpy(hyt.data(), yt, hyt.size() * 4, cudaMemcpyDeviceToHost));
   CK(cudaMemcpy(hp.data(), P, hp.size() * 2, cudaMemcpyDeviceToHost));
+  std::vector<float> hq(size_t(tiles) * M);
+  CK(cudaMemcpy(hq.data(), tq, hq.size() * 4, cudaMemcpyDeviceToHost));
   double em = 0, es = 0, ep_ = 0, ey = 0;
   for (int i = 0; i < M; ++i) {
     for (int t = 0; t < tiles; ++t) {
       double mx = -1e300;
       for (int v = t * 256; v < std::min(N, t * 256 + 256); ++v) mx = std::max(mx, double(r[size_t(i) * N + v]));
       double s = 0;
+      const double q = hq[size_t(t) * M + i];
       for (int v = t * 256; v < std::min(N, t * 256 + 256); ++v) {
-        const double e = std::exp(double(r[size_t(i) * N + v]) - mx);
+        const double e = std::exp(double(r[size_t(i) * N + v]) - q);
         s += e;
         uint32_t bits = uint32_t(hp[size_t(i) * ldp + v]) << 16;
         float pv;
         memcpy(&pv, &bits, 4);
-        ep_ = std::max(ep_, std::fabs(pv - e));
+        ep_ = std::max(ep_, std::fabs(pv - e) / std::max(1.0, e));
       }
       em = std::max(em, std::fabs(htm[size_t(t) * M + i] - mx));
       es = std::max(es, std::fabs(hts[size_t(t) * M + i] - s) / s);
@@ -137,7 +153,7 @@ static void check_stats(int cg, int M, int N, int K, int nsm) {
     if (hl[i] >= rb && hl[i] < rb + N) ey = std::max(ey, double(std::fabs(hyt[i] - r[size_t(i) * N + (hl[i] - rb)])));
   }
   const bool ok = em < 1e-3 && es < 1e-4 && ep_ < 4e-3 && ey < 1e-3;
-  printf("stats cg=%d M=%d N=%d K=%d : tile_max_err=%.2e tile_sum_relerr=%.2e P_err=%.2e ytgt_err=%.2e %s\n", cg, M,
+  printf("stats cg=%d mc=%d M=%d N=%d K=%d : tile_max_err=%.2e tile_sum_relerr=%.2e P_err=%.2e ytgt_err=%.2e %s\n", cg, mc, M,
          N, K, em, es, ep_, ey, ok ? "ok" : "FAIL");
   if (!ok) ++failures;
   cudaFree(A);
@@ -148,6 +164,13 @@ static void check_stats(int cg, int M, int N, int K, int nsm) {
   cudaFree(ts);
   cudaFree(yt);
   cudaFree(lab);
+  cudaFree(tq);
+  cudaFree(ref);
+  cudaFree(flg);
+  cudaFree(badr);
+  cudaFree(cnt);
+  cudaFree(bl);
+  cudaFree(fl);
 }
 
 template <class F>
@@ -197,7 +220,18 @@ static void bench_stats(int cg, int M, int N, int K, int nsm) {
   CK(cudaMalloc(&yt, int64_t(M) * 4));
   init_bf16<<<1024, 256>>>(A, int64_t(M) * K, 3u, 1.f);
   init_bf16<<<1024, 256>>>(B, int64_t(N) * K, 4u, 0.02f);
-  vp::EpiLogitStats::Params ep{P, N, tm, ts, M, nullptr, 0, N, yt};
+  float* tq;
+  float* ref;
+  int *flg, *badr, *cnt, *bl;
+  int2* fl;
+  CK(cudaMalloc(&tq, int64_t(tiles) * M * 4));
+  CK(cudaMalloc(&ref, M * 4));
+  CK(cudaMalloc(&flg, 4096 * 4));
+  CK(cudaMalloc(&badr, M * 4));
+  CK(cudaMalloc(&cnt, 8));
+  CK(cudaMalloc(&bl, M * 4));
+  CK(cudaMalloc(&fl, int64_t(M / 32 + 1) * tiles * 8));
+  vp::EpiLogitStats::Params ep{P, N, tm, ts, M, nullptr, 0, N, yt, tq, ref, flg, badr, cnt, bl, cnt + 1, fl};
   const float ms = time_ms([&] { vp::launch_gemm<vp::EpiLogitStats>(cg, {A, K, false}, {B, K, false}, M, N, K, 0, ep, nsm, 0); }, 5);
   printf("bench stats cg=%d M=%d N=%d K=%d : %.3f ms  %.1f TFLOP/s\n", cg, M, N, K, ms,
          2.0 * M * N * double(K) / ms / 1e9);
@@ -218,16 +252,20 @@ int main(int argc, char** argv) {
     return 0;
   }
   printf("SMs=%d\n", nsm);
-  for (int cg : {1, 2}) {
-    check_store(cg, false, false, 256, 256, 64, nsm);
-    check_store(cg, false, false, 512, 768, 1024, nsm);
-    check_store(cg, false, true, 512, 768, 1024, nsm);
-    check_store(cg, true, true, 512, 768, 1024, nsm);
-    check_store(cg, false, false, 300, 520, 200, nsm);
-    check_store(cg, false, true, 300, 520, 200, nsm);
-    check_store(cg, true, true, 300, 520, 200, nsm);
-    check_stats(cg, 300, 1000, 256, nsm);
-    check_stats(cg, 512, 777, 512, nsm);
+  for (int v = 0; v < 3; ++v) {
+    const int cg = v == 0 ? 1 : 2, mc = v == 2 ? 2 : 1;
+    check_store(cg, false, false, 256, 256, 64, nsm, mc);
+    check_store(cg, false, false, 512, 768, 1024, nsm, mc);
+    check_store(cg, false, true, 512, 768, 1024, nsm, mc);
+    check_store(cg, true, true, 512, 768, 1024, nsm, mc);
+    check_store(cg, false, false, 300, 520, 200, nsm, mc);
+    check_store(cg, false, true, 300, 520, 200, nsm, mc);
+    check_store(cg, true, true, 300, 520, 200, nsm, mc);
+    check_store(cg, false, false, 600, 3000, 320, nsm, mc);
+    check_store(cg, true, true, 700, 1100, 640, nsm, mc);
+    check_stats(cg, 300, 1000, 256, nsm, mc);
+    check_stats(cg, 512, 777, 512, nsm, mc);
+    check_stats(cg, 1000, 5000, 128, nsm, mc);
   }
   if (do_bench) {
     for (int cg : {1, 2}) bench_store(cg, false, false, 8192, 8192, 8192, 0, nsm);
