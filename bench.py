@@ -204,26 +204,24 @@ def run_ours(args):
     import torch
     import torch.distributed as dist
 
+    from paper_2411_05288_b200 import dist as vpd
     from paper_2411_05288_b200 import vocab_math as vm
 
-    rank, world, local = dist_env()
+    rank, world, local = vpd.env()
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     T, h, V = args.tokens, args.hidden, args.vocab
-    if V % world:
-        raise SystemExit("vocab must divide by the number of GPUs (pad_vocab_size)")
-    rows = V // world
+    row_begin, row_end = vpd.shard_rows(vm.pad_vocab_size(V, world) if V % world else V, world, rank)
+    rows = row_end - row_begin
     ctx = vm.Context(local, cta_group=args.cta_group)
     for kv in args.opt:
         k, v = kv.split("=")
         ctx.set_option(k, int(v))
     if world > 1:
-        uid = [vm.Context.unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        ctx.comm_init(world, rank, uid[0])
+        vpd.init_comm(ctx)
     ctx.reserve(T, h, world)
 
     # synthetic inputs of the named shape (X~N(0,1), W~N(0,0.02^2), seed 1234)
@@ -232,7 +230,7 @@ def run_ours(args):
     labels = torch.randint(0, V, (T,), device="cuda", generator=gen)
     gen.manual_seed(1234 + 1 + rank)
     W_k = (torch.randn(rows, h, device="cuda", generator=gen) * 0.02).to(torch.bfloat16)
-    shard = vm.EmbeddingShard(W_k, rank, rank * rows, (rank + 1) * rows)
+    shard = vm.EmbeddingShard(W_k, rank, row_begin, row_end)
     batch = vm.TokenBatch(X, labels)
     state = vm.ShardState(ctx, T, h, rows)
     outs = (torch.empty(T, dtype=torch.float32, device="cuda"), torch.empty(T, h, dtype=torch.float32, device="cuda"),
@@ -246,11 +244,7 @@ def run_ours(args):
         torch.cuda.synchronize()
 
     def max_over_ranks(x: float) -> float:
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return vpd.max_over_ranks(x, device="cuda")
 
     # ---- device-resident throughput (value) ----
     for _ in range(args.warmup):

@@ -121,7 +121,8 @@ struct vp_ctx_s {
     VP_CUDA(cudaSetDevice(device));
     (void)cudaGetLastError();  // drop stale non-sticky errors left by other code
   }
-  bool distributed() const { return comm != nullptr && nranks > 1; }
+  bool force_collectives = false;  // route exchanges through NCCL even with 1 rank (tests)
+  bool distributed() const { return comm != nullptr && (nranks > 1 || force_collectives); }
   template <class T>
   T* buf(DevBuf& b, size_t count) {
     return static_cast<T*>(b.get(count * sizeof(T)));
@@ -744,6 +745,8 @@ int vp_ctx_set_option(vp_ctx_t c, const char* key, int64_t value) {
         require(value >= -1 && value <= 2, "vp_ctx_set_option: policy must be -1..2");
         c->pol[idx] = int(value);
       }
+    } else if (k == "force_collectives") {
+      c->force_collectives = value != 0;
     } else if (k == "multicast") {
       require(value == 1 || value == 2, "vp_ctx_set_option: multicast must be 1 or 2");
       require(value == 1 || c->cg == 2, "vp_ctx_set_option: multicast needs cta_group 2");

@@ -245,3 +245,30 @@ def test_extreme_logit_gap_takes_the_overflow_path(ctx):
         for p in (1, 2):
             res, _ = run_device(ctx, alg, batch, Wd, p, h)
             assert_parity(res, ref, f"gap {alg} p={p}")
+
+
+def test_nccl_exchange_path_with_a_one_rank_group(ctx):
+    # Every NCCL call site of the library (stats all-gather, dX / loss
+    # all-reduce, naive max/sum all-reduces) exercised on the one GPU through
+    # a 1-rank communicator; results must equal the single-device path.
+    X, W, g = oracle.random_instance(96, 64, 512, 4)
+    Xb, Wb, batch, Wd = device_case(X, W, g)
+    shards = vm.shard_weights(Wd, 1)
+    nctx = vm.Context(0)
+    nctx.comm_init(1, 0, vm.Context.unique_id())
+    nctx.set_option("force_collectives", 1)
+    assert nctx.comm_info() == (1, 0)
+    for alg in ALGS:
+        fn = {"naive": vm.run_naive, "alg1": vm.run_alg1, "alg2": vm.run_alg2}[alg]
+        a = fn(ctx, batch, shards)
+        b = fn(nctx, batch, shards)
+        nctx.sync()
+        ctx.sync()
+        for x, y in ((a.loss, b.loss), (a.grad_x, b.grad_x), (a.grad_w_full(), b.grad_w_full()),
+                     (a.stats.m, b.stats.m), (a.stats.sum, b.stats.sum)):
+            assert torch.allclose(x, y, rtol=1e-6, atol=1e-7), alg
+    t = torch.arange(16, dtype=torch.float32, device="cuda")
+    vm.allreduce_sum(nctx, t)
+    nctx.sync()
+    assert torch.equal(t, torch.arange(16, dtype=torch.float32, device="cuda"))
+    nctx.close()
