@@ -89,7 +89,9 @@ int vp_ctx_reserve(vp_ctx_t ctx, int64_t n_tok, int64_t h, int p);
 /* Options: "cta_group" (1 or 2, default 2), "gemm_sms" (SMs used by GEMMs),
  * "raster_{logits,dx,dw}" (tile order, see GemmGeom::raster),
  * "policy_{logits,dx,dw}" (TMA L2 policy: -1 default, 0 normal, 1 first, 2 last),
- * "multicast" (1 = CTA-pair clusters, 2 = 4-CTA clusters sharing B by TMA multicast). */
+ * "multicast" (1 = CTA-pair clusters, 2 = 4-CTA clusters sharing B by TMA multicast),
+ * "nh_dx" / "nh_dw" (1 = 256x256 pair tiles, 2 = 256x512 pair tiles),
+ * "force_collectives" (1 = use the NCCL group even with one rank; tests). */
 int vp_ctx_set_option(vp_ctx_t ctx, const char* key, int64_t value);
 /* Number of kernels this context has launched (evidence counter). */
 int64_t vp_ctx_launch_count(vp_ctx_t ctx);

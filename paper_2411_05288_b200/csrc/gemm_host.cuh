@@ -57,28 +57,28 @@ struct Operand {
   bool mn_major;
 };
 
-template <int CG, bool A_MN, bool B_MN, class Epi, int MC = 1>
+template <int CG, bool A_MN, bool B_MN, class Epi, int MC = 1, int NH = 1>
 inline void launch_gemm_t(const Operand& A, const Operand& B, int M, int N, int K, int raster,
                           const typename Epi::Params& ep, int num_sms, cudaStream_t st, int pol_a = -1,
                           int pol_b = -1) {
-  using C = GemmCfg<CG>;
+  using C = GemmCfg<CG, NH>;
   const CUtensorMap ta = A_MN ? make_tmap_bf16(A.ptr, uint64_t(M), uint64_t(K), uint64_t(A.ld), 64, 64)
                               : make_tmap_bf16(A.ptr, uint64_t(K), uint64_t(M), uint64_t(A.ld), 64, C::BM_CTA);
   // with multicast each CTA loads half of its B block (64 rows / one 64-col chunk)
   const CUtensorMap tb = B_MN ? make_tmap_bf16(B.ptr, uint64_t(N), uint64_t(K), uint64_t(B.ld), 64, 64)
                               : make_tmap_bf16(B.ptr, uint64_t(K), uint64_t(N), uint64_t(B.ld), 64,
-                                               MC == 2 ? 64 : C::B_ROWS);
+                                               MC == 2 ? 64 : C::B_HALF_ROWS);
   GemmGeom g;
   g.M = M;
   g.N = N;
   g.K = K;
   g.tiles_m = (M + C::BM - 1) / C::BM;
-  g.tiles_n = (N + C::BN - 1) / C::BN;
+  g.tiles_n = (N + C::BN_TILE - 1) / C::BN_TILE;
   g.num_kb = (K + C::BK - 1) / C::BK;
   g.raster = raster;
   g.pol_a = pol_a;
   g.pol_b = pol_b;
-  auto kern = gemm_sm100_kernel<CG, A_MN, B_MN, Epi, MC>;
+  auto kern = gemm_sm100_kernel<CG, A_MN, B_MN, Epi, MC, NH>;
   static bool attr_done = false;
   if (!attr_done) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
@@ -131,21 +131,24 @@ inline void launch_gemm_t(const Operand& A, const Operand& B, int M, int N, int 
 template <class Epi>
 inline void launch_gemm(int cg, const Operand& A, const Operand& B, int M, int N, int K, int raster,
                         const typename Epi::Params& ep, int num_sms, cudaStream_t st, int pol_a = -1,
-                        int pol_b = -1, int mc = 1) {
-#define VP_GEMM_CASE(CGV, AM, BM_, MCV)                                                             \
-  if (cg == CGV && A.mn_major == AM && B.mn_major == BM_ && mc == MCV) {                            \
-    launch_gemm_t<CGV, AM, BM_, Epi, MCV>(A, B, M, N, K, raster, ep, num_sms, st, pol_a, pol_b);     \
-    return;                                                                                         \
+                        int pol_b = -1, int mc = 1, int nh = 1) {
+#define VP_GEMM_CASE(CGV, AM, BM_, MCV, NHV)                                                            \
+  if (cg == CGV && A.mn_major == AM && B.mn_major == BM_ && mc == MCV && nh == NHV) {                   \
+    launch_gemm_t<CGV, AM, BM_, Epi, MCV, NHV>(A, B, M, N, K, raster, ep, num_sms, st, pol_a, pol_b);    \
+    return;                                                                                             \
   }
-  VP_GEMM_CASE(2, false, false, 2)
-  VP_GEMM_CASE(2, false, true, 2)
-  VP_GEMM_CASE(2, true, true, 2)
-  VP_GEMM_CASE(2, false, false, 1)
-  VP_GEMM_CASE(2, false, true, 1)
-  VP_GEMM_CASE(2, true, true, 1)
-  VP_GEMM_CASE(1, false, false, 1)
-  VP_GEMM_CASE(1, false, true, 1)
-  VP_GEMM_CASE(1, true, true, 1)
+  VP_GEMM_CASE(2, false, false, 1, 1)
+  VP_GEMM_CASE(2, false, true, 1, 1)
+  VP_GEMM_CASE(2, true, true, 1, 1)
+  VP_GEMM_CASE(2, false, false, 2, 1)
+  VP_GEMM_CASE(2, false, true, 2, 1)
+  VP_GEMM_CASE(2, true, true, 2, 1)
+  VP_GEMM_CASE(2, false, false, 1, 2)
+  VP_GEMM_CASE(2, false, true, 1, 2)
+  VP_GEMM_CASE(2, true, true, 1, 2)
+  VP_GEMM_CASE(1, false, false, 1, 1)
+  VP_GEMM_CASE(1, false, true, 1, 1)
+  VP_GEMM_CASE(1, true, true, 1, 1)
 #undef VP_GEMM_CASE
   throw std::invalid_argument("launch_gemm: unsupported operand layout combination");
 }

@@ -46,15 +46,20 @@ __device__ __forceinline__ uint64_t make_policy(int p, bool dflt_first) {
   return p == 1 ? ptx::policy_evict_first() : p == 2 ? ptx::policy_evict_last() : ptx::policy_evict_normal();
 }
 
-template <int CG>
+// NH = N halves per tile: NH == 2 gives a 256 x 512 pair tile computed as two
+// N=256 MMAs per K step into all 512 TMEM columns (one accumulator, no TMEM
+// double buffering): 25% fewer operand bytes per flop and half the A re-reads.
+template <int CG, int NH = 1>
 struct GemmCfg {
   static constexpr int BM_CTA = 128;          // accumulator rows per CTA
   static constexpr int BM = 128 * CG;         // MMA M
   static constexpr int BN = 256;              // MMA N
+  static constexpr int BN_TILE = BN * NH;     // tile N
   static constexpr int BK = 64;               // 128 B of bf16 = one swizzle row
   static constexpr int UK = 16;               // K per tcgen05.mma (kind::f16)
-  static constexpr int B_ROWS = BN / CG;      // B rows loaded per CTA
-  static constexpr int STAGES = CG == 2 ? 6 : 4;
+  static constexpr int B_HALF_ROWS = BN / CG; // B rows per CTA per N half
+  static constexpr int B_ROWS = NH * B_HALF_ROWS;  // B rows loaded per CTA
+  static constexpr int STAGES = CG == 2 ? (NH == 2 ? 4 : 6) : 4;
   static constexpr int A_BYTES = BM_CTA * BK * 2;
   static constexpr int B_BYTES = B_ROWS * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
@@ -90,12 +95,14 @@ __device__ __forceinline__ void tile_coords(const GemmGeom& g, int t, int& mb, i
 // multicasts them to its counterpart in the other pair, halving B's L2
 // traffic.  A stage may then be refilled only after BOTH pairs consumed it,
 // so every empty barrier expects one commit from each pair leader.
-template <int CG, bool A_MN, bool B_MN, class Epi, int MC = 1>
+template <int CG, bool A_MN, bool B_MN, class Epi, int MC = 1, int NH = 1>
 __global__ void __launch_bounds__(256, 1)
     gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       const GemmGeom g, const typename Epi::Params ep) {
-  using C = GemmCfg<CG>;
+  using C = GemmCfg<CG, NH>;
   static_assert(MC == 1 || (MC == 2 && CG == 2), "multicast clusters are built from CTA pairs");
+  static_assert(NH == 1 || (NH == 2 && CG == 2 && MC == 1), "512-wide tiles: CTA pairs without multicast");
+  constexpr int NACC = NH == 1 ? 2 : 1;  // TMEM accumulator buffers
   constexpr int CL = CG * MC;  // CTAs per cluster
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -151,7 +158,7 @@ __global__ void __launch_bounds__(256, 1)
       tile_coords(gc, t, mc, nb);
       const int mb = mc * MC + int(pair);
       const int m0 = mb * C::BM + int(rank) * C::BM_CTA;
-      const int n0 = nb * C::BN + int(rank) * C::B_ROWS;
+      const int n0 = nb * C::BN_TILE + int(rank) * C::B_HALF_ROWS;  // + h * C::BN for N half h
       for (int kb = 0; kb < g.num_kb; ++kb, ++it) {
         const uint32_t s = it % C::STAGES, ph = (it / C::STAGES) & 1u;
         ptx::mbar_wait(bar_empty + 8 * s, ph ^ 1u);
@@ -181,10 +188,15 @@ __global__ void __launch_bounds__(256, 1)
           else
             ptx::tma_load_2d_cg2_mc(&tmB, fb, b_dst + pair * 8192, n0 + int(pair) * 64, k0, mask, polB);
         } else if constexpr (!B_MN) {
-          load(&tmB, b_dst, k0, n0, polB);
+#pragma unroll
+          for (int hh = 0; hh < NH; ++hh)
+            load(&tmB, b_dst + hh * C::B_HALF_ROWS * 128, k0, n0 + hh * C::BN, polB);
         } else {
 #pragma unroll
-          for (int j = 0; j < C::B_ROWS / 64; ++j) load(&tmB, b_dst + j * 8192, n0 + 64 * j, k0, polB);
+          for (int hh = 0; hh < NH; ++hh)
+#pragma unroll
+            for (int j = 0; j < C::B_HALF_ROWS / 64; ++j)
+              load(&tmB, b_dst + hh * C::B_HALF_ROWS * 128 + j * 8192, n0 + hh * C::BN + 64 * j, k0, polB);
         }
       }
     }
@@ -194,7 +206,7 @@ __global__ void __launch_bounds__(256, 1)
     constexpr uint16_t all_mask = uint16_t((1u << CL) - 1u);
     uint32_t it = 0, tc = 0;
     for (int t = cluster; t < num_tiles; t += nclusters, ++tc) {
-      const uint32_t acc = tc & 1u, aph = (tc >> 1) & 1u;
+      const uint32_t acc = tc % NACC, aph = (tc / NACC) & 1u;
       if constexpr (CG == 2) ptx::mbar_wait_cluster(bar_tempty + 8 * acc, aph ^ 1u);
       else ptx::mbar_wait(bar_tempty + 8 * acc, aph ^ 1u);
       ptx::tc_fence_after();
@@ -210,9 +222,13 @@ __global__ void __launch_bounds__(256, 1)
           // MN-major: advance 16 K-rows (2 KB); LBO = 64-wide MN atom (8 KB box).
           const uint64_t ad = A_MN ? ptx::sdesc_sw128(a_base + kk * 2048, 8192, 1024)
                                    : ptx::sdesc_sw128(a_base + kk * 32, 16, 1024);
-          const uint64_t bd = B_MN ? ptx::sdesc_sw128(b_base + kk * 2048, 8192, 1024)
-                                   : ptx::sdesc_sw128(b_base + kk * 32, 16, 1024);
-          ptx::mma_bf16<CG>(d, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+#pragma unroll
+          for (int hh = 0; hh < NH; ++hh) {
+            const uint32_t bh = b_base + hh * C::B_HALF_ROWS * 128;
+            const uint64_t bd = B_MN ? ptx::sdesc_sw128(bh + kk * 2048, 8192, 1024)
+                                     : ptx::sdesc_sw128(bh + kk * 32, 16, 1024);
+            ptx::mma_bf16<CG>(d + hh * C::BN, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+          }
         }
         // free the stage in every CTA whose smem this pair read (all CTAs of
         // the cluster when B was multicast)
@@ -228,12 +244,14 @@ __global__ void __launch_bounds__(256, 1)
       int mc, nb;
       tile_coords(gc, t, mc, nb);
       const int mb = mc * MC + int(pair);
-      const uint32_t acc = tc & 1u, aph = (tc >> 1) & 1u;
+      const uint32_t acc = tc % NACC, aph = (tc / NACC) & 1u;
       ptx::mbar_wait(bar_tfull + 8 * acc, aph);
       ptx::tc_fence_after();
       const uint32_t taddr = tmem_base + acc * C::BN + (uint32_t(ew * 32) << 16);
       const int row = mb * C::BM + int(rank) * C::BM_CTA + ew * 32 + lane;
-      Epi::apply(ep, g, taddr, row, nb * C::BN, nb);
+#pragma unroll 1
+      for (int hh = 0; hh < NH; ++hh)
+        Epi::apply(ep, g, taddr + hh * C::BN, row, nb * C::BN_TILE + hh * C::BN, nb * NH + hh);
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) {
@@ -344,62 +362,14 @@ struct EpiLogitStats {
     int* fix_count;         // (32-row group, tile) pairs stored relative to their own max
     int2* fix_list;         // [ceil(M/32) x tiles_n]
   };
-  __device__ static void apply(const Params& p, const GemmGeom& g, uint32_t taddr, int row, int col0, int nb) {
+  // One pass over the 256 accumulator columns of this row: P = bf16(e^{Y - ref}),
+  // s = sum e^{Y - ref}; with track = true it also takes the tile max and the
+  // label logit (the single-pass path, where ref = r_i is known up front).
+  __device__ static void emit(const Params& p, uint32_t taddr, int row, bool row_ok, int col0, int nvalid,
+                              float ref, int lb, bool track, float& mx, float& yt, bool& has_t, float& sum) {
     constexpr float kLog2e = 1.4426950408889634f;
-    const bool row_ok = row < g.M;
-    const int lane = threadIdx.x & 31;
-    const int nvalid = min(GemmCfg<1>::BN, g.N - col0);
-    int lb = -1;
-    if (row_ok && p.labels) {
-      const int64_t gl = p.labels[row];
-      if (gl >= p.row_begin && gl < p.row_end) lb = int(gl - p.row_begin) - col0;  // offset inside tile
-    }
-    float mx = -INFINITY, yt = 0.f;
-    bool has_t = false;
-#pragma unroll 1
-    for (int c = 0; c < 8; ++c) {
-      if (c * 32 >= nvalid) break;
-      uint32_t r[32];
-      ptx::tmem_ld32(taddr + c * 32, r);
-      ptx::tmem_ld_wait();
-      const int nv = nvalid - c * 32;
-#pragma unroll
-      for (int j = 0; j < 32; ++j)
-        if (j < nv) mx = fmaxf(mx, __uint_as_float(r[j]));
-      const int off = lb - c * 32;
-      if (off >= 0 && off < 32 && off < nv) {
-#pragma unroll
-        for (int j = 0; j < 32; ++j)
-          if (j == off) yt = __uint_as_float(r[j]);
-        has_t = true;
-      }
-    }
-    // ---- choose the reference q for this (row, tile) ----
-    const int blk = row >> 7;
-    float ref = mx;
-    bool own = false, bad = false;
-    if (nb == 0) {
-      if (row_ok) p.row_ref[row] = mx;
-      asm volatile("bar.sync 1, 128;" ::: "memory");  // the 4 epilogue warps of this CTA
-      if (threadIdx.x == 128) {
-        __threadfence();
-        atomicExch(p.ref_flag + blk, 1);
-      }
-    } else {
-      int f;
-      asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(f) : "l"(p.ref_flag + blk) : "memory");
-      if (f) {
-        if (row_ok) {
-          const float r = p.row_ref[row];
-          if (mx - r > kMaxRefGap) bad = true;  // exp(y - r) could overflow: keep own max
-          else ref = r;
-        }
-      } else {
-        own = true;
-      }
-    }
     const float refs = ref * kLog2e;
-    float sum = 0.f;
+    sum = 0.f;
     __nv_bfloat16* dst = p.P + int64_t(row) * p.ldp + col0;
     const bool vec = ((p.ldp & 7) == 0) && ((reinterpret_cast<uintptr_t>(p.P) & 15) == 0);
 #pragma unroll 1
@@ -409,6 +379,18 @@ struct EpiLogitStats {
       ptx::tmem_ld32(taddr + c * 32, r);
       ptx::tmem_ld_wait();
       const int nv = nvalid - c * 32;
+      if (track) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (j < nv) mx = fmaxf(mx, __uint_as_float(r[j]));
+        const int off = lb - c * 32;
+        if (off >= 0 && off < 32 && off < nv) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (j == off) yt = __uint_as_float(r[j]);
+          has_t = true;
+        }
+      }
       uint32_t pk[16];
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
@@ -428,6 +410,67 @@ struct EpiLogitStats {
           for (int j = 0; j < 32; ++j)
             if (j < nv) d16[j] = uint16_t((j & 1) ? (pk[j >> 1] >> 16) : (pk[j >> 1] & 0xFFFFu));
         }
+      }
+    }
+  }
+
+  __device__ static void apply(const Params& p, const GemmGeom& g, uint32_t taddr, int row, int col0, int nb) {
+    const bool row_ok = row < g.M;
+    const int lane = threadIdx.x & 31;
+    const int nvalid = min(GemmCfg<1>::BN, g.N - col0);
+    int lb = -1;
+    if (row_ok && p.labels) {
+      const int64_t gl = p.labels[row];
+      if (gl >= p.row_begin && gl < p.row_end) lb = int(gl - p.row_begin) - col0;  // offset inside tile
+    }
+    const int blk = row >> 7;
+    int f = 0;
+    if (nb != 0) asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(f) : "l"(p.ref_flag + blk) : "memory");
+    float mx = -INFINITY, yt = 0.f, sum = 0.f, ref;
+    bool has_t = false, own = false, bad = false;
+    if (nb == 0 || !f) {
+      // two passes: this tile is its own reference (the j = 0 tile defines r_i;
+      // an early tile whose row reference is not published yet falls back)
+#pragma unroll 1
+      for (int c = 0; c < 8; ++c) {
+        if (c * 32 >= nvalid) break;
+        uint32_t r[32];
+        ptx::tmem_ld32(taddr + c * 32, r);
+        ptx::tmem_ld_wait();
+        const int nv = nvalid - c * 32;
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (j < nv) mx = fmaxf(mx, __uint_as_float(r[j]));
+        const int off = lb - c * 32;
+        if (off >= 0 && off < 32 && off < nv) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (j == off) yt = __uint_as_float(r[j]);
+          has_t = true;
+        }
+      }
+      ref = mx;
+      if (nb == 0) {
+        if (row_ok) p.row_ref[row] = mx;
+        asm volatile("bar.sync 1, 128;" ::: "memory");  // the 4 epilogue warps of this CTA
+        if (threadIdx.x == 128) {
+          __threadfence();
+          atomicExch(p.ref_flag + blk, 1);
+        }
+      } else {
+        own = true;
+      }
+      float m2;
+      emit(p, taddr, row, row_ok, col0, nvalid, ref, lb, false, m2, yt, has_t, sum);
+    } else {
+      // single pass against the published row reference
+      ref = row_ok ? p.row_ref[row] : 0.f;
+      emit(p, taddr, row, row_ok, col0, nvalid, ref, lb, true, mx, yt, has_t, sum);
+      bad = row_ok && (mx - ref > kMaxRefGap);  // e^{Y - r} overflowed: redo against the tile max
+      if (__ballot_sync(0xffffffffu, bad)) {
+        if (bad) ref = mx;
+        float m2;
+        emit(p, taddr, row, row_ok, col0, nvalid, ref, lb, false, m2, yt, has_t, sum);
       }
     }
     if (row_ok) {

@@ -100,9 +100,13 @@ struct vp_ctx_s {
   int cg = 2;
   // GEMM tile rasterisation and TMA L2 policy per GEMM [logits, dX, dW]
   // (measured: evict_normal on both operands beats first/last hints)
-  int raster[3] = {0, 16, 0};
+  int raster[3] = {0, 16, -4};
   int pol[3] = {0, 0, 0};
   int mc = 1;  // CTA pairs per cluster sharing B by TMA multicast (1 or 2)
+  int nh[3] = {1, 2, 2};  // N halves per tile (2 = 256 x 512 pair tiles) for [logits, dX, dW]
+  // tile shapes actually launched: 512-wide tiles and multicast need CTA pairs
+  int eff_nh(int i) const { return cg == 2 ? nh[i] : 1; }
+  int eff_mc(int i) const { return cg == 2 && eff_nh(i) == 1 ? mc : 1; }
   ncclComm_t comm = nullptr;
   int nranks = 1, rank = 0;
   int* d_err = nullptr;
@@ -221,7 +225,7 @@ void gemm_logits(vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* s, vp_state
   timed_gemm(c, 0, [&] {
     vp::launch_gemm<vp::EpiLogitStats>(c->cg, {b->X, b->ldx, false}, {s->W, s->ldw, false}, int(b->n_tok),
                                        int(st->rows), int(b->h), c->raster[0], ep, c->gemm_sms, c->stream,
-                                       c->pol[0], c->pol[0], c->mc);
+                                       c->pol[0], c->pol[0], c->eff_mc(0));
   });
   ++c->launches;
 }
@@ -231,7 +235,7 @@ void gemm_logits_f32(vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* s, vp_s
   timed_gemm(c, 1, [&] {
     vp::launch_gemm<vp::EpiStoreF32>(c->cg, {b->X, b->ldx, false}, {s->W, s->ldw, false}, int(b->n_tok),
                                      int(st->rows), int(b->h), c->raster[0], ep, c->gemm_sms, c->stream, c->pol[0],
-                                     c->pol[0], c->mc);
+                                     c->pol[0], c->eff_mc(0));
   });
   ++c->launches;
 }
@@ -243,7 +247,7 @@ void gemm_dx(vp_ctx_s* c, vp_state_s* st, const vp_shard_t* s, float* out, int64
   timed_gemm(c, 2, [&] {
     vp::launch_gemm<vp::EpiStoreF32>(c->cg, {st->P, st->ldp, false}, {s->W, s->ldw, true}, int(st->n_tok),
                                      int(st->h), int(st->rows), c->raster[1], ep, c->gemm_sms, c->stream, c->pol[1],
-                                     c->pol[1], c->mc);
+                                     c->pol[1], c->eff_mc(1), c->eff_nh(1));
   });
   ++c->launches;
 }
@@ -251,11 +255,11 @@ void gemm_dx(vp_ctx_s* c, vp_state_s* st, const vp_shard_t* s, float* out, int64
 // out[rows x h] = P^T . Xop   (Xop [T x h] bf16)
 void gemm_dw(vp_ctx_s* c, vp_state_s* st, const void* Xop, int64_t ldx, float* out, int64_t ldo) {
   vp::EpiStoreF32::Params ep{out, ldo, nullptr, 0, nullptr};
-  const int tiles_n = int(ceil_div(st->h, 256));
-  const int raster = c->raster[2] == 0 ? -tiles_n : c->raster[2];
+  const int raster = c->raster[2];
   timed_gemm(c, 3, [&] {
     vp::launch_gemm<vp::EpiStoreF32>(c->cg, {st->P, st->ldp, true}, {Xop, ldx, true}, int(st->rows), int(st->h),
-                                     int(st->n_tok), raster, ep, c->gemm_sms, c->stream, c->pol[2], c->pol[2], c->mc);
+                                     int(st->n_tok), raster, ep, c->gemm_sms, c->stream, c->pol[2], c->pol[2],
+                                     c->eff_mc(2), c->eff_nh(2));
   });
   ++c->launches;
 }
@@ -745,6 +749,10 @@ int vp_ctx_set_option(vp_ctx_t c, const char* key, int64_t value) {
         require(value >= -1 && value <= 2, "vp_ctx_set_option: policy must be -1..2");
         c->pol[idx] = int(value);
       }
+    } else if (k == "nh_dx" || k == "nh_dw") {
+      require(value == 1 || value == 2, "vp_ctx_set_option: nh must be 1 or 2");
+      require(value == 1 || c->cg == 2, "vp_ctx_set_option: 512-wide tiles need cta_group 2");
+      c->nh[k == "nh_dx" ? 1 : 2] = int(value);
     } else if (k == "force_collectives") {
       c->force_collectives = value != 0;
     } else if (k == "multicast") {

@@ -38,6 +38,7 @@ __global__ void fill(__nv_bfloat16* p, int64_t n, float s, uint64_t seed) {
 
 int main(int argc, char** argv) {
   const int mc = getenv("VP_MC") ? atoi(getenv("VP_MC")) : 1;
+  const int nh = getenv("VP_NH") ? atoi(getenv("VP_NH")) : 1;
   if (argc < 5) {
     fprintf(stderr, "usage: gemm_probe <k1|dx|dw> <raster> <pol_a> <pol_b> [iters] [V]\n");
     return 2;
@@ -85,15 +86,15 @@ int main(int argc, char** argv) {
     } else if (kind == "dx") {
       vp::EpiStoreF32::Params ep{out, h, nullptr, 0, nullptr};
       vp::launch_gemm<vp::EpiStoreF32>(2, {P, V, false}, {W, h, true}, int(T), int(h), int(V), raster, ep, nsm, 0, pa,
-                                       pb, mc);
+                                       pb, mc, nh);
     } else if (kind == "dw") {
       vp::EpiStoreF32::Params ep{out, h, nullptr, 0, nullptr};
       vp::launch_gemm<vp::EpiStoreF32>(2, {P, V, true}, {X, h, true}, int(V), int(h), int(T), raster, ep, nsm, 0, pa,
-                                       pb, mc);
+                                       pb, mc, nh);
     } else {  // sq8192: plain 8192^3 K-major GEMM (W as an 8192 x 8192 slice), fp32 out
       vp::EpiStoreF32::Params ep{out, 8192, nullptr, 0, nullptr};
       vp::launch_gemm<vp::EpiStoreF32>(2, {W, 8192, false}, {W + int64_t(8192) * 8192, 8192, false}, 8192, 8192,
-                                       8192, raster, ep, nsm, 0, pa, pb, mc);
+                                       8192, raster, ep, nsm, 0, pa, pb, mc, nh);
     }
   };
   run();
@@ -109,7 +110,7 @@ int main(int argc, char** argv) {
   cudaEventElapsedTime(&ms, a, b);
   ms /= iters;
   const double flops = kind == "sq8192" ? 2.0 * 8192.0 * 8192.0 * 8192.0 : 2.0 * T * h * double(V);
-  printf("mc=%d ", mc);
+  printf("mc=%d nh=%d ", mc, nh);
   printf("probe %s raster=%d pol_a=%d pol_b=%d V=%lld: %.3f ms %.1f TFLOP/s\n", kind.c_str(), raster, pa, pb,
          (long long)V, ms, flops / ms / 1e9);
   return 0;

@@ -47,7 +47,7 @@ __global__ void ref_gemm(const __nv_bfloat16* A, int64_t lda, bool amn, const __
 
 static int failures = 0;
 
-static void check_store(int cg, bool amn, bool bmn, int M, int N, int K, int nsm, int mc = 1) {
+static void check_store(int cg, bool amn, bool bmn, int M, int N, int K, int nsm, int mc = 1, int nh = 1) {
   const int64_t lda = amn ? ((M + 7) / 8 * 8) : ((K + 7) / 8 * 8);
   const int64_t ldb = bmn ? ((N + 7) / 8 * 8) : ((K + 7) / 8 * 8);
   const int64_t asz = amn ? int64_t(K) * lda : int64_t(M) * lda;
@@ -62,7 +62,7 @@ static void check_store(int cg, bool amn, bool bmn, int M, int N, int K, int nsm
   init_bf16<<<256, 256>>>(B, bsz, 91u, 1.f);
   CK(cudaMemset(D, 0xFF, int64_t(M) * N * 4));
   vp::EpiStoreF32::Params ep{D, N, nullptr, 0};
-  vp::launch_gemm<vp::EpiStoreF32>(cg, {A, lda, amn}, {B, ldb, bmn}, M, N, K, 0, ep, nsm, 0, -1, -1, mc);
+  vp::launch_gemm<vp::EpiStoreF32>(cg, {A, lda, amn}, {B, ldb, bmn}, M, N, K, 0, ep, nsm, 0, -1, -1, mc, nh);
   ref_gemm<<<dim3((N + 127) / 128, M), 128>>>(A, lda, amn, B, ldb, bmn, R, M, N, K);
   CK(cudaDeviceSynchronize());
   std::vector<float> d(size_t(M) * N), r(size_t(M) * N);
@@ -76,7 +76,7 @@ static void check_store(int cg, bool amn, bool bmn, int M, int N, int K, int nsm
     maxerr = std::max(maxerr, std::isnan(e) ? 1e30 : e);
     maxref = std::max(maxref, double(std::fabs(r[i])));
   }
-  printf("store cg=%d mc=%d A_%s B_%s M=%d N=%d K=%d : max_abs_err=%.3e max_ref=%.3e bad=%zu %s\n", cg, mc,
+  printf("store cg=%d mc=%d nh=%d A_%s B_%s M=%d N=%d K=%d : max_abs_err=%.3e max_ref=%.3e bad=%zu %s\n", cg, mc, nh,
          amn ? "MN" : "K", bmn ? "MN" : "K", M, N, K, maxerr, maxref, bad, bad ? "FAIL" : "ok");
   if (bad) ++failures;
   cudaFree(A);
@@ -267,6 +267,13 @@ int main(int argc, char** argv) {
     check_stats(cg, 512, 777, 512, nsm, mc);
     check_stats(cg, 1000, 5000, 128, nsm, mc);
   }
+  for (bool amn : {false, true})
+    for (bool bmn : {false, true}) {
+      if (amn && !bmn) continue;
+      check_store(2, amn, bmn, 512, 1024, 512, nsm, 1, 2);
+      check_store(2, amn, bmn, 300, 520, 200, nsm, 1, 2);
+      check_store(2, amn, bmn, 700, 1300, 640, nsm, 1, 2);
+    }
   if (do_bench) {
     for (int cg : {1, 2}) bench_store(cg, false, false, 8192, 8192, 8192, 0, nsm);
     bench_stats(2, 8192, 32000, 4096, nsm);
