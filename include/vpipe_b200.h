@@ -90,8 +90,12 @@ int vp_ctx_reserve(vp_ctx_t ctx, int64_t n_tok, int64_t h, int p);
  * "raster_{logits,dx,dw}" (tile order, see GemmGeom::raster),
  * "policy_{logits,dx,dw}" (TMA L2 policy: -1 default, 0 normal, 1 first, 2 last),
  * "multicast" (1 = CTA-pair clusters, 2 = 4-CTA clusters sharing B by TMA multicast),
- * "nh_dx" / "nh_dw" (1 = 256x256 pair tiles, 2 = 256x512 pair tiles),
- * "force_collectives" (1 = use the NCCL group even with one rank; tests). */
+ * "nh_logits" / "nh_dx" / "nh_dw" (1 = 256x256 pair tiles, 2 = 256x512 pair tiles),
+ * "force_collectives" (1 = use the NCCL group even with one rank; tests),
+ * "overlap_c1" (1 = vp_run_alg2 overlaps the dX / loss all-reduce with pass T
+ * on a high-priority comm stream; default 1), "comm_sms" (SMs left to NCCL
+ * during the overlap and NCCL's maxCTAs; set before vp_ctx_comm_init),
+ * "epi_wait" (GEMM epilogue wait: 0 try_wait loop, 1 nanosleep backoff). */
 int vp_ctx_set_option(vp_ctx_t ctx, const char* key, int64_t value);
 /* Number of kernels this context has launched (evidence counter). */
 int64_t vp_ctx_launch_count(vp_ctx_t ctx);

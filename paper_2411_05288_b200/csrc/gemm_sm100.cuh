@@ -39,6 +39,11 @@ struct GemmGeom {
   // L2 policies of the A / B TMA loads: 0 evict_normal, 1 evict_first,
   // 2 evict_last, -1 = the epilogue's default (see Epi::kAStreams).
   int pol_a = -1, pol_b = -1;
+  // optional probe: CTA 0 writes {clock64, globaltimer} at start and end
+  unsigned long long* prof = nullptr;
+  // how the epilogue warps wait for an accumulator: 0 try_wait loop,
+  // 1 nanosleep backoff (fewer issued instructions while a main loop runs)
+  int epi_wait = 1;
 };
 
 __device__ __forceinline__ uint64_t make_policy(int p, bool dflt_first) {
@@ -130,6 +135,12 @@ __global__ void __launch_bounds__(256, 1)
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&tmA);
     ptx::prefetch_tmap(&tmB);
+    if (g.prof && blockIdx.x == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      g.prof[0] = clock64();
+      g.prof[1] = t;
+    }
   }
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
@@ -245,7 +256,8 @@ __global__ void __launch_bounds__(256, 1)
       tile_coords(gc, t, mc, nb);
       const int mb = mc * MC + int(pair);
       const uint32_t acc = tc % NACC, aph = (tc / NACC) & 1u;
-      ptx::mbar_wait(bar_tfull + 8 * acc, aph);
+      if (g.epi_wait) ptx::mbar_wait_backoff(bar_tfull + 8 * acc, aph);
+      else ptx::mbar_wait(bar_tfull + 8 * acc, aph);
       ptx::tc_fence_after();
       const uint32_t taddr = tmem_base + acc * C::BN + (uint32_t(ew * 32) << 16);
       const int row = mb * C::BM + int(rank) * C::BM_CTA + ew * 32 + lane;
@@ -266,6 +278,12 @@ __global__ void __launch_bounds__(256, 1)
   if (warp == 2) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc<CG>(tmem_base, C::TMEM_COLS);
+  }
+  if (g.prof && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g.prof[2] = clock64();
+    g.prof[3] = t;
   }
 }
 

@@ -103,7 +103,7 @@ struct vp_ctx_s {
   int raster[3] = {0, 16, -4};
   int pol[3] = {0, 0, 0};
   int mc = 1;  // CTA pairs per cluster sharing B by TMA multicast (1 or 2)
-  int nh[3] = {1, 2, 2};  // N halves per tile (2 = 256 x 512 pair tiles) for [logits, dX, dW]
+  int nh[3] = {2, 2, 2};  // N halves per tile (2 = 256 x 512 pair tiles) for [logits, dX, dW]
   // tile shapes actually launched: 512-wide tiles and multicast need CTA pairs
   int eff_nh(int i) const { return cg == 2 ? nh[i] : 1; }
   int eff_mc(int i) const { return cg == 2 && eff_nh(i) == 1 ? mc : 1; }
@@ -126,6 +126,13 @@ struct vp_ctx_s {
     (void)cudaGetLastError();  // drop stale non-sticky errors left by other code
   }
   bool force_collectives = false;  // route exchanges through NCCL even with 1 rank (tests)
+  // C1 overlap (alg2, R/PAPER.md:243/:329): the dX / loss all-reduce runs on a
+  // high-priority comm stream while pass T's dW GEMM keeps the compute stream,
+  // leaving comm_sms SMs free for NCCL's CTAs.
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t ev_ready = nullptr, ev_done = nullptr;
+  bool overlap_c1 = true, reduce_pending = false;
+  int comm_sms = 8;
   bool distributed() const { return comm != nullptr && (nranks > 1 || force_collectives); }
   template <class T>
   T* buf(DevBuf& b, size_t count) {
@@ -225,7 +232,7 @@ void gemm_logits(vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* s, vp_state
   timed_gemm(c, 0, [&] {
     vp::launch_gemm<vp::EpiLogitStats>(c->cg, {b->X, b->ldx, false}, {s->W, s->ldw, false}, int(b->n_tok),
                                        int(st->rows), int(b->h), c->raster[0], ep, c->gemm_sms, c->stream,
-                                       c->pol[0], c->pol[0], c->eff_mc(0));
+                                       c->pol[0], c->pol[0], c->eff_mc(0), c->eff_nh(0));
   });
   ++c->launches;
 }
@@ -461,7 +468,7 @@ void alg2_T(vp_ctx_s* c, vp_state_s* st, vp_stats_t g, const vp_batch_t* b, cons
 }
 
 void alg2_C1(vp_ctx_s* c, const vp_state_t* states, const vp_shard_t* shards, int n, const vp_batch_t* b,
-             double fault_scale, vp_stats_t out, float* gx, int64_t ldgx) {
+             double fault_scale, vp_stats_t out, float* gx, int64_t ldgx, bool reduce = true) {
   require(n >= 1 && states != nullptr, "alg2_barrier_C1: no states");
   check_batch(b);
   for (int k = 0; k < n; ++k) {
@@ -488,14 +495,14 @@ void alg2_C1(vp_ctx_s* c, const vp_state_t* states, const vp_shard_t* shards, in
       S, out.m, out.sum, b->labels, int(b->n_tok), int(b->h), gx, ldgx);
   VP_KCHECK();
   ++c->launches;
-  if (c->distributed()) {
+  if (c->distributed() && reduce) {
     require(ldgx == b->h, "alg2_barrier_C1: grad_x must be dense (ldgx == h) for the all-reduce");
     VP_NCCL(ncclAllReduce(gx, gx, size_t(b->n_tok * b->h), ncclFloat32, ncclSum, c->comm, c->stream));
   }
 }
 
 void loss_of(vp_ctx_s* c, const vp_state_t* states, const vp_shard_t* shards, int n, vp_stats_t g,
-             const vp_batch_t* b, float* loss) {
+             const vp_batch_t* b, float* loss, bool reduce = true) {
   require(n >= 1 && n <= vp::kMaxLocalShards, "loss: bad shard count");
   require(loss != nullptr, "loss: null output");
   vp::LossShards S{};
@@ -509,7 +516,7 @@ void loss_of(vp_ctx_s* c, const vp_state_t* states, const vp_shard_t* shards, in
                                                                        loss);
   VP_KCHECK();
   ++c->launches;
-  if (c->distributed())
+  if (c->distributed() && reduce)
     VP_NCCL(ncclAllReduce(loss, loss, size_t(b->n_tok), ncclFloat32, ncclSum, c->comm, c->stream));
 }
 
@@ -531,6 +538,25 @@ void reduce_partials(vp_ctx_s* c, float* const* partials, int n, int64_t T, int6
   ++c->launches;
 }
 
+// Fork the queued all-reduces (grad_x, loss) onto the comm stream after the
+// compute stream's current work; the compute stream continues with pass T.
+void fork_allreduces(vp_ctx_s* c, float* gx, int64_t n_gx, float* loss, int64_t n_loss) {
+  VP_CUDA(cudaEventRecord(c->ev_ready, c->stream));
+  VP_CUDA(cudaStreamWaitEvent(c->comm_stream, c->ev_ready, 0));
+  VP_NCCL(ncclGroupStart());
+  VP_NCCL(ncclAllReduce(gx, gx, size_t(n_gx), ncclFloat32, ncclSum, c->comm, c->comm_stream));
+  VP_NCCL(ncclAllReduce(loss, loss, size_t(n_loss), ncclFloat32, ncclSum, c->comm, c->comm_stream));
+  VP_NCCL(ncclGroupEnd());
+  VP_CUDA(cudaEventRecord(c->ev_done, c->comm_stream));
+  c->reduce_pending = true;
+}
+
+void join_allreduces(vp_ctx_s* c) {
+  if (!c->reduce_pending) return;
+  VP_CUDA(cudaStreamWaitEvent(c->stream, c->ev_done, 0));
+  c->reduce_pending = false;
+}
+
 void run_alg(int alg, vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* shards, const vp_state_t* states, int n,
              double fault_scale, vp_stats_t out, float* loss, float* gx, int64_t ldgx, float* const* gw,
              int64_t ldgw) {
@@ -538,9 +564,25 @@ void run_alg(int alg, vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* shards
   require(!c->distributed() || n == 1, "run: one shard per rank in an NCCL group");
   if (alg == 2) {
     for (int k = 0; k < n; ++k) alg2_S(c, b, &shards[k], states[k]);
-    alg2_C1(c, states, shards, n, b, fault_scale, out, gx, ldgx);
-    loss_of(c, states, shards, n, out, b, loss);
-    for (int k = 0; k < n; ++k) alg2_T(c, states[k], out, b, &shards[k], gw[k], ldgw);
+    const bool overlap = c->distributed() && c->overlap_c1 && c->comm_stream != nullptr;
+    alg2_C1(c, states, shards, n, b, fault_scale, out, gx, ldgx, /*reduce=*/!overlap);
+    loss_of(c, states, shards, n, out, b, loss, /*reduce=*/!overlap);
+    const int sms = c->gemm_sms;
+    if (overlap) {
+      // C1's only heavy exchange overlaps pass T (T is "arbitrarily delayable")
+      require(ldgx == b->h, "alg2_barrier_C1: grad_x must be dense (ldgx == h) for the all-reduce");
+      fork_allreduces(c, gx, b->n_tok * b->h, loss, b->n_tok);
+      c->gemm_sms = std::max(2, (c->gemm_sms - c->comm_sms) / 2 * 2);
+    }
+    try {
+      for (int k = 0; k < n; ++k) alg2_T(c, states[k], out, b, &shards[k], gw[k], ldgw);
+    } catch (...) {
+      c->gemm_sms = sms;
+      join_allreduces(c);
+      throw;
+    }
+    c->gemm_sms = sms;
+    join_allreduces(c);
   } else {
     for (int k = 0; k < n; ++k) pass_S_common(c, b, &shards[k], states[k]);
     merge_stats(c, states, n, fault_scale, out);
@@ -683,6 +725,9 @@ int vp_ctx_destroy(vp_ctx_t c) {
     c->activate();
     cudaStreamSynchronize(c->stream);
     if (c->comm) ncclCommDestroy(c->comm);
+    if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+    if (c->ev_ready) cudaEventDestroy(c->ev_ready);
+    if (c->ev_done) cudaEventDestroy(c->ev_done);
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
     for (DevBuf* b : {&c->inv, &c->scale, &c->xs, &c->keys, &c->gathered, &c->packed, &c->tmp_m, &c->tmp_s})
       b->release();
@@ -749,10 +794,19 @@ int vp_ctx_set_option(vp_ctx_t c, const char* key, int64_t value) {
         require(value >= -1 && value <= 2, "vp_ctx_set_option: policy must be -1..2");
         c->pol[idx] = int(value);
       }
-    } else if (k == "nh_dx" || k == "nh_dw") {
+    } else if (k == "nh_logits" || k == "nh_dx" || k == "nh_dw") {
       require(value == 1 || value == 2, "vp_ctx_set_option: nh must be 1 or 2");
       require(value == 1 || c->cg == 2, "vp_ctx_set_option: 512-wide tiles need cta_group 2");
-      c->nh[k == "nh_dx" ? 1 : 2] = int(value);
+      c->nh[k == "nh_logits" ? 0 : k == "nh_dx" ? 1 : 2] = int(value);
+    } else if (k == "overlap_c1") {
+      c->overlap_c1 = value != 0;
+    } else if (k == "comm_sms") {
+      require(value >= 1 && value <= 64, "vp_ctx_set_option: comm_sms must be 1..64");
+      require(c->comm == nullptr, "vp_ctx_set_option: comm_sms must be set before vp_ctx_comm_init");
+      c->comm_sms = int(value);
+    } else if (k == "epi_wait") {
+      require(value == 0 || value == 1, "vp_ctx_set_option: epi_wait must be 0 or 1");
+      vp::g_epi_wait = int(value);
     } else if (k == "force_collectives") {
       c->force_collectives = value != 0;
     } else if (k == "multicast") {
@@ -813,9 +867,16 @@ int vp_ctx_comm_init(vp_ctx_t c, int nranks, int rank, const void* id128) {
     c->activate();
     ncclUniqueId id;
     std::memcpy(&id, id128, sizeof(id));
-    VP_NCCL(ncclCommInitRank(&c->comm, nranks, id, rank));
+    ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+    cfg.maxCTAs = c->comm_sms;  // NCCL runs beside the persistent GEMMs on the SMs they leave free
+    VP_NCCL(ncclCommInitRankConfig(&c->comm, nranks, id, rank, &cfg));
     c->nranks = nranks;
     c->rank = rank;
+    int lo = 0, hi = 0;
+    VP_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    VP_CUDA(cudaStreamCreateWithPriority(&c->comm_stream, cudaStreamNonBlocking, hi));
+    VP_CUDA(cudaEventCreateWithFlags(&c->ev_ready, cudaEventDisableTiming));
+    VP_CUDA(cudaEventCreateWithFlags(&c->ev_done, cudaEventDisableTiming));
   });
 }
 

@@ -258,7 +258,10 @@ def test_nccl_exchange_path_with_a_one_rank_group(ctx):
     nctx.comm_init(1, 0, vm.Context.unique_id())
     nctx.set_option("force_collectives", 1)
     assert nctx.comm_info() == (1, 0)
-    for alg in ALGS:
+    cases = [(alg, True) for alg in ALGS] + [("alg2", False)]
+    for alg, overlap in cases:
+        # alg2 forks its C1 all-reduces onto the comm stream beside pass T (overlap_c1)
+        nctx.set_option("overlap_c1", int(overlap))
         fn = {"naive": vm.run_naive, "alg1": vm.run_alg1, "alg2": vm.run_alg2}[alg]
         a = fn(ctx, batch, shards)
         b = fn(nctx, batch, shards)

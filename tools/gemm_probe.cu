@@ -97,6 +97,9 @@ int main(int argc, char** argv) {
                                        8192, raster, ep, nsm, 0, pa, pb, mc, nh);
     }
   };
+  unsigned long long* prof;
+  CK(cudaMallocManaged(&prof, 32));
+  vp::g_gemm_prof = prof;
   run();
   CK(cudaDeviceSynchronize());
   cudaEvent_t a, b;
@@ -109,6 +112,18 @@ int main(int argc, char** argv) {
   float ms;
   cudaEventElapsedTime(&ms, a, b);
   ms /= iters;
+  CK(cudaDeviceSynchronize());
+  {
+    const double cyc = double(prof[2] - prof[0]), ns = double(prof[3] - prof[1]);
+    const int64_t Mx = kind == "dw" ? V : (kind == "sq8192" ? 8192 : T);
+    const int64_t Nx = kind == "k1" ? V : (kind == "sq8192" ? 8192 : h);
+    const int64_t Kx = kind == "k1" ? h : (kind == "dx" ? V : (kind == "dw" ? T : 8192));
+    const double tiles = double((Mx + 255) / 256) * double((Nx + 256 * nh - 1) / (256 * nh));
+    const double ideal = tiles * double((Kx + 63) / 64) * 4.0 * 128.0 * nh;  // MMA issue cycles, all tiles
+    const double par = double(nsm / 2);                                        // CTA pairs
+    printf("  last launch (CTA 0): %.0f cycles in %.3f ms -> %.0f MHz; MMA-ideal %.0f cycles/pair -> %.1f%% of ideal\n",
+           cyc, ns / 1e6, cyc / ns * 1e3, ideal / par, 100.0 * (ideal / par) / cyc);
+  }
   const double flops = kind == "sq8192" ? 2.0 * 8192.0 * 8192.0 * 8192.0 : 2.0 * T * h * double(V);
   printf("mc=%d nh=%d ", mc, nh);
   printf("probe %s raster=%d pol_a=%d pol_b=%d V=%lld: %.3f ms %.1f TFLOP/s\n", kind.c_str(), raster, pa, pb,
