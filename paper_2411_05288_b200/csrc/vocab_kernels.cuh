@@ -80,7 +80,9 @@ __global__ void k_stats_reduce_ref(const float* __restrict__ tile_m, const float
     for (int j = w; j < ntiles; j += 8) {
       const int64_t o = int64_t(j) * ld + row;
       const float mj = tile_m[o];
-      const float sj = tile_s[o] * fast_exp(tile_q[o] - mj);  // relative to the tile max
+      // relative to the tile max, in the log domain: a tile far below the row
+      // reference stores s = 0 (underflow) while e^{q - m} overflows
+      const float sj = expf(logf(tile_s[o]) + (tile_q[o] - mj));
       const float nm = fmaxf(m, mj);
       s = s * fast_exp(m - nm) + sj * fast_exp(mj - nm);
       m = nm;

@@ -225,7 +225,8 @@ def test_headline_shape_properties_and_sampled_rows(ctx):
     assert err.item() <= GRAD_REL_L2
 
 
-def test_extreme_logit_gap_takes_the_overflow_path(ctx):
+@pytest.mark.parametrize("nh_logits", [1, 2])
+def test_extreme_logit_gap_takes_the_overflow_path(ctx, nh_logits):
     # a row whose first vocab tile is ~0 while a later column is 100 nats
     # higher: exp(y - r_i) would overflow, so the row is re-referenced to its
     # max (EpiLogitStats kMaxRefGap path); results must still match the oracle
@@ -241,10 +242,15 @@ def test_extreme_logit_gap_takes_the_overflow_path(ctx):
     g[3], g[7] = 5, 900
     Xb, Wb, batch, Wd = device_case(X, W, g)
     ref = oracle.oracle_output_layer(Xb, g, Wb)
+    # 256- or 512-wide logits tiles change which tiles see the row reference
+    # (and which sit > 87 nats below it: underflowed exp-sums)
+    tctx = vm.Context(0)
+    tctx.set_option("nh_logits", nh_logits)
     for alg in ALGS:
         for p in (1, 2):
-            res, _ = run_device(ctx, alg, batch, Wd, p, h)
-            assert_parity(res, ref, f"gap {alg} p={p}")
+            res, _ = run_device(tctx, alg, batch, Wd, p, h)
+            assert_parity(res, ref, f"gap {alg} p={p} nh={nh_logits}")
+    tctx.close()
 
 
 def test_nccl_exchange_path_with_a_one_rank_group(ctx):
