@@ -95,7 +95,10 @@ int vp_ctx_reserve(vp_ctx_t ctx, int64_t n_tok, int64_t h, int p);
  * "overlap_c1" (1 = vp_run_alg2 overlaps the dX / loss all-reduce with pass T
  * on a high-priority comm stream; default 1), "comm_sms" (SMs left to NCCL
  * during the overlap and NCCL's maxCTAs; set before vp_ctx_comm_init),
- * "epi_wait" (GEMM epilogue wait: 0 try_wait loop, 1 nanosleep backoff). */
+ * "epi_wait" (GEMM epilogue wait: 0 try_wait loop, 1 nanosleep backoff),
+ * "accumulate_grad_w" (1 = the T passes add dW_k into grad_w: gradient
+ * accumulation, or tied input/output embeddings sharing the shard's buffer
+ * with vp_input_backward(accumulate=1); R/PAPER.md:333). */
 int vp_ctx_set_option(vp_ctx_t ctx, const char* key, int64_t value);
 /* Number of kernels this context has launched (evidence counter). */
 int64_t vp_ctx_launch_count(vp_ctx_t ctx);

@@ -303,6 +303,7 @@ struct EpiStoreF32 {
     float* tile_max;         // optional [tiles_n x ld_stats]
     int64_t ld_stats;
     const float* row_scale;  // optional per-row factor applied on store
+    int accumulate = 0;      // out += D instead of out = D (gradient accumulation)
   };
   __device__ static void apply(const Params& p, const GemmGeom& g, uint32_t taddr, int row, int col0, int nb) {
     const bool row_ok = row < g.M;
@@ -331,13 +332,22 @@ struct EpiStoreF32 {
         if (nv >= 32 && vec) {
           float4* d4 = reinterpret_cast<float4*>(dst + c * 32);
 #pragma unroll
-          for (int j = 0; j < 8; ++j)
-            d4[j] = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
-                                __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+          for (int j = 0; j < 8; ++j) {
+            float4 v = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
+                                   __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
+            if (p.accumulate) {
+              const float4 o = d4[j];
+              v.x += o.x;
+              v.y += o.y;
+              v.z += o.z;
+              v.w += o.w;
+            }
+            d4[j] = v;
+          }
         } else {
 #pragma unroll
           for (int j = 0; j < 32; ++j)
-            if (j < nv) dst[c * 32 + j] = __uint_as_float(r[j]);
+            if (j < nv) dst[c * 32 + j] = __uint_as_float(r[j]) + (p.accumulate ? dst[c * 32 + j] : 0.f);
         }
       }
     }

@@ -133,6 +133,9 @@ struct vp_ctx_s {
   cudaEvent_t ev_ready = nullptr, ev_done = nullptr;
   bool overlap_c1 = true, reduce_pending = false;
   int comm_sms = 8;
+  // dW passes add into grad_w instead of overwriting it (gradient accumulation
+  // across microbatches; tied input/output embeddings sharing one dE/dW buffer)
+  bool accumulate_dw = false;
   bool distributed() const { return comm != nullptr && (nranks > 1 || force_collectives); }
   template <class T>
   T* buf(DevBuf& b, size_t count) {
@@ -261,7 +264,7 @@ void gemm_dx(vp_ctx_s* c, vp_state_s* st, const vp_shard_t* s, float* out, int64
 
 // out[rows x h] = P^T . Xop   (Xop [T x h] bf16)
 void gemm_dw(vp_ctx_s* c, vp_state_s* st, const void* Xop, int64_t ldx, float* out, int64_t ldo) {
-  vp::EpiStoreF32::Params ep{out, ldo, nullptr, 0, nullptr};
+  vp::EpiStoreF32::Params ep{out, ldo, nullptr, 0, nullptr, c->accumulate_dw ? 1 : 0};
   const int raster = c->raster[2];
   timed_gemm(c, 3, [&] {
     vp::launch_gemm<vp::EpiStoreF32>(c->cg, {st->P, st->ldp, true}, {Xop, ldx, true}, int(st->rows), int(st->h),
@@ -798,6 +801,8 @@ int vp_ctx_set_option(vp_ctx_t c, const char* key, int64_t value) {
       require(value == 1 || value == 2, "vp_ctx_set_option: nh must be 1 or 2");
       require(value == 1 || c->cg == 2, "vp_ctx_set_option: 512-wide tiles need cta_group 2");
       c->nh[k == "nh_logits" ? 0 : k == "nh_dx" ? 1 : 2] = int(value);
+    } else if (k == "accumulate_grad_w") {
+      c->accumulate_dw = value != 0;
     } else if (k == "overlap_c1") {
       c->overlap_c1 = value != 0;
     } else if (k == "comm_sms") {
