@@ -281,3 +281,31 @@ def test_nccl_exchange_path_with_a_one_rank_group(ctx):
     nctx.sync()
     assert torch.equal(t, torch.arange(16, dtype=torch.float32, device="cuda"))
     nctx.close()
+
+
+def test_tied_embeddings_accumulate_into_one_shard_gradient(ctx):
+    # Tied input/output embeddings on the same shard (R/PAPER.md:333): the
+    # output layer's dW_k and the input layer's dE_k land in ONE fp32 buffer
+    # (accumulate_grad_w + input_backward(accumulate=True)); also gradient
+    # accumulation over two microbatches.
+    X, W, g = oracle.random_instance(48, 32, 256, 6)
+    Xb, Wb, batch, Wd = device_case(X, W, g)
+    toks = torch.from_numpy(np.asarray(g[::-1].copy(), np.int64)).cuda()
+    grad_in = torch.randn(48, 32, device="cuda").to(torch.bfloat16)
+    shards = vm.shard_weights(Wd, 2)
+    ref_out = vm.run_alg2(ctx, batch, shards)
+    ref_in = [vm.input_backward(ctx, grad_in, toks, s) for s in shards]
+    actx = vm.Context(0)
+    actx.set_option("accumulate_grad_w", 1)
+    bufs = [torch.zeros(s.rows(), 32, dtype=torch.float32, device="cuda") for s in shards]
+    outs = vm._alloc_outputs(actx, batch, shards)
+    outs = (outs[0], outs[1], bufs, outs[3])
+    for _ in range(2):  # two microbatches into the same buffers
+        vm.run_alg2(actx, batch, shards, outputs=outs)
+    for s, b in zip(shards, bufs):
+        vm.input_backward(actx, grad_in, toks, s, out=b, accumulate=True)
+    actx.sync()
+    for k in range(2):
+        want = 2 * ref_out.grad_w[k] + ref_in[k]
+        assert torch.allclose(bufs[k], want, rtol=1e-4, atol=1e-5), k
+    actx.close()
