@@ -263,7 +263,10 @@ __global__ void __launch_bounds__(256, 1)
       const int row = mb * C::BM + int(rank) * C::BM_CTA + ew * 32 + lane;
 #pragma unroll 1
       for (int hh = 0; hh < NH; ++hh)
-        Epi::apply(ep, g, taddr + hh * C::BN, row, nb * C::BN_TILE + hh * C::BN, nb * NH + hh);
+        // a 512-wide tile's second half may lie wholly past N (ragged last
+        // tile): it has no columns, no stats slot and nothing to store
+        if (nb * C::BN_TILE + hh * C::BN < g.N)
+          Epi::apply(ep, g, taddr + hh * C::BN, row, nb * C::BN_TILE + hh * C::BN, nb * NH + hh);
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) {

@@ -309,3 +309,51 @@ def test_tied_embeddings_accumulate_into_one_shard_gradient(ctx):
         want = 2 * ref_out.grad_w[k] + ref_in[k]
         assert torch.allclose(bufs[k], want, rtol=1e-4, atol=1e-5), k
     actx.close()
+
+
+@pytest.mark.parametrize("rows", [96, 200, 256, 300, 512, 520, 768, 1000])
+def test_shard_widths_around_the_512_wide_tile(ctx, rows):
+    # 256x512 pair tiles: a shard whose width leaves the last tile's second
+    # 256-column half wholly past the shard (rows mod 512 in (0, 256]) must not
+    # touch that half's stats slots (the smoke() instance: 96 tokens, h=64,
+    # V=512 over 2 shards, U[-1,1] operands).
+    for seed in (0, 1):
+        X, W, g = oracle.random_instance(96, 64, 2 * rows, seed)
+        Xb, Wb, batch, Wd = device_case(X, W, g)
+        ref = oracle.oracle_output_layer(Xb, g, Wb, want_softmax=False)
+        for alg in ALGS:
+            res, _ = run_device(ctx, alg, batch, Wd, 2, 64, with_softmax=False)
+            assert_parity(res, ref, f"rows={rows} seed={seed} {alg}")
+
+
+def test_memcheck_of_a_ragged_alg2_step():
+    # compute-sanitizer memcheck over one ragged alg2 step + the input layer:
+    # no out-of-bounds global access from any kernel (tcgen05 GEMM epilogues,
+    # stats, scatter).
+    import os
+    import shutil
+    import subprocess
+    import sys
+    san = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+    if not os.path.exists(san):
+        pytest.skip("compute-sanitizer not found")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = (
+        "import sys; sys.path[:0] = [%r, %r]\n"
+        "import numpy as np, torch, oracle\n"
+        "from paper_2411_05288_b200 import vocab_math as vm\n"
+        "ctx = vm.Context(0)\n"
+        "X, W, g = oracle.random_instance(96, 64, 600, 0)\n"
+        "Xd = torch.from_numpy(X.astype(np.float32)).to(torch.bfloat16).cuda()\n"
+        "Wd = torch.from_numpy(W.astype(np.float32)).to(torch.bfloat16).cuda()\n"
+        "b = vm.TokenBatch(Xd, torch.from_numpy(g).cuda())\n"
+        "for fn in (vm.run_alg2, vm.run_alg1, vm.run_naive):\n"
+        "    fn(ctx, b, vm.shard_weights(Wd, 2))\n"
+        "s = vm.shard_weights(Wd, 3)[1]\n"
+        "vm.input_forward(ctx, b.labels, s); vm.input_backward(ctx, Xd, b.labels, s)\n"
+        "ctx.sync(); ctx.close(); print('memcheck-run-ok')\n" % (root, os.path.join(root, "oracle")))
+    r = subprocess.run([san, "--tool", "memcheck", "--error-exitcode", "7", sys.executable, "-c", script],
+                       capture_output=True, text=True, timeout=600)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0 and "memcheck-run-ok" in out, out[-4000:]
+    assert "ERROR SUMMARY: 0 errors" in out, out[-4000:]
