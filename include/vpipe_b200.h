@@ -96,6 +96,8 @@ int vp_ctx_reserve(vp_ctx_t ctx, int64_t n_tok, int64_t h, int p);
  * on a high-priority comm stream; default 1), "comm_sms" (SMs left to NCCL
  * during the overlap and NCCL's maxCTAs; set before vp_ctx_comm_init),
  * "epi_wait" (GEMM epilogue wait: 0 try_wait loop, 1 nanosleep backoff),
+ * "tma_store" (1 = GEMM epilogues store through smem staging + TMA, the
+ * default; 0 = per-thread st.global; process-wide),
  * "accumulate_grad_w" (1 = the T passes add dW_k into grad_w: gradient
  * accumulation, or tied input/output embeddings sharing the shard's buffer
  * with vp_input_backward(accumulate=1); R/PAPER.md:333). */

@@ -48,6 +48,38 @@ inline CUtensorMap make_tmap_bf16(const void* ptr, uint64_t inner, uint64_t oute
   return m;
 }
 
+// 2-D tensor map of the epilogue's TMA stores: row-major [outer x inner]
+// elements of `esize` bytes, SWIZZLE_128B boxes of [32 rows x 128 B].
+inline CUtensorMap make_store_map(const void* ptr, CUtensorMapDataType dt, int esize, uint64_t inner,
+                                  uint64_t outer, uint64_t ld) {
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {inner, outer};
+  const cuuint64_t strides[1] = {ld * uint64_t(esize)};
+  const cuuint32_t box[2] = {cuuint32_t(128 / esize), 32};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = get_encode_fn()(&m, dt, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                               CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled (store) failed: " + std::to_string(int(r)));
+  return m;
+}
+
+inline int g_tma_store = 1;  // epilogue stores through TMA when the output allows it (16-B aligned rows)
+
+inline bool tma_store_ok(const void* p, int64_t ld, int esize) {
+  return g_tma_store && (reinterpret_cast<uintptr_t>(p) & 15) == 0 && (ld * esize) % 16 == 0;
+}
+inline void prepare_store(EpiStoreF32::Params& ep, int M, int N) {
+  ep.use_tma = tma_store_ok(ep.out, ep.ldo, 4);
+  if (ep.use_tma)
+    ep.map = make_store_map(ep.out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, uint64_t(N), uint64_t(M), uint64_t(ep.ldo));
+}
+inline void prepare_store(EpiLogitStats::Params& ep, int M, int N) {
+  ep.use_tma = tma_store_ok(ep.P, ep.ldp, 2);
+  if (ep.use_tma)
+    ep.map = make_store_map(ep.P, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, uint64_t(N), uint64_t(M), uint64_t(ep.ldp));
+}
+
 // One GEMM operand: row-major storage `ptr` with leading dimension `ld`.
 //   K-major : storage [rows x K]  (A: rows = M, B: rows = N)
 //   MN-major: storage [K x rows]
@@ -128,7 +160,9 @@ inline void launch_gemm_t(const Operand& A, const Operand& B, int M, int N, int 
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta, tb, g, ep);
+  typename Epi::Params epc = ep;
+  prepare_store(epc, M, N);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta, tb, g, epc);
   if (e != cudaSuccess) throw std::runtime_error(std::string("gemm launch: ") + cudaGetErrorString(e));
 }
 

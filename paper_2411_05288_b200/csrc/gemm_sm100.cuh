@@ -68,8 +68,9 @@ struct GemmCfg {
   static constexpr int A_BYTES = BM_CTA * BK * 2;
   static constexpr int B_BYTES = B_ROWS * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STG_BYTES = 4 * 8192;  // epilogue TMA-store staging: 2 x 4 KB per epilogue warp
   static constexpr int BAR_BYTES = 8 * (2 * STAGES + 4) + 16;
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + BAR_BYTES + 1024;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + STG_BYTES + BAR_BYTES + 1024;
   static constexpr int THREADS = 256;
   static constexpr int TMEM_COLS = 512;
 };
@@ -94,6 +95,64 @@ __device__ __forceinline__ void tile_coords(const GemmGeom& g, int t, int& mb, i
   }
 }
 
+// Per-warp staging: two 4 KB boxes, double-buffered against the async stores.
+struct Stager {
+  uint32_t base;
+  uint32_t k = 0;
+  __device__ explicit Stager(uint32_t b) : base(b) {}
+  // next free box (the store issued two boxes ago has finished reading it)
+  __device__ __forceinline__ uint32_t next() {
+    if ((threadIdx.x & 31) == 0) ptx::bulk_wait_read<1>();
+    __syncwarp();
+    const uint32_t b = base + (k & 1u) * 4096u;
+    ++k;
+    return b;
+  }
+  // smem address of 16-byte chunk q of this thread's row (row = lane)
+  __device__ static __forceinline__ uint32_t chunk(uint32_t box, int q) {
+    const uint32_t r = threadIdx.x & 31;
+    return box + r * 128u + ((uint32_t(q) ^ (r & 7u)) << 4);
+  }
+  __device__ __forceinline__ void store(const CUtensorMap* m, uint32_t box, int c0, int c1, bool add = false) {
+    ptx::fence_proxy_async_smem();
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) {
+      if (add) ptx::tma_reduce_add_2d(m, box, c0, c1);
+      else ptx::tma_store_2d(m, box, c0, c1);
+      ptx::bulk_commit();
+    }
+  }
+  // all issued stores complete (global writes done)
+  __device__ __forceinline__ void drain() {
+    if ((threadIdx.x & 31) == 0) ptx::bulk_wait<0>();
+    __syncwarp();
+  }
+};
+
+// Walk the nch 32-column chunks of this warp's accumulator rows with the
+// TMEM load of chunk c+1 in flight while chunk c is processed: f(regs, c).
+template <class F>
+__device__ __forceinline__ void tmem_chunks(uint32_t taddr, int nch, F&& f) {
+  uint32_t ra[32], rb[32];
+  ptx::tmem_ld32(taddr, ra);
+  ptx::tmem_ld_wait();
+  ptx::tmem_pin(ra);
+#pragma unroll 1
+  for (int c = 0; c < nch; c += 2) {
+    if (c + 1 < nch) ptx::tmem_ld32(taddr + (c + 1) * 32, rb);
+    f(ra, c);
+    if (c + 1 >= nch) break;
+    ptx::tmem_ld_wait();
+    ptx::tmem_pin(rb);
+    if (c + 2 < nch) ptx::tmem_ld32(taddr + (c + 2) * 32, ra);
+    f(rb, c + 1);
+    if (c + 2 < nch) {
+      ptx::tmem_ld_wait();
+      ptx::tmem_pin(ra);
+    }
+  }
+}
+
 // MC = CTA pairs per cluster along M (CG == 2 only).  MC == 2: a 4-CTA
 // cluster computes a 512 x 256 "cluster tile" as two pair tiles (m, n) and
 // (m+1, n) that need the same B rows; each CTA loads HALF of its B rows and
@@ -103,7 +162,7 @@ __device__ __forceinline__ void tile_coords(const GemmGeom& g, int t, int& mb, i
 template <int CG, bool A_MN, bool B_MN, class Epi, int MC = 1, int NH = 1>
 __global__ void __launch_bounds__(256, 1)
     gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                      const GemmGeom g, const typename Epi::Params ep) {
+                      const GemmGeom g, const __grid_constant__ typename Epi::Params ep) {
   using C = GemmCfg<CG, NH>;
   static_assert(MC == 1 || (MC == 2 && CG == 2), "multicast clusters are built from CTA pairs");
   static_assert(NH == 1 || (NH == 2 && CG == 2 && MC == 1), "512-wide tiles: CTA pairs without multicast");
@@ -114,11 +173,13 @@ __global__ void __launch_bounds__(256, 1)
   const uint32_t sbase = ptx::smem_u32(smem);
   const uint32_t sA = sbase;
   const uint32_t sB = sbase + C::STAGES * C::A_BYTES;
-  const uint32_t bar_full = sbase + C::STAGES * C::STAGE_BYTES;
+  const uint32_t stg = sbase + C::STAGES * C::STAGE_BYTES;  // 1024-aligned
+  const uint32_t bar_full = stg + C::STG_BYTES;
   const uint32_t bar_empty = bar_full + 8 * C::STAGES;
   const uint32_t bar_tfull = bar_empty + 8 * C::STAGES;
   const uint32_t bar_tempty = bar_tfull + 16;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::STAGES * C::STAGE_BYTES + 8 * (2 * C::STAGES + 4));
+  uint32_t* tmem_slot =
+      reinterpret_cast<uint32_t*>(smem + C::STAGES * C::STAGE_BYTES + C::STG_BYTES + 8 * (2 * C::STAGES + 4));
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t crank = CL > 1 ? ptx::cluster_ctarank() : 0u;  // rank in cluster
@@ -211,7 +272,85 @@ __global__ void __launch_bounds__(256, 1)
         }
       }
     }
-  } else if (warp == 1 && lane == 0 && rank == 0) {
+  } else if (NH == 2 && warp == 1 && lane == 0 && rank == 0) {
+    // ===== MMA issuer, 512-wide tiles: staggered N halves =====
+    // The tile's two 256-column halves are separate accumulators (TMEM
+    // columns [0,256) and [256,512)) released separately by the epilogue.
+    // Around tile boundaries the halves run D k-blocks apart, so each half's
+    // epilogue overlaps MMAs of the other half instead of idling the tensor
+    // pipe:
+    //   tile end   : H0(K-D..K-1), commit full[0] | H1(K-D..K-1), commit full[1]
+    //                 (epilogue of half 0 runs under H1's last D k-blocks)
+    //   tile start : wait empty[0], H0(0..D-1) | wait empty[1], H1(0..D-1)
+    //                 (epilogue of half 1 runs under H0's first D k-blocks)
+    // D <= STAGES (the D k-blocks stay resident in smem until H1 has read
+    // them) and D <= K/2 (start and end groups disjoint).
+    constexpr uint32_t idesc = ptx::idesc_bf16_f32(C::BM, C::BN, A_MN, B_MN);
+    const int D = min(C::STAGES, g.num_kb / 2);
+    uint32_t it0 = 0, tc = 0;
+    auto issue = [&](int kb, int hh) {
+      const uint32_t s = (it0 + kb) % C::STAGES;
+      const uint32_t a_base = sA + s * C::A_BYTES, bh = sB + s * C::B_BYTES + hh * C::B_HALF_ROWS * 128;
+      const uint32_t d = tmem_base + hh * C::BN;
+#pragma unroll
+      for (int kk = 0; kk < C::BK / C::UK; ++kk) {
+        const uint64_t ad = A_MN ? ptx::sdesc_sw128(a_base + kk * 2048, 8192, 1024)
+                                 : ptx::sdesc_sw128(a_base + kk * 32, 16, 1024);
+        const uint64_t bd = B_MN ? ptx::sdesc_sw128(bh + kk * 2048, 8192, 1024) : ptx::sdesc_sw128(bh + kk * 32, 16, 1024);
+        ptx::mma_bf16<CG>(d, ad, bd, idesc, (kb | kk) != 0 ? 1u : 0u);
+      }
+    };
+    // probe (g.prof, CTA 0): cycles the issuer spent waiting for smem stages / accumulators
+    const bool probe = g.prof != nullptr && blockIdx.x == 0;
+    unsigned long long w_full = 0, w_acc = 0;
+    auto wait_full = [&](int kb) {
+      const uint32_t it = it0 + kb;
+      const unsigned long long c0 = probe ? clock64() : 0;
+      ptx::mbar_wait(bar_full + 8 * (it % C::STAGES), (it / C::STAGES) & 1u);
+      if (probe) w_full += clock64() - c0;
+      ptx::tc_fence_after();
+    };
+    auto release = [&](int kb) { ptx::mma_commit<CG>(bar_empty + 8 * ((it0 + kb) % C::STAGES), pair_mask); };
+    auto wait_acc = [&](int hh) {
+      const unsigned long long c0 = probe ? clock64() : 0;
+      ptx::mbar_wait_cluster(bar_tempty + 8 * hh, (tc & 1u) ^ 1u);
+      if (probe) w_acc += clock64() - c0;
+      ptx::tc_fence_after();
+    };
+    const int K = g.num_kb;
+    for (int t = cluster; t < num_tiles; t += nclusters, ++tc, it0 += uint32_t(K)) {
+      wait_acc(0);
+      for (int kb = 0; kb < D; ++kb) {
+        wait_full(kb);
+        issue(kb, 0);
+      }
+      wait_acc(1);
+      for (int kb = 0; kb < D; ++kb) {
+        issue(kb, 1);
+        release(kb);
+      }
+      for (int kb = D; kb < K - D; ++kb) {
+        wait_full(kb);
+        issue(kb, 0);
+        issue(kb, 1);
+        release(kb);
+      }
+      for (int kb = K - D; kb < K; ++kb) {
+        wait_full(kb);
+        issue(kb, 0);
+      }
+      ptx::mma_commit<CG>(bar_tfull, pair_mask);
+      for (int kb = K - D; kb < K; ++kb) {
+        issue(kb, 1);
+        release(kb);
+      }
+      ptx::mma_commit<CG>(bar_tfull + 8, pair_mask);
+    }
+    if (probe) {
+      g.prof[4] = w_full;
+      g.prof[5] = w_acc;
+    }
+  } else if (NH == 1 && warp == 1 && lane == 0 && rank == 0) {
     // ===== MMA issuer (pair leader, one thread) =====
     constexpr uint32_t idesc = ptx::idesc_bf16_f32(C::BM, C::BN, A_MN, B_MN);
     constexpr uint16_t all_mask = uint16_t((1u << CL) - 1u);
@@ -250,11 +389,38 @@ __global__ void __launch_bounds__(256, 1)
   } else if (warp >= 4) {
     // ===== epilogue =====
     const int ew = warp - 4;
+    Stager sg(stg + uint32_t(ew) * 8192u);
     uint32_t tc = 0;
+    unsigned long long epi_wait_cyc = 0, epi_work_cyc = 0;  // probe (NH == 2, CTA 0, warp 4)
     for (int t = cluster; t < num_tiles; t += nclusters, ++tc) {
       int mc, nb;
       tile_coords(gc, t, mc, nb);
       const int mb = mc * MC + int(pair);
+      if constexpr (NH == 2) {
+        // halves complete (and are released) separately: see the staggered issuer
+        const int row = mb * C::BM + int(rank) * C::BM_CTA + ew * 32 + lane;
+        const bool probe = g.prof != nullptr && blockIdx.x == 0 && ew == 0;
+#pragma unroll 1
+        for (int hh = 0; hh < 2; ++hh) {
+          const unsigned long long c0 = probe ? clock64() : 0;
+          if (g.epi_wait) ptx::mbar_wait_backoff(bar_tfull + 8 * hh, tc & 1u);
+          else ptx::mbar_wait(bar_tfull + 8 * hh, tc & 1u);
+          ptx::tc_fence_after();
+          const unsigned long long c1 = probe ? clock64() : 0;
+          const uint32_t taddr = tmem_base + hh * C::BN + (uint32_t(ew * 32) << 16);
+          // a 512-wide tile's second half may lie wholly past N (ragged last
+          // tile): it has no columns, no stats slot and nothing to store
+          if (nb * C::BN_TILE + hh * C::BN < g.N) Epi::apply(ep, g, taddr, row, nb * C::BN_TILE + hh * C::BN, nb * 2 + hh, sg);
+          if (probe && lane == 0) {
+            epi_wait_cyc += c1 - c0;
+            epi_work_cyc += clock64() - c1;
+          }
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive_remote(bar_tempty + 8 * hh, leader);
+        }
+        continue;
+      }
       const uint32_t acc = tc % NACC, aph = (tc / NACC) & 1u;
       if (g.epi_wait) ptx::mbar_wait_backoff(bar_tfull + 8 * acc, aph);
       else ptx::mbar_wait(bar_tfull + 8 * acc, aph);
@@ -266,13 +432,18 @@ __global__ void __launch_bounds__(256, 1)
         // a 512-wide tile's second half may lie wholly past N (ragged last
         // tile): it has no columns, no stats slot and nothing to store
         if (nb * C::BN_TILE + hh * C::BN < g.N)
-          Epi::apply(ep, g, taddr + hh * C::BN, row, nb * C::BN_TILE + hh * C::BN, nb * NH + hh);
+          Epi::apply(ep, g, taddr + hh * C::BN, row, nb * C::BN_TILE + hh * C::BN, nb * NH + hh, sg);
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) {
         if constexpr (CG == 1) ptx::mbar_arrive(bar_tempty + 8 * acc);
         else ptx::mbar_arrive_remote(bar_tempty + 8 * acc, leader);
       }
+    }
+    sg.drain();
+    if (g.prof != nullptr && blockIdx.x == 0 && ew == 0 && lane == 0) {
+      g.prof[6] = epi_wait_cyc;
+      g.prof[7] = epi_work_cyc;
     }
   }
   __syncwarp();
@@ -294,6 +465,15 @@ __global__ void __launch_bounds__(256, 1)
 // Epilogues.  apply() runs on one epilogue warp: thread `lane` owns
 // accumulator row `row` (may be >= M: masked), columns [col0, col0 + 256).
 // tcgen05.ld is warp-collective, so loads stay outside row masks.
+//
+// Stores go through a per-warp smem staging box and TMA (Params::use_tma):
+// the warp writes a 32-row x 128-byte box in the SWIZZLE_128B layout (each
+// thread one row, 16-byte chunks XOR-permuted by row: bank-conflict free)
+// and one lane issues cp.async.bulk.tensor.  The global writes are full
+// lines and asynchronous, so the epilogue finishes (and releases its TMEM
+// accumulator) in a fraction of the time per-row st.global takes; rows and
+// columns outside the tensor are clipped by the TMA unit.  use_tma = 0 keeps
+// direct stores (unaligned buffers).
 // ---------------------------------------------------------------------------
 
 // D -> fp32 out (row-major, ldo), optionally also the per-(row, tile) max of
@@ -307,31 +487,49 @@ struct EpiStoreF32 {
     int64_t ld_stats;
     const float* row_scale;  // optional per-row factor applied on store
     int accumulate = 0;      // out += D instead of out = D (gradient accumulation)
+    int use_tma = 0;         // stores through `map` (fp32 [M x N], 32 x 32 boxes, SWIZZLE_128B)
+    CUtensorMap map;
   };
-  __device__ static void apply(const Params& p, const GemmGeom& g, uint32_t taddr, int row, int col0, int nb) {
+  __device__ static void apply(const Params& p, const GemmGeom& g, uint32_t taddr, int row, int col0, int nb,
+                               Stager& sg) {
     const bool row_ok = row < g.M;
     const int nvalid = min(GemmCfg<1>::BN, g.N - col0);
-    float* dst = p.out + int64_t(row) * p.ldo + col0;
-    const bool vec = ((p.ldo & 3) == 0) && ((reinterpret_cast<uintptr_t>(p.out) & 15) == 0);
-    float mx = -INFINITY;
+    const int nch = (nvalid + 31) / 32;
     const float rs = (p.row_scale && row_ok) ? p.row_scale[row] : 1.f;
-#pragma unroll 1
-    for (int c = 0; c < 8; ++c) {
-      if (c * 32 >= nvalid) break;  // warp-uniform
-      uint32_t r[32];
-      ptx::tmem_ld32(taddr + c * 32, r);
-      ptx::tmem_ld_wait();
-      const int nv = nvalid - c * 32;
-      if (p.row_scale) {
+    float mx = -INFINITY;
+    const int row0 = row - int(threadIdx.x & 31);
+    if (p.use_tma) {
+      tmem_chunks(taddr, nch, [&](uint32_t (&r)[32], int c) {
+        if (p.row_scale) {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) * rs);
-      }
-      if (p.tile_max) {
+          for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) * rs);
+        }
+        if (p.tile_max) {
+          const int nv = nvalid - c * 32;
 #pragma unroll
-        for (int j = 0; j < 32; ++j)
-          if (j < nv) mx = fmaxf(mx, __uint_as_float(r[j]));
-      }
-      if (row_ok) {
+          for (int j = 0; j < 32; ++j)
+            if (j < nv) mx = fmaxf(mx, __uint_as_float(r[j]));
+        }
+        const uint32_t box = sg.next();
+#pragma unroll
+        for (int q = 0; q < 8; ++q) ptx::st_shared_v4(Stager::chunk(box, q), r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
+        sg.store(&p.map, box, col0 + c * 32, row0, p.accumulate != 0);
+      });
+    } else {
+      float* dst = p.out + int64_t(row) * p.ldo + col0;
+      const bool vec = ((p.ldo & 3) == 0) && ((reinterpret_cast<uintptr_t>(p.out) & 15) == 0);
+      tmem_chunks(taddr, nch, [&](uint32_t (&r)[32], int c) {
+        const int nv = nvalid - c * 32;
+        if (p.row_scale) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) * rs);
+        }
+        if (p.tile_max) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (j < nv) mx = fmaxf(mx, __uint_as_float(r[j]));
+        }
+        if (!row_ok) return;
         if (nv >= 32 && vec) {
           float4* d4 = reinterpret_cast<float4*>(dst + c * 32);
 #pragma unroll
@@ -352,7 +550,7 @@ struct EpiStoreF32 {
           for (int j = 0; j < 32; ++j)
             if (j < nv) dst[c * 32 + j] = __uint_as_float(r[j]) + (p.accumulate ? dst[c * 32 + j] : 0.f);
         }
-      }
+      });
     }
     if (p.tile_max && row_ok) p.tile_max[int64_t(nb) * p.ld_stats + row] = mx;
   }
@@ -392,23 +590,40 @@ struct EpiLogitStats {
     int* bad_list;          // [M]
     int* fix_count;         // (32-row group, tile) pairs stored relative to their own max
     int2* fix_list;         // [ceil(M/32) x tiles_n]
+    int use_tma = 0;        // P stored through `map` (bf16 [M x N], 32 x 64 boxes, SWIZZLE_128B)
+    CUtensorMap map;
   };
+  // max of the valid columns and the label logit (first pass of a two-pass tile)
+  __device__ static void scan(uint32_t taddr, int nvalid, int lb, float& mx, float& yt, bool& has_t) {
+    tmem_chunks(taddr, (nvalid + 31) / 32, [&](uint32_t (&r)[32], int c) {
+      const int nv = nvalid - c * 32;
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (j < nv) mx = fmaxf(mx, __uint_as_float(r[j]));
+      const int off = lb - c * 32;
+      if (off >= 0 && off < 32 && off < nv) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (j == off) yt = __uint_as_float(r[j]);
+        has_t = true;
+      }
+    });
+  }
   // One pass over the 256 accumulator columns of this row: P = bf16(e^{Y - ref}),
   // s = sum e^{Y - ref}; with track = true it also takes the tile max and the
   // label logit (the single-pass path, where ref = r_i is known up front).
   __device__ static void emit(const Params& p, uint32_t taddr, int row, bool row_ok, int col0, int nvalid,
-                              float ref, int lb, bool track, float& mx, float& yt, bool& has_t, float& sum) {
+                              float ref, int lb, bool track, float& mx, float& yt, bool& has_t, float& sum,
+                              Stager& sg) {
     constexpr float kLog2e = 1.4426950408889634f;
     const float refs = ref * kLog2e;
     sum = 0.f;
+    const int row0 = row - int(threadIdx.x & 31);
     __nv_bfloat16* dst = p.P + int64_t(row) * p.ldp + col0;
     const bool vec = ((p.ldp & 7) == 0) && ((reinterpret_cast<uintptr_t>(p.P) & 15) == 0);
-#pragma unroll 1
-    for (int c = 0; c < 8; ++c) {
-      if (c * 32 >= nvalid) break;
-      uint32_t r[32];
-      ptx::tmem_ld32(taddr + c * 32, r);
-      ptx::tmem_ld_wait();
+    const int nch = (nvalid + 31) / 32;
+    uint32_t box = 0;
+    tmem_chunks(taddr, nch, [&](uint32_t (&r)[32], int c) {
       const int nv = nvalid - c * 32;
       if (track) {
 #pragma unroll
@@ -430,7 +645,16 @@ struct EpiLogitStats {
         sum += e0 + e1;
         pk[j] = ptx::pack_bf16(e0, e1);
       }
-      if (row_ok) {
+      if (p.use_tma) {
+        // a 64-column box holds chunks c (even: 16-byte chunks 0..3) and c+1 (4..7)
+        if ((c & 1) == 0) box = sg.next();
+        const int q0 = (c & 1) * 4;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) ptx::st_shared_v4(Stager::chunk(box, q0 + q), pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+        // an odd chunk count only occurs in the shard's last tile, whose
+        // columns past N are clipped by the TMA unit
+        if ((c & 1) == 1 || c + 1 == nch) sg.store(&p.map, box, col0 + (c & ~1) * 32, row0);
+      } else if (row_ok) {
         if (nv >= 32 && vec) {
           uint4* d4 = reinterpret_cast<uint4*>(dst + c * 32);
 #pragma unroll
@@ -442,10 +666,11 @@ struct EpiLogitStats {
             if (j < nv) d16[j] = uint16_t((j & 1) ? (pk[j >> 1] >> 16) : (pk[j >> 1] & 0xFFFFu));
         }
       }
-    }
+    });
   }
 
-  __device__ static void apply(const Params& p, const GemmGeom& g, uint32_t taddr, int row, int col0, int nb) {
+  __device__ static void apply(const Params& p, const GemmGeom& g, uint32_t taddr, int row, int col0, int nb,
+                               Stager& sg) {
     const bool row_ok = row < g.M;
     const int lane = threadIdx.x & 31;
     const int nvalid = min(GemmCfg<1>::BN, g.N - col0);
@@ -462,24 +687,7 @@ struct EpiLogitStats {
     if (nb == 0 || !f) {
       // two passes: this tile is its own reference (the j = 0 tile defines r_i;
       // an early tile whose row reference is not published yet falls back)
-#pragma unroll 1
-      for (int c = 0; c < 8; ++c) {
-        if (c * 32 >= nvalid) break;
-        uint32_t r[32];
-        ptx::tmem_ld32(taddr + c * 32, r);
-        ptx::tmem_ld_wait();
-        const int nv = nvalid - c * 32;
-#pragma unroll
-        for (int j = 0; j < 32; ++j)
-          if (j < nv) mx = fmaxf(mx, __uint_as_float(r[j]));
-        const int off = lb - c * 32;
-        if (off >= 0 && off < 32 && off < nv) {
-#pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (j == off) yt = __uint_as_float(r[j]);
-          has_t = true;
-        }
-      }
+      scan(taddr, nvalid, lb, mx, yt, has_t);
       ref = mx;
       if (nb == 0) {
         if (row_ok) p.row_ref[row] = mx;
@@ -492,16 +700,18 @@ struct EpiLogitStats {
         own = true;
       }
       float m2;
-      emit(p, taddr, row, row_ok, col0, nvalid, ref, lb, false, m2, yt, has_t, sum);
+      emit(p, taddr, row, row_ok, col0, nvalid, ref, lb, false, m2, yt, has_t, sum, sg);
     } else {
       // single pass against the published row reference
       ref = row_ok ? p.row_ref[row] : 0.f;
-      emit(p, taddr, row, row_ok, col0, nvalid, ref, lb, true, mx, yt, has_t, sum);
+      emit(p, taddr, row, row_ok, col0, nvalid, ref, lb, true, mx, yt, has_t, sum, sg);
       bad = row_ok && (mx - ref > kMaxRefGap);  // e^{Y - r} overflowed: redo against the tile max
       if (__ballot_sync(0xffffffffu, bad)) {
         if (bad) ref = mx;
+        // the first pass's P boxes must land before they are overwritten
+        if (p.use_tma) sg.drain();
         float m2;
-        emit(p, taddr, row, row_ok, col0, nvalid, ref, lb, false, m2, yt, has_t, sum);
+        emit(p, taddr, row, row_ok, col0, nvalid, ref, lb, false, m2, yt, has_t, sum, sg);
       }
     }
     if (row_ok) {

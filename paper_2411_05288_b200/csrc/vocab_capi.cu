@@ -809,6 +809,9 @@ int vp_ctx_set_option(vp_ctx_t c, const char* key, int64_t value) {
       require(value >= 1 && value <= 64, "vp_ctx_set_option: comm_sms must be 1..64");
       require(c->comm == nullptr, "vp_ctx_set_option: comm_sms must be set before vp_ctx_comm_init");
       c->comm_sms = int(value);
+    } else if (k == "tma_store") {
+      require(value == 0 || value == 1, "vp_ctx_set_option: tma_store must be 0 or 1");
+      vp::g_tma_store = int(value);
     } else if (k == "epi_wait") {
       require(value == 0 || value == 1, "vp_ctx_set_option: epi_wait must be 0 or 1");
       vp::g_epi_wait = int(value);

@@ -48,6 +48,7 @@ int main(int argc, char** argv) {
   const int iters = argc > 5 ? atoi(argv[5]) : 10;
   const int64_t T = 8192, h = 4096, V = argc > 6 ? atoll(argv[6]) : 256000;
   int nsm = 0;
+  if (getenv("VP_TMA_STORE")) vp::g_tma_store = atoi(getenv("VP_TMA_STORE"));
   CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0));
   __nv_bfloat16 *X, *W, *P;
   float* out;
@@ -82,7 +83,7 @@ int main(int argc, char** argv) {
       CK(cudaMemsetAsync(bad, 0, T * 4));
       CK(cudaMemsetAsync(cnt, 0, 8));
       vp::launch_gemm<vp::EpiLogitStats>(2, {X, h, false}, {W, h, false}, int(T), int(V), int(h), raster, ep, nsm, 0,
-                                         pa, pb, mc);
+                                         pa, pb, mc, nh);
     } else if (kind == "dx") {
       vp::EpiStoreF32::Params ep{out, h, nullptr, 0, nullptr};
       vp::launch_gemm<vp::EpiStoreF32>(2, {P, V, false}, {W, h, true}, int(T), int(h), int(V), raster, ep, nsm, 0, pa,
@@ -98,7 +99,8 @@ int main(int argc, char** argv) {
     }
   };
   unsigned long long* prof;
-  CK(cudaMallocManaged(&prof, 32));
+  CK(cudaMallocManaged(&prof, 64));
+  CK(cudaMemset(prof, 0, 64));
   vp::g_gemm_prof = prof;
   run();
   CK(cudaDeviceSynchronize());
@@ -123,6 +125,9 @@ int main(int argc, char** argv) {
     const double par = double(nsm / 2);                                        // CTA pairs
     printf("  last launch (CTA 0): %.0f cycles in %.3f ms -> %.0f MHz; MMA-ideal %.0f cycles/pair -> %.1f%% of ideal\n",
            cyc, ns / 1e6, cyc / ns * 1e3, ideal / par, 100.0 * (ideal / par) / cyc);
+    if (nh == 2)
+      printf("  CTA 0 issuer waits: smem stages %.1f%%, accumulators %.1f%%; epilogue warp: waiting %.1f%%, working %.1f%%\n",
+             100.0 * prof[4] / cyc, 100.0 * prof[5] / cyc, 100.0 * prof[6] / cyc, 100.0 * prof[7] / cyc);
   }
   const double flops = kind == "sq8192" ? 2.0 * 8192.0 * 8192.0 * 8192.0 : 2.0 * T * h * double(V);
   printf("mc=%d nh=%d ", mc, nh);

@@ -85,7 +85,7 @@ static void check_store(int cg, bool amn, bool bmn, int M, int N, int K, int nsm
   cudaFree(R);
 }
 
-static void check_stats(int cg, int M, int N, int K, int nsm, int mc = 1) {
+static void check_stats(int cg, int M, int N, int K, int nsm, int mc = 1, int nh = 1) {
   const int64_t ld = (K + 7) / 8 * 8;
   const int64_t ldp = (N + 63) / 64 * 64;
   const int tiles = (N + 255) / 256;
@@ -120,7 +120,7 @@ static void check_stats(int cg, int M, int N, int K, int nsm, int mc = 1) {
   CK(cudaMemset(badr, 0, M * 4));
   CK(cudaMemset(cnt, 0, 8));
   vp::EpiLogitStats::Params ep{P, ldp, tm, ts, M, lab, rb, rb + N, yt, tq, ref, flg, badr, cnt, bl, cnt + 1, fl};
-  vp::launch_gemm<vp::EpiLogitStats>(cg, {A, ld, false}, {B, ld, false}, M, N, K, 0, ep, nsm, 0, -1, -1, mc);
+  vp::launch_gemm<vp::EpiLogitStats>(cg, {A, ld, false}, {B, ld, false}, M, N, K, 0, ep, nsm, 0, -1, -1, mc, nh);
   ref_gemm<<<dim3((N + 127) / 128, M), 128>>>(A, ld, false, B, ld, false, R, M, N, K);
   CK(cudaDeviceSynchronize());
   std::vector<float> r(size_t(M) * N), htm(size_t(tiles) * M), hts(size_t(tiles) * M), hyt(M);
@@ -245,6 +245,7 @@ static void bench_stats(int cg, int M, int N, int K, int nsm) {
 
 int main(int argc, char** argv) {
   int nsm = 0;
+  if (getenv("VP_TMA_STORE")) vp::g_tma_store = atoi(getenv("VP_TMA_STORE"));
   CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0));
   const bool do_bench = argc > 1 && std::string(argv[1]) == "bench";
   if (argc > 1 && std::string(argv[1]) == "one") {  // one 8192^3 GEMM: one <cg>
@@ -273,7 +274,17 @@ int main(int argc, char** argv) {
       check_store(2, amn, bmn, 512, 1024, 512, nsm, 1, 2);
       check_store(2, amn, bmn, 300, 520, 200, nsm, 1, 2);
       check_store(2, amn, bmn, 700, 1300, 640, nsm, 1, 2);
+      // K = 1, 2, 3 k-blocks (stagger depth 0, 1, 1) and a long K (depth = STAGES)
+      check_store(2, amn, bmn, 300, 700, 64, nsm, 1, 2);
+      check_store(2, amn, bmn, 300, 700, 128, nsm, 1, 2);
+      check_store(2, amn, bmn, 300, 700, 192, nsm, 1, 2);
+      check_store(2, amn, bmn, 520, 1100, 2048, nsm, 1, 2);
     }
+  check_stats(2, 300, 1000, 256, nsm, 1, 2);
+  check_stats(2, 512, 777, 512, nsm, 1, 2);
+  check_stats(2, 1000, 5000, 128, nsm, 1, 2);
+  check_stats(2, 700, 3000, 64, nsm, 1, 2);
+  check_stats(2, 600, 1300, 1024, nsm, 1, 2);
   if (do_bench) {
     for (int cg : {1, 2}) bench_store(cg, false, false, 8192, 8192, 8192, 0, nsm);
     bench_stats(2, 8192, 32000, 4096, nsm);
