@@ -3,6 +3,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <cmath>
 #include <cstdio>
 #include <stdexcept>
 #include <string>
@@ -80,6 +81,39 @@ inline void prepare_store(EpiLogitStats::Params& ep, int M, int N) {
     ep.map = make_store_map(ep.P, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, uint64_t(N), uint64_t(M), uint64_t(ep.ldp));
 }
 
+// Split-K state owned by the caller (one per stream: flags are reused across
+// launches with a monotonically increasing base, so two GEMMs sharing one
+// SplitCfg must not run concurrently).  flags: >= 2 * max_tiles ints, zeroed once.
+struct SplitCfg {
+  int* flags = nullptr;
+  int max_tiles = 0;
+  int base = 0;
+  int force = 0;  // > 0: use exactly this many splits (tests); 0: choose by wave quantisation
+};
+
+// Splits for a persistent GEMM of `tiles` tiles on `clusters` clusters and
+// num_kb k-blocks: the smallest S in 1..4 whose wave efficiency
+// tiles*S / (clusters * ceil(tiles*S / clusters)) is within 1% of the best,
+// keeping >= 16 k-blocks per split; S = 1 unless that gains > 2%.
+inline int choose_splits(int tiles, int clusters, int num_kb) {
+  auto eff = [&](int S) {
+    const double w = double(tiles) * S / clusters;
+    return w / std::ceil(w);
+  };
+  int best = 1;
+  double be = eff(1);
+  for (int S = 2; S <= 4; ++S)
+    if (num_kb / S >= 16 && eff(S) > be + 0.02) {
+      best = S;
+      be = eff(S);
+    }
+  return best;
+}
+
+template <class Params>
+inline bool splittable(const Params&) { return false; }
+inline bool splittable(const EpiStoreF32::Params& p) { return p.tile_max == nullptr; }
+
 // One GEMM operand: row-major storage `ptr` with leading dimension `ld`.
 //   K-major : storage [rows x K]  (A: rows = M, B: rows = N)
 //   MN-major: storage [K x rows]
@@ -95,7 +129,7 @@ inline int g_epi_wait = 1;                          // GemmGeom::epi_wait for su
 template <int CG, bool A_MN, bool B_MN, class Epi, int MC = 1, int NH = 1>
 inline void launch_gemm_t(const Operand& A, const Operand& B, int M, int N, int K, int raster,
                           const typename Epi::Params& ep, int num_sms, cudaStream_t st, int pol_a = -1,
-                          int pol_b = -1) {
+                          int pol_b = -1, SplitCfg* split = nullptr) {
   using C = GemmCfg<CG, NH>;
   const CUtensorMap ta = A_MN ? make_tmap_bf16(A.ptr, uint64_t(M), uint64_t(K), uint64_t(A.ld), 64, 64)
                               : make_tmap_bf16(A.ptr, uint64_t(K), uint64_t(M), uint64_t(A.ld), 64, C::BM_CTA);
@@ -148,7 +182,17 @@ inline void launch_gemm_t(const Operand& A, const Operand& B, int M, int N, int 
     max_active = n;
   }
   int cap = num_sms / CL < max_active ? num_sms / CL : max_active;
-  const int clusters = tiles < cap ? tiles : cap;
+  int clusters = tiles < cap ? tiles : cap;
+  if (MC == 1 && split != nullptr && split->flags != nullptr && splittable(ep) && tiles <= split->max_tiles) {
+    const int S = split->force > 0 ? split->force : choose_splits(tiles, cap, g.num_kb);
+    if (S > 1 && g.num_kb >= S) {
+      g.splits = S;
+      g.split_flags = split->flags;
+      g.flag_base = split->base;
+      split->base += S;
+      clusters = tiles * S < cap ? tiles * S : cap;
+    }
+  }
   cfg.gridDim = dim3(unsigned(clusters * CL), 1, 1);
   cfg.blockDim = dim3(C::THREADS, 1, 1);
   cfg.dynamicSmemBytes = C::SMEM_BYTES;
@@ -170,11 +214,11 @@ inline void launch_gemm_t(const Operand& A, const Operand& B, int M, int N, int 
 template <class Epi>
 inline void launch_gemm(int cg, const Operand& A, const Operand& B, int M, int N, int K, int raster,
                         const typename Epi::Params& ep, int num_sms, cudaStream_t st, int pol_a = -1,
-                        int pol_b = -1, int mc = 1, int nh = 1) {
-#define VP_GEMM_CASE(CGV, AM, BM_, MCV, NHV)                                                            \
-  if (cg == CGV && A.mn_major == AM && B.mn_major == BM_ && mc == MCV && nh == NHV) {                   \
-    launch_gemm_t<CGV, AM, BM_, Epi, MCV, NHV>(A, B, M, N, K, raster, ep, num_sms, st, pol_a, pol_b);    \
-    return;                                                                                             \
+                        int pol_b = -1, int mc = 1, int nh = 1, SplitCfg* split = nullptr) {
+#define VP_GEMM_CASE(CGV, AM, BM_, MCV, NHV)                                                                  \
+  if (cg == CGV && A.mn_major == AM && B.mn_major == BM_ && mc == MCV && nh == NHV) {                         \
+    launch_gemm_t<CGV, AM, BM_, Epi, MCV, NHV>(A, B, M, N, K, raster, ep, num_sms, st, pol_a, pol_b, split);  \
+    return;                                                                                                   \
   }
   VP_GEMM_CASE(2, false, false, 1, 1)
   VP_GEMM_CASE(2, false, true, 1, 1)

@@ -44,6 +44,14 @@ struct GemmGeom {
   // how the epilogue warps wait for an accumulator: 0 try_wait loop,
   // 1 nanosleep backoff (fewer issued instructions while a main loop runs)
   int epi_wait = 1;
+  // Split-K (few-wave GEMMs, e.g. dX with K = V_k): every tile is computed as
+  // `splits` units over consecutive K ranges; unit u = s * tiles + t.  Split 0
+  // stores, split s > 0 adds its partial after split s-1 of the same tile
+  // (and CTA) has landed — a fixed order, so results are deterministic.
+  // split_flags[2 * t + rank] holds flag_base + (splits completed).
+  int splits = 1;
+  int* split_flags = nullptr;
+  int flag_base = 0;
 };
 
 __device__ __forceinline__ uint64_t make_policy(int p, bool dflt_first) {
@@ -99,10 +107,16 @@ __device__ __forceinline__ void tile_coords(const GemmGeom& g, int t, int& mb, i
 struct Stager {
   uint32_t base;
   uint32_t k = 0;
+  bool probe = false;              // count cycles spent waiting for a free box (lane 0)
+  unsigned long long wait_cyc = 0;
   __device__ explicit Stager(uint32_t b) : base(b) {}
   // next free box (the store issued two boxes ago has finished reading it)
   __device__ __forceinline__ uint32_t next() {
-    if ((threadIdx.x & 31) == 0) ptx::bulk_wait_read<1>();
+    if ((threadIdx.x & 31) == 0) {
+      const unsigned long long c0 = probe ? clock64() : 0;
+      ptx::bulk_wait_read<1>();
+      if (probe) wait_cyc += clock64() - c0;
+    }
     __syncwarp();
     const uint32_t b = base + (k & 1u) * 4096u;
     ++k;
@@ -153,6 +167,29 @@ __device__ __forceinline__ void tmem_chunks(uint32_t taddr, int nch, F&& f) {
   }
 }
 
+// Split-K ordering (epilogue warps of one CTA).  split_wait: every lane
+// waits until the previous split of this tile/CTA has landed in global
+// memory; split_done: after this split's stores completed, publish it.
+__device__ __forceinline__ void split_wait(const int* flag, int want) {
+  if ((threadIdx.x & 31) == 0) {
+    int v;
+    for (;;) {
+      asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+      if (v - want >= 0) break;
+      __nanosleep(256);
+    }
+    asm volatile("fence.proxy.async.global;" ::: "memory");  // later TMA reduces see those writes
+  }
+  __syncwarp();
+}
+__device__ __forceinline__ void split_done(int* flag, int value, Stager& sg) {
+  sg.drain();  // this warp's TMA stores are complete
+  if ((threadIdx.x & 31) == 0) asm volatile("fence.proxy.async.global;" ::: "memory");
+  __threadfence();
+  asm volatile("bar.sync 1, 128;" ::: "memory");  // the 4 epilogue warps of this CTA
+  if (threadIdx.x == 128) asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(flag), "r"(value) : "memory");
+}
+
 // MC = CTA pairs per cluster along M (CG == 2 only).  MC == 2: a 4-CTA
 // cluster computes a 512 x 256 "cluster tile" as two pair tiles (m, n) and
 // (m+1, n) that need the same B rows; each CTA loads HALF of its B rows and
@@ -192,6 +229,15 @@ __global__ void __launch_bounds__(256, 1)
   GemmGeom gc = g;
   gc.tiles_m = tiles_mc;
   const int num_tiles = tiles_mc * g.tiles_n;
+  const int num_units = num_tiles * g.splits;
+  // unit -> (tile, split, k-block range)
+  auto unit_tile = [&](int u) { return u % num_tiles; };
+  auto unit_split = [&](int u) { return u / num_tiles; };
+  auto unit_kb0 = [&](int u) { return int((int64_t(u / num_tiles) * g.num_kb) / g.splits); };
+  auto unit_nkb = [&](int u) {
+    const int sp = u / num_tiles;
+    return int((int64_t(sp + 1) * g.num_kb) / g.splits - (int64_t(sp) * g.num_kb) / g.splits);
+  };
 
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&tmA);
@@ -225,13 +271,14 @@ __global__ void __launch_bounds__(256, 1)
     const uint64_t polA = make_policy(g.pol_a, Epi::kAStreams);
     const uint64_t polB = make_policy(g.pol_b, !Epi::kAStreams);
     uint32_t it = 0;
-    for (int t = cluster; t < num_tiles; t += nclusters) {
+    for (int u = cluster; u < num_units; u += nclusters) {
       int mc, nb;
-      tile_coords(gc, t, mc, nb);
+      tile_coords(gc, unit_tile(u), mc, nb);
       const int mb = mc * MC + int(pair);
       const int m0 = mb * C::BM + int(rank) * C::BM_CTA;
       const int n0 = nb * C::BN_TILE + int(rank) * C::B_HALF_ROWS;  // + h * C::BN for N half h
-      for (int kb = 0; kb < g.num_kb; ++kb, ++it) {
+      const int kbase = unit_kb0(u), nkb = unit_nkb(u);
+      for (int kb = kbase; kb < kbase + nkb; ++kb, ++it) {
         const uint32_t s = it % C::STAGES, ph = (it / C::STAGES) & 1u;
         ptx::mbar_wait(bar_empty + 8 * s, ph ^ 1u);
         // The leader's barrier expects the bytes landing in BOTH CTAs of its
@@ -286,7 +333,6 @@ __global__ void __launch_bounds__(256, 1)
     // D <= STAGES (the D k-blocks stay resident in smem until H1 has read
     // them) and D <= K/2 (start and end groups disjoint).
     constexpr uint32_t idesc = ptx::idesc_bf16_f32(C::BM, C::BN, A_MN, B_MN);
-    const int D = min(C::STAGES, g.num_kb / 2);
     uint32_t it0 = 0, tc = 0;
     auto issue = [&](int kb, int hh) {
       const uint32_t s = (it0 + kb) % C::STAGES;
@@ -317,8 +363,9 @@ __global__ void __launch_bounds__(256, 1)
       if (probe) w_acc += clock64() - c0;
       ptx::tc_fence_after();
     };
-    const int K = g.num_kb;
-    for (int t = cluster; t < num_tiles; t += nclusters, ++tc, it0 += uint32_t(K)) {
+    for (int u = cluster; u < num_units; u += nclusters, ++tc) {
+      const int K = unit_nkb(u);
+      const int D = min(C::STAGES, K / 2);
       wait_acc(0);
       for (int kb = 0; kb < D; ++kb) {
         wait_full(kb);
@@ -345,6 +392,7 @@ __global__ void __launch_bounds__(256, 1)
         release(kb);
       }
       ptx::mma_commit<CG>(bar_tfull + 8, pair_mask);
+      it0 += uint32_t(K);
     }
     if (probe) {
       g.prof[4] = w_full;
@@ -355,13 +403,14 @@ __global__ void __launch_bounds__(256, 1)
     constexpr uint32_t idesc = ptx::idesc_bf16_f32(C::BM, C::BN, A_MN, B_MN);
     constexpr uint16_t all_mask = uint16_t((1u << CL) - 1u);
     uint32_t it = 0, tc = 0;
-    for (int t = cluster; t < num_tiles; t += nclusters, ++tc) {
+    for (int u = cluster; u < num_units; u += nclusters, ++tc) {
+      const int nkb = unit_nkb(u);
       const uint32_t acc = tc % NACC, aph = (tc / NACC) & 1u;
       if constexpr (CG == 2) ptx::mbar_wait_cluster(bar_tempty + 8 * acc, aph ^ 1u);
       else ptx::mbar_wait(bar_tempty + 8 * acc, aph ^ 1u);
       ptx::tc_fence_after();
       const uint32_t d = tmem_base + acc * C::BN;
-      for (int kb = 0; kb < g.num_kb; ++kb, ++it) {
+      for (int kb = 0; kb < nkb; ++kb, ++it) {
         const uint32_t s = it % C::STAGES, ph = (it / C::STAGES) & 1u;
         ptx::mbar_wait(bar_full + 8 * s, ph);
         ptx::tc_fence_after();
@@ -390,16 +439,20 @@ __global__ void __launch_bounds__(256, 1)
     // ===== epilogue =====
     const int ew = warp - 4;
     Stager sg(stg + uint32_t(ew) * 8192u);
+    sg.probe = g.prof != nullptr && blockIdx.x == 0 && ew == 0;
     uint32_t tc = 0;
     unsigned long long epi_wait_cyc = 0, epi_work_cyc = 0;  // probe (NH == 2, CTA 0, warp 4)
-    for (int t = cluster; t < num_tiles; t += nclusters, ++tc) {
+    for (int u = cluster; u < num_units; u += nclusters, ++tc) {
       int mc, nb;
+      const int t = unit_tile(u), sp = unit_split(u);
       tile_coords(gc, t, mc, nb);
       const int mb = mc * MC + int(pair);
+      int* flag = g.splits > 1 ? g.split_flags + 2 * t + int(rank) : nullptr;
       if constexpr (NH == 2) {
         // halves complete (and are released) separately: see the staggered issuer
         const int row = mb * C::BM + int(rank) * C::BM_CTA + ew * 32 + lane;
         const bool probe = g.prof != nullptr && blockIdx.x == 0 && ew == 0;
+        const typename Epi::Pre pre = Epi::prepare(ep, g, row, nb * C::BN_TILE);
 #pragma unroll 1
         for (int hh = 0; hh < 2; ++hh) {
           const unsigned long long c0 = probe ? clock64() : 0;
@@ -410,7 +463,9 @@ __global__ void __launch_bounds__(256, 1)
           const uint32_t taddr = tmem_base + hh * C::BN + (uint32_t(ew * 32) << 16);
           // a 512-wide tile's second half may lie wholly past N (ragged last
           // tile): it has no columns, no stats slot and nothing to store
-          if (nb * C::BN_TILE + hh * C::BN < g.N) Epi::apply(ep, g, taddr, row, nb * C::BN_TILE + hh * C::BN, nb * 2 + hh, sg);
+          if (hh == 0 && sp > 0) split_wait(flag, g.flag_base + sp);
+          if (nb * C::BN_TILE + hh * C::BN < g.N)
+            Epi::apply(ep, g, taddr, row, nb * C::BN_TILE + hh * C::BN, nb * 2 + hh, sg, pre, sp > 0);
           if (probe && lane == 0) {
             epi_wait_cyc += c1 - c0;
             epi_work_cyc += clock64() - c1;
@@ -419,9 +474,11 @@ __global__ void __launch_bounds__(256, 1)
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive_remote(bar_tempty + 8 * hh, leader);
         }
+        if (flag) split_done(flag, g.flag_base + sp + 1, sg);
         continue;
       }
       const uint32_t acc = tc % NACC, aph = (tc / NACC) & 1u;
+      const typename Epi::Pre pre = Epi::prepare(ep, g, mb * C::BM + int(rank) * C::BM_CTA + ew * 32 + lane, nb * C::BN_TILE);
       if (g.epi_wait) ptx::mbar_wait_backoff(bar_tfull + 8 * acc, aph);
       else ptx::mbar_wait(bar_tfull + 8 * acc, aph);
       ptx::tc_fence_after();
@@ -431,18 +488,22 @@ __global__ void __launch_bounds__(256, 1)
       for (int hh = 0; hh < NH; ++hh)
         // a 512-wide tile's second half may lie wholly past N (ragged last
         // tile): it has no columns, no stats slot and nothing to store
-        if (nb * C::BN_TILE + hh * C::BN < g.N)
-          Epi::apply(ep, g, taddr + hh * C::BN, row, nb * C::BN_TILE + hh * C::BN, nb * NH + hh, sg);
+        if (nb * C::BN_TILE + hh * C::BN < g.N) {
+          if (hh == 0 && sp > 0) split_wait(flag, g.flag_base + sp);
+          Epi::apply(ep, g, taddr + hh * C::BN, row, nb * C::BN_TILE + hh * C::BN, nb * NH + hh, sg, pre, sp > 0);
+        }
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) {
         if constexpr (CG == 1) ptx::mbar_arrive(bar_tempty + 8 * acc);
         else ptx::mbar_arrive_remote(bar_tempty + 8 * acc, leader);
       }
+      if (flag) split_done(flag, g.flag_base + sp + 1, sg);
     }
     sg.drain();
     if (g.prof != nullptr && blockIdx.x == 0 && ew == 0 && lane == 0) {
       g.prof[6] = epi_wait_cyc;
+      g.prof[8] = sg.wait_cyc;
       g.prof[7] = epi_work_cyc;
     }
   }
@@ -490,12 +551,20 @@ struct EpiStoreF32 {
     int use_tma = 0;         // stores through `map` (fp32 [M x N], 32 x 32 boxes, SWIZZLE_128B)
     CUtensorMap map;
   };
+  // per-row inputs loaded before the accumulator is waited for (hides their latency)
+  struct Pre {
+    float rs;
+  };
+  __device__ static Pre prepare(const Params& p, const GemmGeom& g, int row, int /*tile_col0*/) {
+    return Pre{(p.row_scale && row < g.M) ? p.row_scale[row] : 1.f};
+  }
   __device__ static void apply(const Params& p, const GemmGeom& g, uint32_t taddr, int row, int col0, int nb,
-                               Stager& sg) {
+                               Stager& sg, const Pre& pre, bool split_add) {
     const bool row_ok = row < g.M;
     const int nvalid = min(GemmCfg<1>::BN, g.N - col0);
     const int nch = (nvalid + 31) / 32;
-    const float rs = (p.row_scale && row_ok) ? p.row_scale[row] : 1.f;
+    const float rs = pre.rs;
+    const bool add = p.accumulate != 0 || split_add;
     float mx = -INFINITY;
     const int row0 = row - int(threadIdx.x & 31);
     if (p.use_tma) {
@@ -513,7 +582,7 @@ struct EpiStoreF32 {
         const uint32_t box = sg.next();
 #pragma unroll
         for (int q = 0; q < 8; ++q) ptx::st_shared_v4(Stager::chunk(box, q), r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
-        sg.store(&p.map, box, col0 + c * 32, row0, p.accumulate != 0);
+        sg.store(&p.map, box, col0 + c * 32, row0, add);
       });
     } else {
       float* dst = p.out + int64_t(row) * p.ldo + col0;
@@ -536,7 +605,7 @@ struct EpiStoreF32 {
           for (int j = 0; j < 8; ++j) {
             float4 v = make_float4(__uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]),
                                    __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]));
-            if (p.accumulate) {
+            if (add) {
               const float4 o = d4[j];
               v.x += o.x;
               v.y += o.y;
@@ -548,7 +617,7 @@ struct EpiStoreF32 {
         } else {
 #pragma unroll
           for (int j = 0; j < 32; ++j)
-            if (j < nv) dst[c * 32 + j] = __uint_as_float(r[j]) + (p.accumulate ? dst[c * 32 + j] : 0.f);
+            if (j < nv) dst[c * 32 + j] = __uint_as_float(r[j]) + (add ? dst[c * 32 + j] : 0.f);
         }
       });
     }
@@ -595,11 +664,17 @@ struct EpiLogitStats {
   };
   // max of the valid columns and the label logit (first pass of a two-pass tile)
   __device__ static void scan(uint32_t taddr, int nvalid, int lb, float& mx, float& yt, bool& has_t) {
+    float mp[4] = {mx, mx, mx, mx};
     tmem_chunks(taddr, (nvalid + 31) / 32, [&](uint32_t (&r)[32], int c) {
       const int nv = nvalid - c * 32;
+      if (nv >= 32) {
 #pragma unroll
-      for (int j = 0; j < 32; ++j)
-        if (j < nv) mx = fmaxf(mx, __uint_as_float(r[j]));
+        for (int j = 0; j < 32; ++j) mp[j & 3] = fmaxf(mp[j & 3], __uint_as_float(r[j]));
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (j < nv) mp[j & 3] = fmaxf(mp[j & 3], __uint_as_float(r[j]));
+      }
       const int off = lb - c * 32;
       if (off >= 0 && off < 32 && off < nv) {
 #pragma unroll
@@ -608,6 +683,7 @@ struct EpiLogitStats {
         has_t = true;
       }
     });
+    mx = fmaxf(fmaxf(mp[0], mp[1]), fmaxf(mp[2], mp[3]));
   }
   // One pass over the 256 accumulator columns of this row: P = bf16(e^{Y - ref}),
   // s = sum e^{Y - ref}; with track = true it also takes the tile max and the
@@ -623,12 +699,41 @@ struct EpiLogitStats {
     const bool vec = ((p.ldp & 7) == 0) && ((reinterpret_cast<uintptr_t>(p.P) & 15) == 0);
     const int nch = (nvalid + 31) / 32;
     uint32_t box = 0;
+    float sp[4] = {0.f, 0.f, 0.f, 0.f};  // independent partial sums / maxima (no serial chains)
+    float mp[4] = {mx, mx, mx, mx};
     tmem_chunks(taddr, nch, [&](uint32_t (&r)[32], int c) {
       const int nv = nvalid - c * 32;
-      if (track) {
+      uint32_t pk[16];
+      if (nv >= 32) {
+        // full chunk: no column masks
+        if (track) {
 #pragma unroll
-        for (int j = 0; j < 32; ++j)
-          if (j < nv) mx = fmaxf(mx, __uint_as_float(r[j]));
+          for (int j = 0; j < 32; ++j) mp[j & 3] = fmaxf(mp[j & 3], __uint_as_float(r[j]));
+        }
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const float e0 = ptx::ex2(fmaf(__uint_as_float(r[2 * j]), kLog2e, -refs));
+          const float e1 = ptx::ex2(fmaf(__uint_as_float(r[2 * j + 1]), kLog2e, -refs));
+          sp[(2 * j) & 3] += e0;
+          sp[(2 * j + 1) & 3] += e1;
+          pk[j] = ptx::pack_bf16(e0, e1);
+        }
+      } else {
+        if (track) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (j < nv) mp[j & 3] = fmaxf(mp[j & 3], __uint_as_float(r[j]));
+        }
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const float e0 = (2 * j < nv) ? ptx::ex2(fmaf(__uint_as_float(r[2 * j]), kLog2e, -refs)) : 0.f;
+          const float e1 = (2 * j + 1 < nv) ? ptx::ex2(fmaf(__uint_as_float(r[2 * j + 1]), kLog2e, -refs)) : 0.f;
+          sp[(2 * j) & 3] += e0;
+          sp[(2 * j + 1) & 3] += e1;
+          pk[j] = ptx::pack_bf16(e0, e1);
+        }
+      }
+      if (track) {
         const int off = lb - c * 32;
         if (off >= 0 && off < 32 && off < nv) {
 #pragma unroll
@@ -636,14 +741,6 @@ struct EpiLogitStats {
             if (j == off) yt = __uint_as_float(r[j]);
           has_t = true;
         }
-      }
-      uint32_t pk[16];
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const float e0 = (2 * j < nv) ? ptx::ex2(fmaf(__uint_as_float(r[2 * j]), kLog2e, -refs)) : 0.f;
-        const float e1 = (2 * j + 1 < nv) ? ptx::ex2(fmaf(__uint_as_float(r[2 * j + 1]), kLog2e, -refs)) : 0.f;
-        sum += e0 + e1;
-        pk[j] = ptx::pack_bf16(e0, e1);
       }
       if (p.use_tma) {
         // a 64-column box holds chunks c (even: 16-byte chunks 0..3) and c+1 (4..7)
@@ -667,21 +764,51 @@ struct EpiLogitStats {
         }
       }
     });
+    sum = (sp[0] + sp[1]) + (sp[2] + sp[3]);
+    if (track) mx = fmaxf(fmaxf(mp[0], mp[1]), fmaxf(mp[2], mp[3]));
   }
 
+  // Per-row inputs loaded before the accumulator is waited for: the label,
+  // and (tiles past the first) the row-reference flag and r_i.  A flag still
+  // clear here is re-checked in apply().
+  struct Pre {
+    int64_t label;
+    int flag;
+    float ref;
+  };
+  __device__ static int load_flag(const Params& p, int row) {
+    int f;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(f) : "l"(p.ref_flag + (row >> 7)) : "memory");
+    return f;
+  }
+  __device__ static Pre prepare(const Params& p, const GemmGeom& g, int row, int tile_col0) {
+    Pre r{-1, 0, 0.f};
+    if (row < g.M) {
+      if (p.labels) r.label = p.labels[row];
+      if (tile_col0 != 0) {
+        r.flag = load_flag(p, row);
+        if (r.flag) r.ref = p.row_ref[row];
+      }
+    }
+    return r;
+  }
   __device__ static void apply(const Params& p, const GemmGeom& g, uint32_t taddr, int row, int col0, int nb,
-                               Stager& sg) {
+                               Stager& sg, const Pre& pre, bool /*split_add: never split*/) {
     const bool row_ok = row < g.M;
     const int lane = threadIdx.x & 31;
     const int nvalid = min(GemmCfg<1>::BN, g.N - col0);
     int lb = -1;
-    if (row_ok && p.labels) {
-      const int64_t gl = p.labels[row];
-      if (gl >= p.row_begin && gl < p.row_end) lb = int(gl - p.row_begin) - col0;  // offset inside tile
-    }
+    if (row_ok && pre.label >= p.row_begin && pre.label < p.row_end)
+      lb = int(pre.label - p.row_begin) - col0;  // offset inside tile
     const int blk = row >> 7;
-    int f = 0;
-    if (nb != 0) asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(f) : "l"(p.ref_flag + blk) : "memory");
+    int f = pre.flag;
+    float pref = pre.ref;
+    if (nb != 0 && !f && row_ok) {
+      f = load_flag(p, row);
+      if (f) pref = p.row_ref[row];
+    }
+    f = __all_sync(0xffffffffu, f || !row_ok);  // warp-uniform path (rows past M follow their warp)
+    (void)blk;
     float mx = -INFINITY, yt = 0.f, sum = 0.f, ref;
     bool has_t = false, own = false, bad = false;
     if (nb == 0 || !f) {
@@ -694,7 +821,7 @@ struct EpiLogitStats {
         asm volatile("bar.sync 1, 128;" ::: "memory");  // the 4 epilogue warps of this CTA
         if (threadIdx.x == 128) {
           __threadfence();
-          atomicExch(p.ref_flag + blk, 1);
+          atomicExch(p.ref_flag + (row >> 7), 1);
         }
       } else {
         own = true;
@@ -703,7 +830,7 @@ struct EpiLogitStats {
       emit(p, taddr, row, row_ok, col0, nvalid, ref, lb, false, m2, yt, has_t, sum, sg);
     } else {
       // single pass against the published row reference
-      ref = row_ok ? p.row_ref[row] : 0.f;
+      ref = row_ok ? pref : 0.f;
       emit(p, taddr, row, row_ok, col0, nvalid, ref, lb, true, mx, yt, has_t, sum, sg);
       bad = row_ok && (mx - ref > kMaxRefGap);  // e^{Y - r} overflowed: redo against the tile max
       if (__ballot_sync(0xffffffffu, bad)) {

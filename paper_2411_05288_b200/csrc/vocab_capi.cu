@@ -104,6 +104,10 @@ struct vp_ctx_s {
   int pol[3] = {0, 0, 0};
   int mc = 1;  // CTA pairs per cluster sharing B by TMA multicast (1 or 2)
   int nh[3] = {2, 2, 2};  // N halves per tile (2 = 256 x 512 pair tiles) for [logits, dX, dW]
+  // split-K of the dX GEMM (K = V_k, few waves): ordered, deterministic;
+  // splits_dx option: 0 = by wave quantisation, 1 = off, 2..4 = forced
+  vp::SplitCfg split;
+  int splits_dx = 0;
   // tile shapes actually launched: 512-wide tiles and multicast need CTA pairs
   int eff_nh(int i) const { return cg == 2 ? nh[i] : 1; }
   int eff_mc(int i) const { return cg == 2 && eff_nh(i) == 1 ? mc : 1; }
@@ -254,10 +258,11 @@ void gemm_logits_f32(vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* s, vp_s
 void gemm_dx(vp_ctx_s* c, vp_state_s* st, const vp_shard_t* s, float* out, int64_t ldo,
              const float* row_scale = nullptr) {
   vp::EpiStoreF32::Params ep{out, ldo, nullptr, 0, row_scale};
+  c->split.force = c->splits_dx;
   timed_gemm(c, 2, [&] {
     vp::launch_gemm<vp::EpiStoreF32>(c->cg, {st->P, st->ldp, false}, {s->W, s->ldw, true}, int(st->n_tok),
                                      int(st->h), int(st->rows), c->raster[1], ep, c->gemm_sms, c->stream, c->pol[1],
-                                     c->pol[1], c->eff_mc(1), c->eff_nh(1));
+                                     c->pol[1], c->eff_mc(1), c->eff_nh(1), c->splits_dx == 1 ? nullptr : &c->split);
   });
   ++c->launches;
 }
@@ -714,6 +719,9 @@ int vp_ctx_create(int device, vp_ctx_t* out) {
       c->stream = c->own_stream;
       VP_CUDA(cudaMalloc(&c->d_err, sizeof(int)));
       VP_CUDA(cudaMemset(c->d_err, 0, sizeof(int)));
+      c->split.max_tiles = 1 << 14;
+      VP_CUDA(cudaMalloc(&c->split.flags, size_t(2 * c->split.max_tiles) * sizeof(int)));
+      VP_CUDA(cudaMemset(c->split.flags, 0, size_t(2 * c->split.max_tiles) * sizeof(int)));
     } catch (...) {
       delete c;
       throw;
@@ -735,6 +743,7 @@ int vp_ctx_destroy(vp_ctx_t c) {
     for (DevBuf* b : {&c->inv, &c->scale, &c->xs, &c->keys, &c->gathered, &c->packed, &c->tmp_m, &c->tmp_s})
       b->release();
     if (c->d_err) cudaFree(c->d_err);
+    if (c->split.flags) cudaFree(c->split.flags);
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
     delete c;
   });
@@ -809,6 +818,9 @@ int vp_ctx_set_option(vp_ctx_t c, const char* key, int64_t value) {
       require(value >= 1 && value <= 64, "vp_ctx_set_option: comm_sms must be 1..64");
       require(c->comm == nullptr, "vp_ctx_set_option: comm_sms must be set before vp_ctx_comm_init");
       c->comm_sms = int(value);
+    } else if (k == "splits_dx") {
+      require(value >= 0 && value <= 4, "vp_ctx_set_option: splits_dx must be in 0..4");
+      c->splits_dx = int(value);
     } else if (k == "tma_store") {
       require(value == 0 || value == 1, "vp_ctx_set_option: tma_store must be 0 or 1");
       vp::g_tma_store = int(value);

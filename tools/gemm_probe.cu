@@ -75,6 +75,13 @@ int main(int argc, char** argv) {
   CK(cudaMalloc(&fl, int64_t(T / 32 + 1) * ntiles * 8));
   const int64_t out_elems = kind == "dw" ? V * h : kind == "sq8192" ? int64_t(8192) * 8192 : T * h;
   CK(cudaMalloc(&out, out_elems * 4));
+  // VP_SPLIT: split-K of the dx GEMM (0 = off, -1 = auto, 2..4 forced)
+  const int split_dx = getenv("VP_SPLIT") ? atoi(getenv("VP_SPLIT")) : -1;
+  vp::SplitCfg scfg;
+  CK(cudaMalloc(&scfg.flags, 2 * 16384 * sizeof(int)));
+  CK(cudaMemset(scfg.flags, 0, 2 * 16384 * sizeof(int)));
+  scfg.max_tiles = 16384;
+  scfg.force = split_dx > 0 ? split_dx : 0;
   auto run = [&] {
     if (kind == "k1") {
       vp::EpiLogitStats::Params ep{P,   V,   tm,  ts,  T,   nullptr, 0,   V,   yt,  tq,
@@ -87,7 +94,7 @@ int main(int argc, char** argv) {
     } else if (kind == "dx") {
       vp::EpiStoreF32::Params ep{out, h, nullptr, 0, nullptr};
       vp::launch_gemm<vp::EpiStoreF32>(2, {P, V, false}, {W, h, true}, int(T), int(h), int(V), raster, ep, nsm, 0, pa,
-                                       pb, mc, nh);
+                                       pb, mc, nh, split_dx ? &scfg : nullptr);
     } else if (kind == "dw") {
       vp::EpiStoreF32::Params ep{out, h, nullptr, 0, nullptr};
       vp::launch_gemm<vp::EpiStoreF32>(2, {P, V, true}, {X, h, true}, int(V), int(h), int(T), raster, ep, nsm, 0, pa,
@@ -99,8 +106,8 @@ int main(int argc, char** argv) {
     }
   };
   unsigned long long* prof;
-  CK(cudaMallocManaged(&prof, 64));
-  CK(cudaMemset(prof, 0, 64));
+  CK(cudaMallocManaged(&prof, 128));
+  CK(cudaMemset(prof, 0, 128));
   vp::g_gemm_prof = prof;
   run();
   CK(cudaDeviceSynchronize());
@@ -128,6 +135,7 @@ int main(int argc, char** argv) {
     if (nh == 2)
       printf("  CTA 0 issuer waits: smem stages %.1f%%, accumulators %.1f%%; epilogue warp: waiting %.1f%%, working %.1f%%\n",
              100.0 * prof[4] / cyc, 100.0 * prof[5] / cyc, 100.0 * prof[6] / cyc, 100.0 * prof[7] / cyc);
+    printf("  CTA 0 epilogue warp: waiting for a free staging box %.2f%%\n", 100.0 * prof[8] / cyc);
   }
   const double flops = kind == "sq8192" ? 2.0 * 8192.0 * 8192.0 * 8192.0 : 2.0 * T * h * double(V);
   printf("mc=%d nh=%d ", mc, nh);

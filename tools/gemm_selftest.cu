@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "../paper_2411_05288_b200/csrc/gemm_host.cuh"
@@ -47,7 +48,11 @@ __global__ void ref_gemm(const __nv_bfloat16* A, int64_t lda, bool amn, const __
 
 static int failures = 0;
 
-static void check_store(int cg, bool amn, bool bmn, int M, int N, int K, int nsm, int mc = 1, int nh = 1) {
+static int* g_flags = nullptr;
+static vp::SplitCfg g_split;
+
+static void check_store(int cg, bool amn, bool bmn, int M, int N, int K, int nsm, int mc = 1, int nh = 1,
+                        int split = 0) {
   const int64_t lda = amn ? ((M + 7) / 8 * 8) : ((K + 7) / 8 * 8);
   const int64_t ldb = bmn ? ((N + 7) / 8 * 8) : ((K + 7) / 8 * 8);
   const int64_t asz = amn ? int64_t(K) * lda : int64_t(M) * lda;
@@ -62,7 +67,24 @@ static void check_store(int cg, bool amn, bool bmn, int M, int N, int K, int nsm
   init_bf16<<<256, 256>>>(B, bsz, 91u, 1.f);
   CK(cudaMemset(D, 0xFF, int64_t(M) * N * 4));
   vp::EpiStoreF32::Params ep{D, N, nullptr, 0};
-  vp::launch_gemm<vp::EpiStoreF32>(cg, {A, lda, amn}, {B, ldb, bmn}, M, N, K, 0, ep, nsm, 0, -1, -1, mc, nh);
+  if (split && !g_flags) {
+    CK(cudaMalloc(&g_flags, 2 * 4096 * sizeof(int)));
+    CK(cudaMemset(g_flags, 0, 2 * 4096 * sizeof(int)));
+    g_split.flags = g_flags;
+    g_split.max_tiles = 4096;
+  }
+  g_split.force = split;
+  vp::launch_gemm<vp::EpiStoreF32>(cg, {A, lda, amn}, {B, ldb, bmn}, M, N, K, 0, ep, nsm, 0, -1, -1, mc, nh,
+                                   split ? &g_split : nullptr);
+  size_t nondet = 0;
+  if (split) {  // ordered split accumulation: a second run gives identical bits
+    std::vector<float> d1(size_t(M) * N), d2(size_t(M) * N);
+    CK(cudaMemcpy(d1.data(), D, d1.size() * 4, cudaMemcpyDeviceToHost));
+    vp::launch_gemm<vp::EpiStoreF32>(cg, {A, lda, amn}, {B, ldb, bmn}, M, N, K, 0, ep, nsm, 0, -1, -1, mc, nh,
+                                     &g_split);
+    CK(cudaMemcpy(d2.data(), D, d2.size() * 4, cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < d1.size(); ++i) nondet += memcmp(&d1[i], &d2[i], 4) != 0;
+  }
   ref_gemm<<<dim3((N + 127) / 128, M), 128>>>(A, lda, amn, B, ldb, bmn, R, M, N, K);
   CK(cudaDeviceSynchronize());
   std::vector<float> d(size_t(M) * N), r(size_t(M) * N);
@@ -76,8 +98,10 @@ static void check_store(int cg, bool amn, bool bmn, int M, int N, int K, int nsm
     maxerr = std::max(maxerr, std::isnan(e) ? 1e30 : e);
     maxref = std::max(maxref, double(std::fabs(r[i])));
   }
-  printf("store cg=%d mc=%d nh=%d A_%s B_%s M=%d N=%d K=%d : max_abs_err=%.3e max_ref=%.3e bad=%zu %s\n", cg, mc, nh,
-         amn ? "MN" : "K", bmn ? "MN" : "K", M, N, K, maxerr, maxref, bad, bad ? "FAIL" : "ok");
+  bad += nondet;
+  printf("store cg=%d mc=%d nh=%d split=%d A_%s B_%s M=%d N=%d K=%d : max_abs_err=%.3e max_ref=%.3e bad=%zu nondet=%zu %s\n",
+         cg, mc, nh, split, amn ? "MN" : "K", bmn ? "MN" : "K", M, N, K, maxerr, maxref, bad, nondet,
+         bad ? "FAIL" : "ok");
   if (bad) ++failures;
   cudaFree(A);
   cudaFree(B);
@@ -280,6 +304,14 @@ int main(int argc, char** argv) {
       check_store(2, amn, bmn, 300, 700, 192, nsm, 1, 2);
       check_store(2, amn, bmn, 520, 1100, 2048, nsm, 1, 2);
     }
+  // split-K (ordered partial accumulation), both tile widths, both cta_groups
+  for (int sp : {2, 3, 4}) {
+    check_store(2, false, true, 520, 1100, 2048, nsm, 1, 2, sp);
+    check_store(2, false, true, 300, 700, 640, nsm, 1, 1, sp);
+    check_store(1, false, true, 300, 700, 640, nsm, 1, 1, sp);
+    check_store(2, true, true, 700, 1300, 1024, nsm, 1, 2, sp);
+  }
+  check_store(2, false, true, 2048, 4096, 8192, nsm, 1, 2, 2);
   check_stats(2, 300, 1000, 256, nsm, 1, 2);
   check_stats(2, 512, 777, 512, nsm, 1, 2);
   check_stats(2, 1000, 5000, 128, nsm, 1, 2);
