@@ -14,17 +14,31 @@
 //   * CG = 2 runs one 256 x 256 tile per CTA pair (cta_group::2): each CTA
 //     loads 128 rows of A and 128 rows of B, the leader CTA's single thread
 //     issues tcgen05.mma for the pair, and each CTA's TMEM holds its 128
-//     accumulator rows.  CG = 1 runs 128 x 256 tiles per CTA.
-//   * TMEM holds two 256-column accumulators so the epilogue of tile i
-//     overlaps the main loop of tile i+1.
-//   * warp roles (256 threads): w0 TMA producer, w1 MMA issuer (leader CTA),
-//     w2 TMEM allocator, w3 idle, w4..w7 epilogue (TMEM lanes 0..127, one
-//     accumulator row per thread).
+//     accumulator rows.  CG = 1 runs 128 x 256 tiles per CTA.  NH = 2 makes
+//     the pair tile 256 x 512 (two N = 256 MMAs per K step, all 512 TMEM
+//     columns) with the two N halves staggered at tile boundaries.
+//   * NH = 1: TMEM holds two 256-column accumulators so the epilogue of tile
+//     i overlaps the main loop of tile i+1.
+//   * warp roles (384 threads): w0 TMA producer, w1 MMA issuer (leader CTA),
+//     w2 TMEM allocator, w3 idle, w4..w11 epilogue (lane quadrant w % 4,
+//     column group (w - 4) / 4: one accumulator row per thread, 128 columns
+//     per call), storing through smem staging + TMA.
+//   * optional split-K units with ordered (deterministic) accumulation.
 #pragma once
 #include <cuda.h>
 #include <cuda_runtime.h>
 
 #include "sm100_ptx.cuh"
+
+#ifndef VP_GEMM_PROBE
+#define VP_GEMM_PROBE 0  // 1: CTA 0 records wait / work cycles into GemmGeom::prof (tools/gemm_probe)
+#endif
+#ifndef VP_EPI_MODE
+#define VP_EPI_MODE 0  // probes only: 1 = TMEM loads only, 2 = nothing, 3 = K1 math without stores, 4 = K1 stores without math
+#endif
+#ifndef VP_K1_POLY
+#define VP_K1_POLY 0  // 1: half of the K1 epilogue's exponentials on the FMA pipe (ptx::ex2_poly)
+#endif
 
 namespace vp {
 
@@ -76,10 +90,12 @@ struct GemmCfg {
   static constexpr int A_BYTES = BM_CTA * BK * 2;
   static constexpr int B_BYTES = B_ROWS * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STG_BYTES = 4 * 8192;  // epilogue TMA-store staging: 2 x 4 KB per epilogue warp
+  static constexpr int EPI_WARPS = 8;
+  static constexpr int STG_WARP = 2 * 2048;                // TMA-store staging per epilogue warp: 2 boxes of 2 KB
+  static constexpr int STG_BYTES = EPI_WARPS * STG_WARP;
   static constexpr int BAR_BYTES = 8 * (2 * STAGES + 4) + 16;
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + STG_BYTES + BAR_BYTES + 1024;
-  static constexpr int THREADS = 256;
+  static constexpr int THREADS = 128 + 32 * EPI_WARPS;
   static constexpr int TMEM_COLS = 512;
 };
 
@@ -103,36 +119,58 @@ __device__ __forceinline__ void tile_coords(const GemmGeom& g, int t, int& mb, i
   }
 }
 
-// Per-warp staging: two 4 KB boxes, double-buffered against the async stores.
+constexpr int kEpiCols = 128;  // accumulator columns per epilogue warp and call (= K1 stats tile width)
+
+// Per-warp staging: two 2 KB boxes (32 rows x 64 B, SWIZZLE_64B), filled as
+// a pair and flushed with one proxy fence + up to two TMA stores (one bulk
+// group); the pair is rewritten only after that group has read its smem.
 struct Stager {
   uint32_t base;
   uint32_t k = 0;
-  bool probe = false;              // count cycles spent waiting for a free box (lane 0)
+  bool probe = false;              // count cycles spent waiting for free boxes (lane 0)
   unsigned long long wait_cyc = 0;
   __device__ explicit Stager(uint32_t b) : base(b) {}
-  // next free box (the store issued two boxes ago has finished reading it)
+  // next box; the first of a pair waits until the previous group read its boxes
   __device__ __forceinline__ uint32_t next() {
-    if ((threadIdx.x & 31) == 0) {
-      const unsigned long long c0 = probe ? clock64() : 0;
-      ptx::bulk_wait_read<1>();
-      if (probe) wait_cyc += clock64() - c0;
+    if ((k & 1u) == 0) {
+      if ((threadIdx.x & 31) == 0) {
+        const unsigned long long c0 = VP_GEMM_PROBE && probe ? clock64() : 0;
+        ptx::bulk_wait_read<0>();
+        if (VP_GEMM_PROBE && probe) wait_cyc += clock64() - c0;
+      }
+      __syncwarp();
     }
-    __syncwarp();
-    const uint32_t b = base + (k & 1u) * 4096u;
+    const uint32_t b = base + (k & 1u) * 2048u;
     ++k;
     return b;
   }
-  // smem address of 16-byte chunk q of this thread's row (row = lane)
+  // smem address of 16-byte chunk q (0..3) of this thread's 64-byte row
+  // (row = lane) in a SWIZZLE_64B box: chunk bits [4:5] ^= row bits [1:2]
   __device__ static __forceinline__ uint32_t chunk(uint32_t box, int q) {
     const uint32_t r = threadIdx.x & 31;
-    return box + r * 128u + ((uint32_t(q) ^ (r & 7u)) << 4);
+    return box + r * 64u + ((uint32_t(q) ^ ((r >> 1) & 3u)) << 4);
   }
-  __device__ __forceinline__ void store(const CUtensorMap* m, uint32_t box, int c0, int c1, bool add = false) {
+  __device__ static __forceinline__ void put(const CUtensorMap* m, uint32_t box, int c0, int c1, bool add) {
+    if (add) ptx::tma_reduce_add_2d(m, box, c0, c1);
+    else ptx::tma_store_2d(m, box, c0, c1);
+  }
+  // store one box / two boxes written since the last flush (one bulk group)
+  __device__ __forceinline__ void flush(const CUtensorMap* m, uint32_t box, int c0, int c1, bool add = false) {
     ptx::fence_proxy_async_smem();
     __syncwarp();
     if ((threadIdx.x & 31) == 0) {
-      if (add) ptx::tma_reduce_add_2d(m, box, c0, c1);
-      else ptx::tma_store_2d(m, box, c0, c1);
+      put(m, box, c0, c1, add);
+      ptx::bulk_commit();
+    }
+    k = (k + 1u) & ~1u;  // a lone box closes its pair
+  }
+  __device__ __forceinline__ void flush2(const CUtensorMap* m, uint32_t b0, int c0, int r0, uint32_t b1, int c1, int r1,
+                                         bool add = false) {
+    ptx::fence_proxy_async_smem();
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) {
+      put(m, b0, c0, r0, add);
+      put(m, b1, c1, r1, add);
       ptx::bulk_commit();
     }
   }
@@ -186,7 +224,7 @@ __device__ __forceinline__ void split_done(int* flag, int value, Stager& sg) {
   sg.drain();  // this warp's TMA stores are complete
   if ((threadIdx.x & 31) == 0) asm volatile("fence.proxy.async.global;" ::: "memory");
   __threadfence();
-  asm volatile("bar.sync 1, 128;" ::: "memory");  // the 4 epilogue warps of this CTA
+  asm volatile("bar.sync 2, 256;" ::: "memory");  // the 8 epilogue warps of this CTA
   if (threadIdx.x == 128) asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(flag), "r"(value) : "memory");
 }
 
@@ -197,7 +235,7 @@ __device__ __forceinline__ void split_done(int* flag, int value, Stager& sg) {
 // traffic.  A stage may then be refilled only after BOTH pairs consumed it,
 // so every empty barrier expects one commit from each pair leader.
 template <int CG, bool A_MN, bool B_MN, class Epi, int MC = 1, int NH = 1>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(384, 1)
     gemm_sm100_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       const GemmGeom g, const __grid_constant__ typename Epi::Params ep) {
   using C = GemmCfg<CG, NH>;
@@ -256,7 +294,7 @@ __global__ void __launch_bounds__(256, 1)
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(bar_tfull + 8 * a, 1);        // one tcgen05.commit
-      ptx::mbar_init(bar_tempty + 8 * a, 4 * CG);  // one arrival per epilogue warp of the pair
+      ptx::mbar_init(bar_tempty + 8 * a, C::EPI_WARPS * CG);  // one arrival per epilogue warp of the pair
     }
     ptx::fence_barrier_init();
   }
@@ -265,7 +303,10 @@ __global__ void __launch_bounds__(256, 1)
   if constexpr (CL > 1) ptx::cluster_sync(); else __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *reinterpret_cast<volatile uint32_t*>(tmem_slot);
-
+  // Register split (launch: 168 per thread): the producer / MMA warpgroup
+  // needs few, the two epilogue warpgroups get the rest (128*56 + 256*224 = 384*168).
+  if (warp < 4) {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 56;");
   if (warp == 0 && lane == 0) {
     // ===== TMA producer =====
     const uint64_t polA = make_policy(g.pol_a, Epi::kAStreams);
@@ -347,7 +388,7 @@ __global__ void __launch_bounds__(256, 1)
       }
     };
     // probe (g.prof, CTA 0): cycles the issuer spent waiting for smem stages / accumulators
-    const bool probe = g.prof != nullptr && blockIdx.x == 0;
+    const bool probe = VP_GEMM_PROBE && g.prof != nullptr && blockIdx.x == 0;
     unsigned long long w_full = 0, w_acc = 0;
     auto wait_full = [&](int kb) {
       const uint32_t it = it0 + kb;
@@ -435,76 +476,77 @@ __global__ void __launch_bounds__(256, 1)
       }
       ptx::mma_commit<CG>(bar_tfull + 8 * acc, pair_mask);
     }
-  } else if (warp >= 4) {
-    // ===== epilogue =====
-    const int ew = warp - 4;
-    Stager sg(stg + uint32_t(ew) * 8192u);
-    sg.probe = g.prof != nullptr && blockIdx.x == 0 && ew == 0;
+  }
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 224;");
+    // ===== epilogue: 8 warps =====
+    // warp 4 + ew reads TMEM lanes 32 * (ew % 4) .. +31 (the lane quadrant a
+    // warp may access is fixed by warp id % 4) and column group ew / 4, i.e.
+    // 128 of the 256 accumulator columns of each N half.
+    const int ew = warp - 4, quad = ew & 3, cgp = ew >> 2;
+    Stager sg(stg + uint32_t(ew) * uint32_t(C::STG_WARP));
+    sg.probe = VP_GEMM_PROBE && g.prof != nullptr && blockIdx.x == 0 && ew == 0;
+    const bool probe = sg.probe;
     uint32_t tc = 0;
-    unsigned long long epi_wait_cyc = 0, epi_work_cyc = 0;  // probe (NH == 2, CTA 0, warp 4)
+    unsigned long long epi_wait_cyc = 0, epi_work_cyc = 0;  // probe (CTA 0, warp 4)
     for (int u = cluster; u < num_units; u += nclusters, ++tc) {
       int mc, nb;
       const int t = unit_tile(u), sp = unit_split(u);
       tile_coords(gc, t, mc, nb);
       const int mb = mc * MC + int(pair);
       int* flag = g.splits > 1 ? g.split_flags + 2 * t + int(rank) : nullptr;
-      if constexpr (NH == 2) {
-        // halves complete (and are released) separately: see the staggered issuer
-        const int row = mb * C::BM + int(rank) * C::BM_CTA + ew * 32 + lane;
-        const bool probe = g.prof != nullptr && blockIdx.x == 0 && ew == 0;
-        const typename Epi::Pre pre = Epi::prepare(ep, g, row, nb * C::BN_TILE);
+      const int row = mb * C::BM + int(rank) * C::BM_CTA + quad * 32 + lane;
+      const typename Epi::Pre pre = Epi::prepare(ep, g, row, nb * C::BN_TILE);
+      // one accumulator per N half (NH == 2, released separately: see the
+      // staggered issuer) or one double-buffered 256-column accumulator (NH == 1)
+      constexpr int NWAIT = NH == 2 ? 2 : 1;
 #pragma unroll 1
-        for (int hh = 0; hh < 2; ++hh) {
-          const unsigned long long c0 = probe ? clock64() : 0;
-          if (g.epi_wait) ptx::mbar_wait_backoff(bar_tfull + 8 * hh, tc & 1u);
-          else ptx::mbar_wait(bar_tfull + 8 * hh, tc & 1u);
-          ptx::tc_fence_after();
-          const unsigned long long c1 = probe ? clock64() : 0;
-          const uint32_t taddr = tmem_base + hh * C::BN + (uint32_t(ew * 32) << 16);
-          // a 512-wide tile's second half may lie wholly past N (ragged last
-          // tile): it has no columns, no stats slot and nothing to store
-          if (hh == 0 && sp > 0) split_wait(flag, g.flag_base + sp);
-          if (nb * C::BN_TILE + hh * C::BN < g.N)
-            Epi::apply(ep, g, taddr, row, nb * C::BN_TILE + hh * C::BN, nb * 2 + hh, sg, pre, sp > 0);
-          if (probe && lane == 0) {
-            epi_wait_cyc += c1 - c0;
-            epi_work_cyc += clock64() - c1;
-          }
-          ptx::tc_fence_before();
-          __syncwarp();
-          if (lane == 0) ptx::mbar_arrive_remote(bar_tempty + 8 * hh, leader);
-        }
-        if (flag) split_done(flag, g.flag_base + sp + 1, sg);
-        continue;
-      }
-      const uint32_t acc = tc % NACC, aph = (tc / NACC) & 1u;
-      const typename Epi::Pre pre = Epi::prepare(ep, g, mb * C::BM + int(rank) * C::BM_CTA + ew * 32 + lane, nb * C::BN_TILE);
-      if (g.epi_wait) ptx::mbar_wait_backoff(bar_tfull + 8 * acc, aph);
-      else ptx::mbar_wait(bar_tfull + 8 * acc, aph);
-      ptx::tc_fence_after();
-      const uint32_t taddr = tmem_base + acc * C::BN + (uint32_t(ew * 32) << 16);
-      const int row = mb * C::BM + int(rank) * C::BM_CTA + ew * 32 + lane;
+      for (int hw = 0; hw < NWAIT; ++hw) {
+        const uint32_t slot = NH == 2 ? uint32_t(hw) : tc % NACC;
+        const uint32_t par = NH == 2 ? (tc & 1u) : ((tc / NACC) & 1u);
+        const unsigned long long c0 = probe ? clock64() : 0;
+        if (g.epi_wait) ptx::mbar_wait_backoff(bar_tfull + 8 * slot, par);
+        else ptx::mbar_wait(bar_tfull + 8 * slot, par);
+        ptx::tc_fence_after();
+        const unsigned long long c1 = probe ? clock64() : 0;
+        if (hw == 0 && sp > 0) split_wait(flag, g.flag_base + sp);
 #pragma unroll 1
-      for (int hh = 0; hh < NH; ++hh)
-        // a 512-wide tile's second half may lie wholly past N (ragged last
-        // tile): it has no columns, no stats slot and nothing to store
-        if (nb * C::BN_TILE + hh * C::BN < g.N) {
-          if (hh == 0 && sp > 0) split_wait(flag, g.flag_base + sp);
-          Epi::apply(ep, g, taddr + hh * C::BN, row, nb * C::BN_TILE + hh * C::BN, nb * NH + hh, sg, pre, sp > 0);
+        for (int hh = (NH == 2 ? hw : 0); hh < (NH == 2 ? hw + 1 : NH); ++hh) {
+          const int col0 = nb * C::BN_TILE + hh * C::BN + cgp * kEpiCols;
+          const uint32_t taddr = tmem_base + (NH == 2 ? 0u : slot * C::BN) + uint32_t(hh * C::BN + cgp * kEpiCols) +
+                                 (uint32_t(quad * 32) << 16);
+          // a ragged last tile's trailing column groups lie wholly past N:
+          // no columns, no stats slot, nothing to store
+#if VP_EPI_MODE == 0 || VP_EPI_MODE >= 3
+          if (col0 < g.N) Epi::apply(ep, g, taddr, row, col0, col0 / kEpiCols, sg, pre, sp > 0);
+#elif VP_EPI_MODE == 1
+          // probe: TMEM loads only (results discarded)
+          tmem_chunks(taddr, 4, [&](uint32_t (&r)[32], int) {
+            uint32_t x = 0;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) x ^= r[j];
+            if (x == 0x9e3779b9u && g.prof) g.prof[15] = x;
+          });
+#endif
         }
-      ptx::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        if constexpr (CG == 1) ptx::mbar_arrive(bar_tempty + 8 * acc);
-        else ptx::mbar_arrive_remote(bar_tempty + 8 * acc, leader);
+        if (probe && lane == 0) {
+          epi_wait_cyc += c1 - c0;
+          epi_work_cyc += clock64() - c1;
+        }
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if constexpr (CG == 1) ptx::mbar_arrive(bar_tempty + 8 * slot);
+          else ptx::mbar_arrive_remote(bar_tempty + 8 * slot, leader);
+        }
       }
       if (flag) split_done(flag, g.flag_base + sp + 1, sg);
     }
     sg.drain();
-    if (g.prof != nullptr && blockIdx.x == 0 && ew == 0 && lane == 0) {
+    if (probe && lane == 0) {
       g.prof[6] = epi_wait_cyc;
-      g.prof[8] = sg.wait_cyc;
       g.prof[7] = epi_work_cyc;
+      g.prof[8] = sg.wait_cyc;
     }
   }
   __syncwarp();
@@ -524,11 +566,11 @@ __global__ void __launch_bounds__(256, 1)
 
 // ---------------------------------------------------------------------------
 // Epilogues.  apply() runs on one epilogue warp: thread `lane` owns
-// accumulator row `row` (may be >= M: masked), columns [col0, col0 + 256).
+// accumulator row `row` (may be >= M: masked), columns [col0, col0 + 128).
 // tcgen05.ld is warp-collective, so loads stay outside row masks.
 //
 // Stores go through a per-warp smem staging box and TMA (Params::use_tma):
-// the warp writes a 32-row x 128-byte box in the SWIZZLE_128B layout (each
+// the warp writes a 32-row x 64-byte box in the SWIZZLE_64B layout (each
 // thread one row, 16-byte chunks XOR-permuted by row: bank-conflict free)
 // and one lane issues cp.async.bulk.tensor.  The global writes are full
 // lines and asynchronous, so the epilogue finishes (and releases its TMEM
@@ -548,7 +590,7 @@ struct EpiStoreF32 {
     int64_t ld_stats;
     const float* row_scale;  // optional per-row factor applied on store
     int accumulate = 0;      // out += D instead of out = D (gradient accumulation)
-    int use_tma = 0;         // stores through `map` (fp32 [M x N], 32 x 32 boxes, SWIZZLE_128B)
+    int use_tma = 0;         // stores through `map` (fp32 [M x N], 32 x 16 boxes, SWIZZLE_64B)
     CUtensorMap map;
   };
   // per-row inputs loaded before the accumulator is waited for (hides their latency)
@@ -561,7 +603,7 @@ struct EpiStoreF32 {
   __device__ static void apply(const Params& p, const GemmGeom& g, uint32_t taddr, int row, int col0, int nb,
                                Stager& sg, const Pre& pre, bool split_add) {
     const bool row_ok = row < g.M;
-    const int nvalid = min(GemmCfg<1>::BN, g.N - col0);
+    const int nvalid = min(kEpiCols, g.N - col0);
     const int nch = (nvalid + 31) / 32;
     const float rs = pre.rs;
     const bool add = p.accumulate != 0 || split_add;
@@ -570,8 +612,15 @@ struct EpiStoreF32 {
     if (p.use_tma) {
       tmem_chunks(taddr, nch, [&](uint32_t (&r)[32], int c) {
         if (p.row_scale) {
+          const uint64_t rs2 = ptx::f2pack(rs, rs);
 #pragma unroll
-          for (int j = 0; j < 32; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) * rs);
+          for (int j = 0; j < 16; ++j) {
+            const uint64_t v = ptx::fmul2(ptx::f2pack(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1])), rs2);
+            float lo, hi;
+            ptx::f2unpack(v, lo, hi);
+            r[2 * j] = __float_as_uint(lo);
+            r[2 * j + 1] = __float_as_uint(hi);
+          }
         }
         if (p.tile_max) {
           const int nv = nvalid - c * 32;
@@ -579,10 +628,15 @@ struct EpiStoreF32 {
           for (int j = 0; j < 32; ++j)
             if (j < nv) mx = fmaxf(mx, __uint_as_float(r[j]));
         }
-        const uint32_t box = sg.next();
+        // two 16-column fp32 boxes per chunk, one fence
+        const uint32_t b0 = sg.next();
 #pragma unroll
-        for (int q = 0; q < 8; ++q) ptx::st_shared_v4(Stager::chunk(box, q), r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
-        sg.store(&p.map, box, col0 + c * 32, row0, add);
+        for (int q = 0; q < 4; ++q) ptx::st_shared_v4(Stager::chunk(b0, q), r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
+        const uint32_t b1 = sg.next();
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          ptx::st_shared_v4(Stager::chunk(b1, q), r[16 + 4 * q], r[16 + 4 * q + 1], r[16 + 4 * q + 2], r[16 + 4 * q + 3]);
+        sg.flush2(&p.map, b0, col0 + c * 32, row0, b1, col0 + c * 32 + 16, row0, add);
       });
     } else {
       float* dst = p.out + int64_t(row) * p.ldo + col0;
@@ -626,22 +680,24 @@ struct EpiStoreF32 {
 };
 
 // K1 fused stats epilogue (forward of the output layer).  For row i and
-// vocab tile j (256 columns of this shard):
+// vocab tile j (kEpiCols = 128 columns of this shard):
 //   m_ij = max_v Y[i,v];  y_tgt[i] = Y[i, g_i - row_begin] when the label falls here;
 //   P[i,v] = bf16(exp(Y[i,v] - q_ij)),  s_ij = sum_v exp(Y[i,v] - q_ij),
-// where the reference q_ij is ONE value per row, r_i = m_i0 (the max of the
-// row's first vocab tile), published by the j = 0 tiles (first wave) through
-// a release flag per 128-row block.  A per-row reference makes
-// softmax' = P * cfac_i (one factor per row), which the dX epilogue and the
-// scaled-X operand of dW absorb: no pass over P is needed after K1.
-// Tiles that run before r_i is published (part of the first wave) use their
-// own max (q_ij = m_ij) and log their 32-row group in fix_list; rows whose
-// logits exceed r_i + kMaxRefGap (exp would overflow) are marked in row_bad
-// and re-referenced to the row max after the stats merge.  Full-vocab
-// logits are never written to or re-read from HBM.
+// where the reference q_ij is ONE value per row, r_i = m_i0 + kRefLift (the
+// max of the row's first vocab tile, lifted), published by the j = 0 tiles
+// through a release flag per 128-row block; later tiles of the row wait for
+// it (tile (m, 0) always precedes (m, j) in the persistent schedule).  A
+// per-row reference makes softmax' = P * cfac_i (one factor per row), which
+// the dX epilogue and the scaled-X operand of dW absorb: no pass over P is
+// needed after K1, and P is rounded to bf16 exactly once.  Rows whose logits
+// exceed r_i + kMaxRefGap (exp would overflow) are marked in row_bad and
+// re-referenced to the row max after the stats merge.  (The fix_list path
+// for tiles stored against their own max is kept for robustness; the wait
+// makes it unreachable.)  Full-vocab logits never touch HBM.
 struct EpiLogitStats {
   static constexpr bool kAStreams = false;  // A = X is reused by every vocab tile
-  static constexpr float kMaxRefGap = 64.f;
+  static constexpr float kMaxRefGap = 64.f;  // e^{Y - q} <= e^64: P, its sums and P.W stay finite in fp32
+  static constexpr float kRefLift = 16.f;    // r_i sits this far above the first vocab tile's max
   struct Params {
     __nv_bfloat16* P;
     int64_t ldp;
@@ -659,7 +715,7 @@ struct EpiLogitStats {
     int* bad_list;          // [M]
     int* fix_count;         // (32-row group, tile) pairs stored relative to their own max
     int2* fix_list;         // [ceil(M/32) x tiles_n]
-    int use_tma = 0;        // P stored through `map` (bf16 [M x N], 32 x 64 boxes, SWIZZLE_128B)
+    int use_tma = 0;        // P stored through `map` (bf16 [M x N], 32 x 32 boxes, SWIZZLE_64B)
     CUtensorMap map;
   };
   // max of the valid columns and the label logit (first pass of a two-pass tile)
@@ -698,38 +754,52 @@ struct EpiLogitStats {
     __nv_bfloat16* dst = p.P + int64_t(row) * p.ldp + col0;
     const bool vec = ((p.ldp & 7) == 0) && ((reinterpret_cast<uintptr_t>(p.P) & 15) == 0);
     const int nch = (nvalid + 31) / 32;
-    uint32_t box = 0;
-    float sp[4] = {0.f, 0.f, 0.f, 0.f};  // independent partial sums / maxima (no serial chains)
-    float mp[4] = {mx, mx, mx, mx};
+    // independent partial sums (packed f32x2 pairs) and maxima: no serial chains
+    uint64_t sp2[2] = {ptx::f2pack(0.f, 0.f), ptx::f2pack(0.f, 0.f)};
+    float mp[2] = {mx, mx};
+    const uint64_t l2e2 = ptx::f2pack(kLog2e, kLog2e), nref2 = ptx::f2pack(-refs, -refs);
+    uint32_t box0 = 0;  // first box of the pair being filled (TMA path)
     tmem_chunks(taddr, nch, [&](uint32_t (&r)[32], int c) {
       const int nv = nvalid - c * 32;
       uint32_t pk[16];
       if (nv >= 32) {
-        // full chunk: no column masks
+        // full chunk: no column masks; FFMA2 / FADD2 on column pairs
         if (track) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j) mp[j & 3] = fmaxf(mp[j & 3], __uint_as_float(r[j]));
+          for (int j = 0; j < 16; ++j)
+            mp[j & 1] = fmaxf(mp[j & 1], fmaxf(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1])));
         }
+#if VP_EPI_MODE == 4
+#pragma unroll
+        for (int j = 0; j < 16; ++j) pk[j] = r[2 * j] ^ r[2 * j + 1];  // probe: stores without the math
+#else
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-          const float e0 = ptx::ex2(fmaf(__uint_as_float(r[2 * j]), kLog2e, -refs));
-          const float e1 = ptx::ex2(fmaf(__uint_as_float(r[2 * j + 1]), kLog2e, -refs));
-          sp[(2 * j) & 3] += e0;
-          sp[(2 * j + 1) & 3] += e1;
+          const uint64_t x2 =
+              ptx::ffma2(ptx::f2pack(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1])), l2e2, nref2);
+          float x0, x1;
+          ptx::f2unpack(x2, x0, x1);
+          const float e0 = ptx::ex2(x0);
+#if VP_K1_POLY
+          const float e1 = ptx::ex2_poly(x1);  // half the exponentials on the FMA pipe
+#else
+          const float e1 = ptx::ex2(x1);
+#endif
+          sp2[j & 1] = ptx::fadd2(sp2[j & 1], ptx::f2pack(e0, e1));
           pk[j] = ptx::pack_bf16(e0, e1);
         }
+#endif
       } else {
         if (track) {
 #pragma unroll
           for (int j = 0; j < 32; ++j)
-            if (j < nv) mp[j & 3] = fmaxf(mp[j & 3], __uint_as_float(r[j]));
+            if (j < nv) mp[j & 1] = fmaxf(mp[j & 1], __uint_as_float(r[j]));
         }
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
           const float e0 = (2 * j < nv) ? ptx::ex2(fmaf(__uint_as_float(r[2 * j]), kLog2e, -refs)) : 0.f;
           const float e1 = (2 * j + 1 < nv) ? ptx::ex2(fmaf(__uint_as_float(r[2 * j + 1]), kLog2e, -refs)) : 0.f;
-          sp[(2 * j) & 3] += e0;
-          sp[(2 * j + 1) & 3] += e1;
+          sp2[j & 1] = ptx::fadd2(sp2[j & 1], ptx::f2pack(e0, e1));
           pk[j] = ptx::pack_bf16(e0, e1);
         }
       }
@@ -742,15 +812,21 @@ struct EpiLogitStats {
           has_t = true;
         }
       }
+#if VP_EPI_MODE == 3
+      if (pk[0] == 0x12345u && pk[15] == 0x777u) has_t = !has_t;  // probe: math without the stores
+      if (false) {
+#else
       if (p.use_tma) {
-        // a 64-column box holds chunks c (even: 16-byte chunks 0..3) and c+1 (4..7)
-        if ((c & 1) == 0) box = sg.next();
-        const int q0 = (c & 1) * 4;
+#endif
+        // one 32-column bf16 box per chunk, flushed in pairs (one fence per
+        // two chunks); columns past N are clipped by the TMA unit
+        const uint32_t box = sg.next();
 #pragma unroll
-        for (int q = 0; q < 4; ++q) ptx::st_shared_v4(Stager::chunk(box, q0 + q), pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
-        // an odd chunk count only occurs in the shard's last tile, whose
-        // columns past N are clipped by the TMA unit
-        if ((c & 1) == 1 || c + 1 == nch) sg.store(&p.map, box, col0 + (c & ~1) * 32, row0);
+        for (int q = 0; q < 4; ++q)
+          ptx::st_shared_v4(Stager::chunk(box, q), pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+        if (c & 1) sg.flush2(&p.map, box0, col0 + (c - 1) * 32, row0, box, col0 + c * 32, row0);
+        else if (c + 1 == nch) sg.flush(&p.map, box, col0 + c * 32, row0);
+        else box0 = box;
       } else if (row_ok) {
         if (nv >= 32 && vec) {
           uint4* d4 = reinterpret_cast<uint4*>(dst + c * 32);
@@ -764,8 +840,11 @@ struct EpiLogitStats {
         }
       }
     });
-    sum = (sp[0] + sp[1]) + (sp[2] + sp[3]);
-    if (track) mx = fmaxf(fmaxf(mp[0], mp[1]), fmaxf(mp[2], mp[3]));
+    float a0, a1, b0, b1;
+    ptx::f2unpack(sp2[0], a0, a1);
+    ptx::f2unpack(sp2[1], b0, b1);
+    sum = (a0 + b0) + (a1 + b1);
+    if (track) mx = fmaxf(mp[0], mp[1]);
   }
 
   // Per-row inputs loaded before the accumulator is waited for: the label,
@@ -796,7 +875,7 @@ struct EpiLogitStats {
                                Stager& sg, const Pre& pre, bool /*split_add: never split*/) {
     const bool row_ok = row < g.M;
     const int lane = threadIdx.x & 31;
-    const int nvalid = min(GemmCfg<1>::BN, g.N - col0);
+    const int nvalid = min(kEpiCols, g.N - col0);
     int lb = -1;
     if (row_ok && pre.label >= p.row_begin && pre.label < p.row_end)
       lb = int(pre.label - p.row_begin) - col0;  // offset inside tile
@@ -804,8 +883,17 @@ struct EpiLogitStats {
     int f = pre.flag;
     float pref = pre.ref;
     if (nb != 0 && !f && row_ok) {
+      // Wait for r_i rather than fall back to this tile's own max (which
+      // would cost a second bf16 rounding of P in the fix pass).  Deadlock
+      // free: under every rasterisation tile (m, 0) precedes all (m, j > 0)
+      // in the persistent schedule, all clusters are co-resident, and a tile
+      // only ever waits on a smaller tile index.
       f = load_flag(p, row);
-      if (f) pref = p.row_ref[row];
+      while (!f) {
+        __nanosleep(128);
+        f = load_flag(p, row);
+      }
+      pref = p.row_ref[row];
     }
     f = __all_sync(0xffffffffu, f || !row_ok);  // warp-uniform path (rows past M follow their warp)
     (void)blk;
@@ -817,7 +905,12 @@ struct EpiLogitStats {
       scan(taddr, nvalid, lb, mx, yt, has_t);
       ref = mx;
       if (nb == 0) {
-        if (row_ok) p.row_ref[row] = mx;
+        // r_i = first-tile max + kRefLift: later tiles overflow-check against
+        // r_i + kMaxRefGap, i.e. kMaxRefGap + kRefLift nats above the first
+        // tile's max, before a row needs the (double-rounding) re-reference;
+        // bf16 keeps full relative precision for the smaller values
+        ref = mx + kRefLift;
+        if (row_ok) p.row_ref[row] = ref;
         asm volatile("bar.sync 1, 128;" ::: "memory");  // the 4 epilogue warps of this CTA
         if (threadIdx.x == 128) {
           __threadfence();

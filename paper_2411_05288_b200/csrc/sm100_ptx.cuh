@@ -305,6 +305,49 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
+// ---- packed fp32 pairs (FFMA2 / FADD2 / FMUL2: two lanes per instruction) --
+__device__ __forceinline__ uint64_t f2pack(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void f2unpack(uint64_t v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+
+// 2^x on the FMA / integer pipes (no MUFU): x = n + f with n = rint(x)
+// (magic-number rounding), f in [-0.5, 0.5], 2^f by a degree-3 minimax
+// polynomial (max relative error 7.5e-5, below bf16's 2^-9 storage step),
+// and 2^n added into the exponent field.  x is clamped to >= -125 (result
+// >= 2^-125.5 instead of flushing to 0; finite up to x < 128).  B200's MUFU
+// issues 2^x at a quarter of the FMA pipe's rate, so the K1 epilogue sends
+// half of its exponentials here (the FlashAttention-4 split).
+__device__ __forceinline__ float ex2_poly(float x) {
+  constexpr float kMagic = 12582912.f;  // 1.5 * 2^23: x + kMagic rounds x to an integer in the low mantissa bits
+  x = fmaxf(x, -125.f);
+  const float t = x + kMagic;
+  const float f = x - (t - kMagic);
+  float p = fmaf(0.0551704922664135f, f, 0.2426093802065827f);
+  p = fmaf(p, f, 0.6932610346899266f);
+  p = fmaf(p, f, 0.9999281846615126f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);

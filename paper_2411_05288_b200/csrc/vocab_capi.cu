@@ -288,14 +288,6 @@ void stats_reduce(vp_ctx_s* c, vp_state_s* st, bool with_sum) {
   ++c->launches;
 }
 
-void rescale_P(vp_ctx_s* c, vp_state_s* st, const float* tile_m, const float* mref, const float* inv) {
-  const int64_t work = st->n_tok * ceil_div(st->rows, 8);
-  vp::k_rescale_P<<<c->grid_for(work, 256), 256, 0, c->stream>>>(st->P, st->ldp, int(st->n_tok), int(st->rows),
-                                                                 tile_m, st->n_tok, mref, inv);
-  VP_KCHECK();
-  ++c->launches;
-}
-
 float* inv_of(vp_ctx_s* c, const float* s, int64_t n) {
   float* inv = c->buf<float>(c->inv, size_t(n));
   vp::k_inv<<<unsigned(ceil_div(n, 256)), 256, 0, c->stream>>>(s, int(n), inv);
@@ -649,7 +641,7 @@ void naive(vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* shards, const vp_
   // F2: exp-sums against the global max, re-reading the logits, then the sum all-reduce
   for (int k = 0; k < n; ++k) {
     vp_state_s* st = states[k];
-    vp::k_naive_exp_sum<<<unsigned(T), 256, 0, c->stream>>>(st->Y, st->rows, int(st->rows), out.m, st->P, st->ldp,
+    vp::k_naive_exp_sum<<<unsigned(T), 256, 0, c->stream>>>(st->Y, st->rows, int(st->rows), out.m, nullptr, st->ldp,
                                                              st->s_loc);
     VP_KCHECK();
     ++c->launches;
@@ -669,7 +661,10 @@ void naive(vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* shards, const vp_
   std::vector<float*> partials(static_cast<size_t>(n));
   for (int k = 0; k < n; ++k) {
     vp_state_s* st = states[k];
-    rescale_P(c, st, nullptr, nullptr, inv);
+    vp::k_naive_softmax<<<c->grid_for(T * ceil_div(st->rows, 8), 256), 256, 0, c->stream>>>(
+        st->Y, st->rows, int(T), int(st->rows), out.m, inv, st->P, st->ldp);
+    VP_KCHECK();
+    ++c->launches;
     st->form = kGlobal;
     st->has_S = true;
     partials[size_t(k)] = c->distributed() ? gx : st->A;

@@ -11,7 +11,7 @@
 
 namespace vp {
 
-constexpr int kTileN = 256;          // K1 vocab tile width (stats granularity)
+constexpr int kTileN = 128;          // K1 vocab tile width (stats granularity) = kEpiCols of the GEMM epilogue
 constexpr int kMaxLocalShards = 16;  // shards simulated on one device
 constexpr float kLog2e = 1.4426950408889634f;
 
@@ -220,42 +220,7 @@ __global__ void k_pack_stats(const float* __restrict__ m, const float* __restric
 }
 
 // ---------------------------------------------------------------------------
-// In-place rescale of the stored P (bf16 [n x ldp], valid cols < cols):
-//   P[i,v] <- P[i,v] * exp(tile_m[v/256][i] - mref[i]) * inv[i]
-// tile_m == null drops the tile factor (P already relative to mref).
-// 8 bf16 per thread (16-byte vectors); grid-stride.
-// ---------------------------------------------------------------------------
-__global__ void k_rescale_P(__nv_bfloat16* __restrict__ P, int64_t ldp, int n, int cols,
-                            const float* __restrict__ tile_m, int64_t ld_stats, const float* __restrict__ mref,
-                            const float* __restrict__ inv) {
-  const int vec_per_row = (cols + 7) / 8;
-  const int64_t total = int64_t(n) * vec_per_row;
-  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < total; t += int64_t(gridDim.x) * blockDim.x) {
-    const int i = int(t / vec_per_row);
-    const int v0 = int(t - int64_t(i) * vec_per_row) * 8;
-    float f = inv[i];
-    if (tile_m) f *= fast_exp(tile_m[int64_t(v0 / kTileN) * ld_stats + i] - mref[i]);
-    uint4* ptr = reinterpret_cast<uint4*>(P + int64_t(i) * ldp + v0);
-    uint4 u = *ptr;
-    __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u);
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      float2 x = __bfloat1622float2(h2[q]);
-      x.x *= f;
-      x.y *= f;
-      h2[q] = __floats2bfloat162_rn(x.x, x.y);
-    }
-    // columns >= cols inside the last vector are padding: keep them zero
-    if (v0 + 8 > cols) {
-      __nv_bfloat16* e = reinterpret_cast<__nv_bfloat16*>(&u);
-      for (int q = cols - v0; q < 8; ++q) e[q] = __float2bfloat16(0.f);
-    }
-    *ptr = u;
-  }
-}
-
-// Per-row factor tables for the rescale:  inv = 1/s  (alg2 local softmax'),
-// inv = 1/sum_g (alg1 global), with mref = m_loc or m_global.
+// inv = 1/s (per-row normalisers).
 __global__ void k_inv(const float* __restrict__ s, int n, float* __restrict__ inv) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) inv[i] = 1.f / s[i];
@@ -392,6 +357,7 @@ __global__ void k_naive_exp_sum(const float* __restrict__ Y, int64_t ldy, int co
 #pragma unroll
     for (int q = 0; q < 4; ++q) e[q] = (v + q < cols) ? fast_exp(Y[int64_t(i) * ldy + v + q] - mi) : 0.f;
     acc += (e[0] + e[1]) + (e[2] + e[3]);
+    if (P == nullptr) continue;  // sums only (the softmax is written once, in B)
     __nv_bfloat162* d = reinterpret_cast<__nv_bfloat162*>(P + int64_t(i) * ldp + v);
     if (v + 4 <= cols) {
       d[0] = __floats2bfloat162_rn(e[0], e[1]);
@@ -420,8 +386,32 @@ __global__ void k_gather_target(const float* __restrict__ Y, int64_t ldy, const 
   if (g >= rb && g < re) yt[i] = Y[int64_t(i) * ldy + (g - rb)];
 }
 
+// Naive B normalisation (VM.cpp:127-131): P[i,v] = bf16(e^{Y[i,v] - m_i} / sum_i),
+// re-reading the fp32 logits (the naive variant's extra pass) and rounding to
+// bf16 once.  8 columns per thread, 16-byte P stores, padding columns zeroed.
+__global__ void k_naive_softmax(const float* __restrict__ Y, int64_t ldy, int n, int cols, const float* __restrict__ m,
+                                const float* __restrict__ inv, __nv_bfloat16* __restrict__ P, int64_t ldp) {
+  const int vec_per_row = (cols + 7) / 8;
+  const int64_t total = int64_t(n) * vec_per_row;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < total; t += int64_t(gridDim.x) * blockDim.x) {
+    const int i = int(t / vec_per_row);
+    const int v0 = int(t - int64_t(i) * vec_per_row) * 8;
+    const float mi = m[i], f = inv[i];
+    const float* y = Y + int64_t(i) * ldy + v0;
+    uint4 u;
+    __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float a = (v0 + 2 * q < cols) ? fast_exp(y[2 * q] - mi) * f : 0.f;
+      const float b = (v0 + 2 * q + 1 < cols) ? fast_exp(y[2 * q + 1] - mi) * f : 0.f;
+      h2[q] = __floats2bfloat162_rn(a, b);
+    }
+    *reinterpret_cast<uint4*>(P + int64_t(i) * ldp + v0) = u;
+  }
+}
+
 // Debug/parity materialisation (assemble_forward softmax, VM.cpp:281-286):
-// out[i, v] = P[i,v] * f(i, v) in fp32 (same factor as k_rescale_P).
+// out[i, v] = P[i,v] * f(i, v) in fp32.
 __global__ void k_materialize(const __nv_bfloat16* __restrict__ P, int64_t ldp, int n, int cols,
                               const float* __restrict__ tile_m, int64_t ld_stats, const float* __restrict__ mref,
                               const float* __restrict__ mul, float* __restrict__ out, int64_t ldo) {

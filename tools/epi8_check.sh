@@ -1,0 +1,8 @@
+#!/bin/bash
+timeout 300 ./tools/gemm_selftest > gpurun_out/selftest.log 2>&1; echo selftest rc=$?; grep -E "FAIL|SELFTEST|CUDA" gpurun_out/selftest.log | head -10
+for k in "k1 0" "dw -4"; do set -- $k; VP_NH=2 timeout 120 ./tools/gemm_probe $1 $2 0 0 20; done
+VP_NH=2 timeout 120 ./tools/gemm_probe_poly k1 0 0 0 20
+timeout 300 ./tools/vpipe_verify --hidden 4096 --vocab 128256 --devices 8 --batch 1 --seq-len 16; echo verify_rc=$?
+for i in 1 2; do timeout 300 python bench.py --no-cpu-baseline --no-e2e > gpurun_out/bench_e8_$i.json 2>gpurun_out/bench_e8_$i.err; echo bench_rc=$?;
+python -c "import json,sys; d=json.load(open('gpurun_out/bench_e8_$i.json')); g=d['roofline']['gemms']; print('%8.0f tok/s %6.2f ms | logits %.2f dx %.2f dw %.2f | clk %s' % (d['value'], d['ms_per_step'], g['logits']['avg_ms'], g['dx']['avg_ms'], g['dw']['avg_ms'], d['clocks']['sm_mhz']))"; done
+timeout 900 python -m pytest tests -m gpu -q 2>&1 | tail -4

@@ -58,7 +58,7 @@ int main(int argc, char** argv) {
   fill<<<1024, 256>>>(X, T * h, 1.f, 1);
   fill<<<1024, 256>>>(W, V * h, 0.02f, 2);
   fill<<<1024, 256>>>(P, T * V, 4e-6f, 3);  // softmax-like magnitudes
-  const int ntiles = int((V + 255) / 256);
+  const int ntiles = int((V + vp::kEpiCols - 1) / vp::kEpiCols);
   float *tm, *ts, *yt;
   CK(cudaMalloc(&tm, int64_t(ntiles) * T * 4));
   CK(cudaMalloc(&ts, int64_t(ntiles) * T * 4));

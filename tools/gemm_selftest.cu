@@ -112,7 +112,7 @@ static void check_store(int cg, bool amn, bool bmn, int M, int N, int K, int nsm
 static void check_stats(int cg, int M, int N, int K, int nsm, int mc = 1, int nh = 1) {
   const int64_t ld = (K + 7) / 8 * 8;
   const int64_t ldp = (N + 63) / 64 * 64;
-  const int tiles = (N + 255) / 256;
+  const int tiles = (N + vp::kEpiCols - 1) / vp::kEpiCols;
   __nv_bfloat16 *A, *B, *P;
   float *R, *tm, *ts, *yt;
   int64_t* lab;
@@ -160,10 +160,10 @@ static void check_stats(int cg, int M, int N, int K, int nsm, int mc = 1, int nh
   for (int i = 0; i < M; ++i) {
     for (int t = 0; t < tiles; ++t) {
       double mx = -1e300;
-      for (int v = t * 256; v < std::min(N, t * 256 + 256); ++v) mx = std::max(mx, double(r[size_t(i) * N + v]));
+      for (int v = t * vp::kEpiCols; v < std::min(N, t * vp::kEpiCols + vp::kEpiCols); ++v) mx = std::max(mx, double(r[size_t(i) * N + v]));
       double s = 0;
       const double q = hq[size_t(t) * M + i];
-      for (int v = t * 256; v < std::min(N, t * 256 + 256); ++v) {
+      for (int v = t * vp::kEpiCols; v < std::min(N, t * vp::kEpiCols + vp::kEpiCols); ++v) {
         const double e = std::exp(double(r[size_t(i) * N + v]) - q);
         s += e;
         uint32_t bits = uint32_t(hp[size_t(i) * ldp + v]) << 16;
@@ -233,7 +233,7 @@ static void bench_store(int cg, bool amn, bool bmn, int M, int N, int K, int ras
 }
 
 static void bench_stats(int cg, int M, int N, int K, int nsm) {
-  const int tiles = (N + 255) / 256;
+  const int tiles = (N + vp::kEpiCols - 1) / vp::kEpiCols;
   __nv_bfloat16 *A, *B, *P;
   float *tm, *ts, *yt;
   CK(cudaMalloc(&A, int64_t(M) * K * 2));
