@@ -364,7 +364,7 @@ void pass_S_common(vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* s, vp_sta
                                                    st->row_ref, vp::EpiLogitStats::kMaxRefGap, st->row_bad,
                                                    st->counters, st->bad_list);
   VP_KCHECK();
-  vp::k_stats_reduce_ref<<<unsigned(ceil_div(T, 32)), 256, 0, c->stream>>>(
+  vp::k_stats_reduce_ref<<<unsigned(ceil_div(T, 32)), 512, 0, c->stream>>>(
       st->tile_m, st->tile_s, st->tile_q, int(st->ntiles), st->n_tok, T, st->row_ref, st->row_bad, st->m_loc,
       st->s_loc, st->cfac);
   VP_KCHECK();

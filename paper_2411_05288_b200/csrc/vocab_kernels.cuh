@@ -68,42 +68,63 @@ __global__ void k_stats_reduce(const float* __restrict__ tile_m, const float* __
 //   m' = max_j m_ij,  s' = sum_j s_ij e^{q_ij - m'}      (tiles in ascending j)
 // and the per-row factor that turns the stored P into softmax':
 //   cfac_i = e^{ref_i - m'_i} / s'_i,  ref_i = row_bad ? m'_i : r_i.
-__global__ void k_stats_reduce_ref(const float* __restrict__ tile_m, const float* __restrict__ tile_s,
-                                   const float* __restrict__ tile_q, int ntiles, int64_t ld, int n,
-                                   const float* __restrict__ row_ref, const int* __restrict__ row_bad,
-                                   float* __restrict__ m_out, float* __restrict__ s_out, float* __restrict__ cfac) {
-  __shared__ float sm[8][32], ss[8][32];
+// Nearly every tile has q_ij = r_i, so the sum is accumulated relative to a
+// running reference R (start r_i): s_ij adds as is, and only a tile with
+// q_ij > R (a re-referenced overflow tile) rescales.  No exp on the common
+// path and no max / sum dependency chain: the kernel runs at load speed.
+// Block = 512 threads = 16 warps x 32 rows; warp w takes tiles w, w+16, ...
+// (fixed order), then the 16 partials merge in w order.
+__global__ void __launch_bounds__(512) k_stats_reduce_ref(const float* __restrict__ tile_m,
+                                                          const float* __restrict__ tile_s,
+                                                          const float* __restrict__ tile_q, int ntiles, int64_t ld,
+                                                          int n, const float* __restrict__ row_ref,
+                                                          const int* __restrict__ row_bad, float* __restrict__ m_out,
+                                                          float* __restrict__ s_out, float* __restrict__ cfac) {
+  constexpr int W = 16;
+  __shared__ float sm[W][32], ss[W][32], sr[W][32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int row = blockIdx.x * 32 + lane;
-  float m = -INFINITY, s = 0.f;
+  float m = -INFINITY, S = 0.f, R = 0.f;
   if (row < n) {
-    for (int j = w; j < ntiles; j += 8) {
+    R = row_ref[row];
+#pragma unroll 4
+    for (int j = w; j < ntiles; j += W) {
       const int64_t o = int64_t(j) * ld + row;
-      const float mj = tile_m[o];
-      // relative to the tile max, in the log domain: a tile far below the row
-      // reference stores s = 0 (underflow) while e^{q - m} overflows
-      const float sj = expf(logf(tile_s[o]) + (tile_q[o] - mj));
-      const float nm = fmaxf(m, mj);
-      s = s * fast_exp(m - nm) + sj * fast_exp(mj - nm);
-      m = nm;
+      const float mj = tile_m[o], sj = tile_s[o], qj = tile_q[o];
+      m = fmaxf(m, mj);
+      if (qj == R) {
+        S += sj;
+      } else if (qj < R) {
+        S += sj * expf(qj - R);
+      } else {
+        S = S * expf(R - qj) + sj;
+        R = qj;
+      }
     }
   }
   sm[w][lane] = m;
-  ss[w][lane] = s;
+  ss[w][lane] = S;
+  sr[w][lane] = R;
   __syncthreads();
   if (w == 0 && row < n) {
-    float M = sm[0][lane], S = ss[0][lane];
-    for (int q = 1; q < 8; ++q) {
-      const float mq = sm[q][lane];
-      if (mq == -INFINITY) continue;
-      const float nm = fmaxf(M, mq);
-      S = S * fast_exp(M - nm) + ss[q][lane] * fast_exp(mq - nm);
-      M = nm;
+    float M = sm[0][lane], Sa = ss[0][lane], Ra = sr[0][lane];
+    for (int q = 1; q < W; ++q) {
+      M = fmaxf(M, sm[q][lane]);
+      const float Rq = sr[q][lane], Sq = ss[q][lane];
+      if (Rq == Ra) {
+        Sa += Sq;
+      } else if (Rq < Ra) {
+        Sa += Sq * expf(Rq - Ra);
+      } else {
+        Sa = Sa * expf(Ra - Rq) + Sq;
+        Ra = Rq;
+      }
     }
+    const float sprime = Sa * expf(Ra - M);  // relative to the row max
     m_out[row] = M;
-    s_out[row] = S;
+    s_out[row] = sprime;
     const float ref = row_bad[row] ? M : row_ref[row];
-    cfac[row] = expf(ref - M) / S;
+    cfac[row] = expf(ref - Ra) / Sa;  // = e^{ref - m'} / s'
   }
 }
 
