@@ -197,6 +197,46 @@ int vp_input_backward(vp_ctx_t ctx, const void* grad_out, int64_t ldg, int grad_
  * post-forward all-reduce, R/PAPER.md:582).  dtype 0 = fp32, 1 = bf16. */
 int vp_allreduce_sum(vp_ctx_t ctx, void* buf, int64_t count, int dtype);
 
+/* ---- vocabulary-pass executor (pipeline integration) --------------------- */
+/* A reference DeviceProgram (P/include/vpipe/schedule.hpp:95-100) in the text
+ * form of serialize_program (P/src/schedule.cpp:512-529); parse errors are
+ * VP_EINVAL with the reference parser's messages (:531-577). */
+typedef struct vp_program_s* vp_program_t;
+int vp_program_parse(const char* text, vp_program_t* out);
+int vp_program_destroy(vp_program_t prog);
+/* barriers: 0 = no vocabulary passes, 1 = Algorithm 2 (vocab2), 2 = Algorithm 1
+ * (vocab1, interlaced, vhalf-vocab1), method_barriers (P/src/schedule.cpp:80-88);
+ * p devices, n microbatches. */
+int vp_program_info(vp_program_t prog, int* barriers, int* p, int* n);
+/* validate_dependencies (P/src/schedule.cpp:390-447) for the vocabulary passes
+ * C0 -> S -> C1 -> T [-> C2]: violations '\n'-separated into buf (NUL-terminated,
+ * truncated to buflen), their number in *count; structural errors (missing or
+ * duplicate passes) as one message, in the reference's wording. */
+int vp_program_validate(vp_program_t prog, char* buf, int64_t buflen, int* count);
+/* Executes the program's vocabulary passes in program order (F/B/IF/IB are the
+ * caller's and are skipped): S / T on the context stream, the barrier
+ * exchanges of C1 (Algorithm 2) / C2 (Algorithm 1) on the high-priority comm
+ * stream, overlapping the passes that follow.  NCCL group (nranks == p): this
+ * rank runs device `rank` with n_shards = 1; local: every device on this GPU,
+ * n_shards = p.  batches, stats, loss, grad_x: one per microbatch (n);
+ * states: [n_shards x n] shard-major; grad_w: one per shard, zeroed, then dW
+ * of every microbatch accumulates into it.  C0 broadcasts X_i from device p-1
+ * (NCCL group: X_i of the other ranks is overwritten). */
+int vp_program_run(vp_ctx_t ctx, vp_program_t prog, const vp_batch_t* batches, const vp_shard_t* shards,
+                   int n_shards, const vp_state_t* states, vp_stats_t* stats, float* const* loss,
+                   float* const* grad_x, int64_t ldgx, float* const* grad_w, int64_t ldgw);
+
+/* ---- CUDA graphs ----------------------------------------------------------- */
+/* Capture the context's work (any vp_* calls on it, including the comm-stream
+ * fork/join and NCCL calls) into a graph replayed with one launch.  Workspace
+ * buffers must already be sized (run the same calls once eagerly first);
+ * GEMM timing must be off. */
+typedef struct vp_graph_s* vp_graph_t;
+int vp_ctx_capture_begin(vp_ctx_t ctx);
+int vp_ctx_capture_end(vp_ctx_t ctx, vp_graph_t* out);
+int vp_graph_launch(vp_graph_t graph, vp_ctx_t ctx);
+int vp_graph_destroy(vp_graph_t graph);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,0 +1,54 @@
+// Test infrastructure only: a driver around the REFERENCE's own schedule
+// builder and validator (compiled from /root/reference/proj/src/schedule.cpp
+// and cost_model.cpp by oracle/Makefile into oracle/_ref/vpipe_sched; never
+// shipped, never on the product path).  Used by tests/golden/make_programs.py
+// to pin the vocabulary-pass executor's program parser and validator
+// (paper_2411_05288_b200 vp_program_*) against the reference itself.
+//
+//   vpipe_sched build <method> <p> <n>   -> serialize_program(build_program(method, cfg))
+//                                           with the reference tests' make_cfg(p, n)
+//                                           (P/tests/test_schedule.cpp:14-24)
+//   vpipe_sched validate                 <- program text on stdin
+//                                        -> one violation per line (validate_dependencies,
+//                                           P/src/schedule.cpp:390-447); "error: ..." when
+//                                           parse_program throws
+#include <iostream>
+#include <iterator>
+#include <sstream>
+#include <string>
+
+#include "vpipe/schedule.hpp"
+
+int main(int argc, char** argv) {
+  using namespace vpipe;
+  if (argc < 2) {
+    std::cerr << "usage: vpipe_sched build <method> <p> <n> | validate\n";
+    return 2;
+  }
+  const std::string cmd = argv[1];
+  try {
+    if (cmd == "build" && argc == 5) {
+      ModelConfig cfg;
+      const int p = std::stoi(argv[3]), n = std::stoi(argv[4]);
+      cfg.b = 1;
+      cfg.s = 8;
+      cfg.h = 16;
+      cfg.V = 16 * p;
+      cfg.L = 2 * p;
+      cfg.p = p;
+      cfg.n = n;
+      std::cout << serialize_program(build_program(method_from_name(argv[2]), cfg));
+      return 0;
+    }
+    if (cmd == "validate") {
+      const std::string text((std::istreambuf_iterator<char>(std::cin)), std::istreambuf_iterator<char>());
+      for (const auto& v : validate_dependencies(parse_program(text))) std::cout << v << "\n";
+      return 0;
+    }
+  } catch (const std::exception& e) {
+    std::cout << "error: " << e.what() << "\n";
+    return 1;
+  }
+  std::cerr << "bad arguments\n";
+  return 2;
+}

@@ -76,6 +76,17 @@ SIGNATURES = {
     "vp_input_backward": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_void_p, c_int64, c_int64,
                                   POINTER(vp_shard_t), c_void_p, c_int64, c_int]),
     "vp_allreduce_sum": (c_int, [c_void_p, c_void_p, c_int64, c_int]),
+    "vp_program_parse": (c_int, [c_char_p, POINTER(c_void_p)]),
+    "vp_program_destroy": (c_int, [c_void_p]),
+    "vp_program_info": (c_int, [c_void_p, POINTER(c_int), POINTER(c_int), POINTER(c_int)]),
+    "vp_program_validate": (c_int, [c_void_p, c_char_p, c_int64, POINTER(c_int)]),
+    "vp_program_run": (c_int, [c_void_p, c_void_p, POINTER(vp_batch_t), POINTER(vp_shard_t), c_int,
+                               POINTER(c_void_p), POINTER(vp_stats_t), POINTER(c_void_p), POINTER(c_void_p), c_int64,
+                               POINTER(c_void_p), c_int64]),
+    "vp_ctx_capture_begin": (c_int, [c_void_p]),
+    "vp_ctx_capture_end": (c_int, [c_void_p, POINTER(c_void_p)]),
+    "vp_graph_launch": (c_int, [c_void_p, c_void_p]),
+    "vp_graph_destroy": (c_int, [c_void_p]),
 }
 
 

@@ -86,13 +86,12 @@ inline void prepare_store(EpiLogitStats::Params& ep, int M, int N) {
     ep.map = make_store_map(ep.P, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, uint64_t(N), uint64_t(M), uint64_t(ep.ldp));
 }
 
-// Split-K state owned by the caller (one per stream: flags are reused across
-// launches with a monotonically increasing base, so two GEMMs sharing one
-// SplitCfg must not run concurrently).  flags: >= 2 * max_tiles ints, zeroed once.
+// Split-K state owned by the caller (one per stream: the flags are reset by
+// each launch, so two GEMMs sharing one SplitCfg must not run concurrently).
+// flags: >= 2 * max_tiles ints.
 struct SplitCfg {
   int* flags = nullptr;
   int max_tiles = 0;
-  int base = 0;
   int force = 0;  // > 0: use exactly this many splits (tests); 0: choose by wave quantisation
 };
 
@@ -193,8 +192,11 @@ inline void launch_gemm_t(const Operand& A, const Operand& B, int M, int N, int 
     if (S > 1 && g.num_kb >= S) {
       g.splits = S;
       g.split_flags = split->flags;
-      g.flag_base = split->base;
-      split->base += S;
+      g.flag_base = 0;
+      // flags restart at 0 for every launch (a memset node in a captured CUDA
+      // graph, so replays never see a previous launch's flags)
+      cudaError_t me = cudaMemsetAsync(split->flags, 0, size_t(2 * tiles) * sizeof(int), st);
+      if (me != cudaSuccess) throw std::runtime_error(std::string("split flags memset: ") + cudaGetErrorString(me));
       clusters = tiles * S < cap ? tiles * S : cap;
     }
   }

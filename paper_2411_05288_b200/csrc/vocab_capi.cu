@@ -13,6 +13,7 @@
 #include "../../include/vpipe_b200.h"
 #include "gemm_host.cuh"
 #include "vocab_kernels.cuh"
+#include "vocab_program.h"
 
 namespace {
 
@@ -687,7 +688,169 @@ void naive(vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* shards, const vp_
   }
 }
 
+// -----------------------------------------------------------------------------
+// Vocabulary-pass executor: runs the S / C0 / C1 / T / C2
+// passes of a reference DeviceProgram (P/include/vpipe/schedule.hpp:95-100) in
+// program order on the GPU.  Transformer passes (F, B, IF, IB) belong to the
+// caller and are skipped.  The dependency contract C0 -> S -> C1 -> T [-> C2]
+// (P/src/schedule.cpp:339-366) is checked up front (validate_vocab); program
+// order then IS a valid stream order, so S and T run on the compute stream in
+// list order, and the heavy exchange of each barrier (the dX / loss
+// all-reduce of C1 for Algorithm 2, of C2 for Algorithm 1) is forked onto the
+// high-priority comm stream, where it overlaps the passes that follow ("T
+// arbitrarily delayable", R/PAPER.md:243, :329).  dW of every microbatch
+// accumulates into the shard's grad_w.
+//   NCCL group (nranks == p): this rank executes device `rank`'s list.
+//   Local: every device's list is executed on this GPU with one shard per
+//   device, merged at the collectives (the reference's in-process devices).
+void run_program(vp_ctx_s* c, const vp::Program& prog, const vp_batch_t* batches, const vp_shard_t* shards, int nsh,
+                 const vp_state_t* states, vp_stats_t* stats, float* const* loss, float* const* gx, int64_t ldgx,
+                 float* const* gw, int64_t ldgw) {
+  require(prog.vocab, "vp_program_run: the program's method has no vocabulary passes");
+  const int p = int(prog.p), n = int(prog.n);
+  const bool dist = c->distributed();
+  if (dist)
+    require(c->nranks == p && nsh == 1, "vp_program_run: an NCCL group runs one program device per rank (nranks == p)");
+  else
+    require(nsh == p, "vp_program_run: a local run executes every program device (one shard per device)");
+  require(nsh <= vp::kMaxLocalShards, "vp_program_run: too many local shards");
+  require(batches && shards && states && stats && loss && gx && gw, "vp_program_run: null argument");
+  {
+    const auto v = vp::validate_vocab(prog);
+    if (!v.empty()) throw std::invalid_argument("vp_program_run: program violates its dependencies: " + v.front());
+  }
+  // every device must issue the same collective sequence (NCCL call order;
+  // the local merge point)
+  std::vector<std::pair<int, int>> seq0;
+  for (int d = 0; d < p; ++d) {
+    std::vector<std::pair<int, int>> seq;
+    for (const auto& ps : prog.order[size_t(d)])
+      if (vp::is_collective(ps.kind)) seq.emplace_back(int(ps.kind), ps.microbatch);
+    if (d == 0) seq0 = seq;
+    else require(seq == seq0, "vp_program_run: devices disagree on the order of their collectives");
+  }
+  for (int i = 0; i < n; ++i) check_batch(&batches[i]);
+  const bool alg2 = prog.barriers == 1;
+  auto st = [&](int ls, int i) { return states[size_t(ls) * size_t(n) + size_t(i)]; };
+  for (int ls = 0; ls < nsh; ++ls) {
+    check_shard(&shards[ls], batches[0].h);
+    require(gw[ls] != nullptr && ldgw >= batches[0].h, "vp_program_run: bad grad_w");
+    const int64_t rows = shards[ls].row_end - shards[ls].row_begin;
+    VP_CUDA(cudaMemsetAsync(gw[ls], 0, size_t(rows * ldgw) * sizeof(float), c->stream));
+    for (int i = 0; i < n; ++i) check_state(st(ls, i), &batches[i], &shards[ls]);
+  }
+  const bool overlap = dist && c->overlap_c1 && c->comm_stream != nullptr;
+  const bool acc0 = c->accumulate_dw;
+  const int sms0 = c->gemm_sms;
+  c->accumulate_dw = true;
+  if (overlap) c->gemm_sms = std::max(2, (c->gemm_sms - c->comm_sms) / 2 * 2);
+  auto restore = [&] {
+    c->accumulate_dw = acc0;
+    c->gemm_sms = sms0;
+  };
+  try {
+    std::vector<int> devs;
+    if (dist) devs.push_back(c->rank);
+    else
+      for (int d = 0; d < p; ++d) devs.push_back(d);
+    std::vector<size_t> pos(devs.size(), 0);
+    auto exec_local = [&](int d, const vp::PPass& ps) {  // S / T of device d
+      const int ls = dist ? 0 : d, i = ps.microbatch;
+      vp_state_s* s_ = st(ls, i);
+      if (ps.kind == vp::PKind::S) {
+        if (alg2) alg2_S(c, &batches[i], &shards[ls], s_);
+        else pass_S_common(c, &batches[i], &shards[ls], s_);
+      } else if (alg2) {
+        alg2_T(c, s_, stats[i], &batches[i], &shards[ls], gw[ls], ldgw);
+      } else {
+        // Algorithm 1: dX partial (local: the state's buffer; NCCL: grad_x, reduced by C2)
+        alg1_T(c, s_, stats[i], &batches[i], &shards[ls], dist ? gx[i] : s_->A, dist ? ldgx : batches[i].h, gw[ls],
+               ldgw);
+      }
+    };
+    auto exec_collective = [&](vp::PKind k, int i) {
+      std::vector<vp_state_t> sts(static_cast<size_t>(nsh));
+      for (int ls = 0; ls < nsh; ++ls) sts[size_t(ls)] = st(ls, i);
+      const vp_batch_t* b = &batches[i];
+      const int64_t T = b->n_tok, h = b->h;
+      if (k == vp::PKind::C0) {
+        // broadcast of the last stage's output (X_i) to every device
+        if (dist)
+          VP_NCCL(ncclBroadcast(b->X, const_cast<void*>(b->X), size_t(T * b->ldx), ncclBfloat16, p - 1, c->comm,
+                                c->stream));
+      } else if (k == vp::PKind::C1) {
+        if (alg2) {
+          alg2_C1(c, sts.data(), shards, nsh, b, 1.0, stats[i], gx[i], ldgx, /*reduce=*/!overlap);
+          loss_of(c, sts.data(), shards, nsh, stats[i], b, loss[i], /*reduce=*/!overlap);
+          if (overlap) {
+            require(ldgx == h, "vp_program_run: grad_x must be dense (ldgx == h) for the all-reduce");
+            fork_allreduces(c, gx[i], T * h, loss[i], T);
+          }
+        } else {
+          merge_stats(c, sts.data(), nsh, 1.0, stats[i]);
+          loss_of(c, sts.data(), shards, nsh, stats[i], b, loss[i]);
+        }
+      } else {  // C2 (Algorithm 1): grad_x = sum of the dX partials
+        if (dist) {
+          require(ldgx == h, "vp_program_run: grad_x must be dense (ldgx == h) for the all-reduce");
+          if (overlap) {
+            VP_CUDA(cudaEventRecord(c->ev_ready, c->stream));
+            VP_CUDA(cudaStreamWaitEvent(c->comm_stream, c->ev_ready, 0));
+            VP_NCCL(ncclAllReduce(gx[i], gx[i], size_t(T * h), ncclFloat32, ncclSum, c->comm, c->comm_stream));
+            VP_CUDA(cudaEventRecord(c->ev_done, c->comm_stream));
+            c->reduce_pending = true;
+          } else {
+            VP_NCCL(ncclAllReduce(gx[i], gx[i], size_t(T * h), ncclFloat32, ncclSum, c->comm, c->stream));
+          }
+        } else {
+          std::vector<float*> parts(static_cast<size_t>(nsh));
+          for (int ls = 0; ls < nsh; ++ls) parts[size_t(ls)] = st(ls, i)->A;
+          reduce_partials(c, parts.data(), nsh, T, h, h, gx[i], ldgx);
+        }
+      }
+    };
+    for (;;) {
+      // run every executing device up to its next collective
+      bool done = true;
+      for (size_t e = 0; e < devs.size(); ++e) {
+        const auto& list = prog.order[size_t(devs[e])];
+        while (pos[e] < list.size()) {
+          const vp::PPass& ps = list[pos[e]];
+          if (!vp::is_vocab_pass(ps.kind)) {
+            ++pos[e];
+            continue;
+          }
+          if (vp::is_collective(ps.kind)) break;
+          exec_local(devs[e], ps);
+          ++pos[e];
+        }
+        if (pos[e] < list.size()) done = false;
+      }
+      if (done) break;
+      // all executing devices now stand at the same collective (sequences agree)
+      const vp::PPass& cp = prog.order[size_t(devs[0])][pos[0]];
+      exec_collective(cp.kind, cp.microbatch);
+      for (size_t e = 0; e < devs.size(); ++e) ++pos[e];
+    }
+  } catch (...) {
+    restore();
+    join_allreduces(c);
+    throw;
+  }
+  restore();
+  join_allreduces(c);
+}
+
 }  // namespace
+
+struct vp_program_s {
+  vp::Program prog;
+};
+
+struct vp_graph_s {
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+};
 
 // =============================================================================
 extern "C" {
@@ -1190,5 +1353,112 @@ int vp_allreduce_sum(vp_ctx_t c, void* buf, int64_t count, int dtype) {
                           c->stream));
   });
 }
+
+int vp_program_parse(const char* text, vp_program_t* out) {
+  return api([&] {
+    require(text != nullptr && out != nullptr, "vp_program_parse: null argument");
+    auto* pr = new vp_program_s();
+    try {
+      pr->prog = vp::parse_program(text);
+    } catch (const vp::ProgramParseError& e) {
+      delete pr;
+      throw std::invalid_argument(e.what());
+    } catch (...) {
+      delete pr;
+      throw;
+    }
+    *out = pr;
+  });
+}
+
+int vp_program_destroy(vp_program_t pr) {
+  delete pr;
+  return VP_OK;
+}
+
+int vp_program_info(vp_program_t pr, int* barriers, int* p, int* n) {
+  return api([&] {
+    require(pr != nullptr, "vp_program_info: null program");
+    if (barriers) *barriers = pr->prog.vocab ? pr->prog.barriers : 0;
+    if (p) *p = int(pr->prog.p);
+    if (n) *n = int(pr->prog.n);
+  });
+}
+
+int vp_program_validate(vp_program_t pr, char* buf, int64_t buflen, int* count) {
+  return api([&] {
+    require(pr != nullptr, "vp_program_validate: null program");
+    const auto v = vp::validate_vocab(pr->prog);
+    std::string all;
+    for (const auto& line : v) all += line + "\n";
+    if (count) *count = int(v.size());
+    if (buf && buflen > 0) {
+      const size_t k = std::min(all.size(), size_t(buflen - 1));
+      std::memcpy(buf, all.data(), k);
+      buf[k] = '\0';
+    }
+  });
+}
+
+int vp_program_run(vp_ctx_t c, vp_program_t pr, const vp_batch_t* batches, const vp_shard_t* shards, int n_shards,
+                   const vp_state_t* states, vp_stats_t* stats, float* const* loss, float* const* grad_x, int64_t ldgx,
+                   float* const* grad_w, int64_t ldgw) {
+  return api([&] {
+    require(c != nullptr && pr != nullptr, "vp_program_run: null argument");
+    c->activate();
+    run_program(c, pr->prog, batches, shards, n_shards, states, stats, loss, grad_x, ldgx, grad_w, ldgw);
+  });
+}
+
+int vp_ctx_capture_begin(vp_ctx_t c) {
+  return api([&] {
+    require(c != nullptr, "vp_ctx_capture_begin: null context");
+    require(c->stream != nullptr, "vp_ctx_capture_begin: the legacy default stream cannot be captured");
+    require(!c->timing, "vp_ctx_capture_begin: disable GEMM timing before capturing");
+    c->activate();
+    VP_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+  });
+}
+
+int vp_ctx_capture_end(vp_ctx_t c, vp_graph_t* out) {
+  return api([&] {
+    require(c != nullptr && out != nullptr, "vp_ctx_capture_end: null argument");
+    c->activate();
+    auto* g = new vp_graph_s();
+    cudaError_t e = cudaStreamEndCapture(c->stream, &g->graph);
+    if (e != cudaSuccess) {
+      delete g;
+      (void)cudaGetLastError();
+      throw CudaError(std::string("cudaStreamEndCapture: ") + cudaGetErrorString(e) +
+                      " (a workspace buffer grew or the stream was synchronised while capturing:"
+                      " run the same call once eagerly first)");
+    }
+    e = cudaGraphInstantiate(&g->exec, g->graph, 0);
+    if (e != cudaSuccess) {
+      cudaGraphDestroy(g->graph);
+      delete g;
+      throw CudaError(std::string("cudaGraphInstantiate: ") + cudaGetErrorString(e));
+    }
+    *out = g;
+  });
+}
+
+int vp_graph_launch(vp_graph_t g, vp_ctx_t c) {
+  return api([&] {
+    require(g != nullptr && c != nullptr, "vp_graph_launch: null argument");
+    c->activate();
+    VP_CUDA(cudaGraphLaunch(g->exec, c->stream));
+  });
+}
+
+int vp_graph_destroy(vp_graph_t g) {
+  if (g) {
+    if (g->exec) cudaGraphExecDestroy(g->exec);
+    if (g->graph) cudaGraphDestroy(g->graph);
+    delete g;
+  }
+  return VP_OK;
+}
+
 
 }  // extern "C"

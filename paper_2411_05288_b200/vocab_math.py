@@ -466,6 +466,111 @@ def allreduce_sum(ctx: Context, t: torch.Tensor) -> torch.Tensor:
     return t
 
 
+# ---------------------------------------------------------------------------
+# Pipeline integration: executing a reference DeviceProgram's vocabulary passes
+class Program:
+    """A reference DeviceProgram (schedule.hpp:95-100) in serialize_program's text
+    form (schedule.cpp:512-529), parsed by the library (vp_program_parse)."""
+
+    def __init__(self, text: str):
+        self.lib = _lib.load()
+        h = ctypes.c_void_p()
+        check(self.lib.vp_program_parse(text.encode(), ctypes.byref(h)))
+        self.handle = h
+        b, p, n = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        check(self.lib.vp_program_info(h, ctypes.byref(b), ctypes.byref(p), ctypes.byref(n)))
+        self.barriers, self.p, self.n = b.value, p.value, n.value
+
+    def validate(self) -> List[str]:
+        """validate_dependencies (schedule.cpp:390-447) on the vocabulary passes."""
+        buf = ctypes.create_string_buffer(1 << 16)
+        cnt = ctypes.c_int()
+        check(self.lib.vp_program_validate(self.handle, buf, len(buf), ctypes.byref(cnt)))
+        return [ln for ln in buf.value.decode().split("\n") if ln]
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            self.lib.vp_program_destroy(self.handle)
+        self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+@dataclass
+class ProgramResult:
+    loss: List[torch.Tensor]          # per microbatch
+    grad_x: List[torch.Tensor]        # per microbatch
+    stats: List[GlobalStats]          # per microbatch
+    grad_w: List[torch.Tensor]        # per local shard, accumulated over the microbatches
+    states: List[List[ShardState]]    # [shard][microbatch]
+
+
+def run_program(ctx: Context, program: Program, batches: Sequence[TokenBatch], shards: Sequence[EmbeddingShard],
+                states=None, outputs: Optional[ProgramResult] = None) -> ProgramResult:
+    """Executes the program's vocabulary passes (vp_program_run): locally every
+    device with one shard each, or this rank's device in an NCCL group."""
+    n = program.n
+    if len(batches) != n:
+        raise ValueError("run_program: one TokenBatch per microbatch")
+    dev = _dev(ctx)
+    if outputs is None:
+        T, h = batches[0].X.shape
+        states = states or [[ShardState(ctx, b.X.shape[0], b.X.shape[1], s.rows()) for b in batches] for s in shards]
+        outputs = ProgramResult(
+            [torch.empty(b.X.shape[0], dtype=torch.float32, device=dev) for b in batches],
+            [torch.empty(b.X.shape[0], b.X.shape[1], dtype=torch.float32, device=dev) for b in batches],
+            [GlobalStats.empty(b.X.shape[0], dev) for b in batches],
+            [torch.empty(s.rows(), h, dtype=torch.float32, device=dev) for s in shards], states)
+    r = outputs
+    bs = (vp_batch_t * n)(*[b.c() for b in batches])
+    st = (ctypes.c_void_p * (len(shards) * n))(*[x.handle.value for row in r.states for x in row])
+    stats = (vp_stats_t * n)(*[x.c() for x in r.stats])
+    loss = (ctypes.c_void_p * n)(*[t.data_ptr() for t in r.loss])
+    gx = (ctypes.c_void_p * n)(*[t.data_ptr() for t in r.grad_x])
+    gw = (ctypes.c_void_p * len(shards))(*[t.data_ptr() for t in r.grad_w])
+    check(ctx.lib.vp_program_run(ctx.handle, program.handle, bs, _shards_arr(shards), len(shards), st, stats, loss,
+                                 gx, r.grad_x[0].stride(0), gw, r.grad_w[0].stride(0)))
+    return r
+
+
+class Graph:
+    """CUDA graph of the context's work (vp_ctx_capture_begin/_end), replayed
+    with one launch.  Run the captured calls once eagerly first (workspace)."""
+
+    def __init__(self, ctx: Context, handle: ctypes.c_void_p):
+        self.ctx, self.handle = ctx, handle
+
+    def launch(self) -> None:
+        check(self.ctx.lib.vp_graph_launch(self.handle, self.ctx.handle))
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            self.ctx.lib.vp_graph_destroy(self.handle)
+        self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def capture(ctx: Context, fn) -> Graph:
+    """Captures everything fn() issues on ctx into a Graph."""
+    check(ctx.lib.vp_ctx_capture_begin(ctx.handle))
+    try:
+        fn()
+    finally:
+        h = ctypes.c_void_p()
+        rc = ctx.lib.vp_ctx_capture_end(ctx.handle, ctypes.byref(h))
+    check(rc)
+    return Graph(ctx, h)
+
+
 def pad_vocab_size(V: int, p: int) -> int:
     """cost_model.cpp:49-55."""
     if V < 1 or p < 1:
