@@ -102,7 +102,13 @@ def test_program_through_a_one_rank_nccl_group(ctx):
 def test_cuda_graph_replay_equals_eager(ctx):
     # capture run_alg2 and a whole program; replays on fresh inputs (copied
     # into the captured buffers) reproduce eager results bit for bit
-    gctx = vm.Context(0)
+    stream = torch.cuda.Stream()  # the legacy default stream cannot be captured
+    with torch.cuda.stream(stream):
+        _graph_replays(ctx)
+
+
+def _graph_replays(ctx):
+    gctx = vm.Context(0)  # runs on the current (side) stream
     X, W, g = oracle.random_instance(300, 128, 1500, 4)
     _, _, batch, Wd = device_case(X, W, g)
     shards = vm.shard_weights(Wd, 2)
