@@ -96,6 +96,9 @@ int vp_ctx_reserve(vp_ctx_t ctx, int64_t n_tok, int64_t h, int p);
  * on a high-priority comm stream; default 1), "comm_sms" (SMs left to NCCL
  * during the overlap and NCCL's maxCTAs; set before vp_ctx_comm_init),
  * "epi_wait" (GEMM epilogue wait: 0 try_wait loop, 1 nanosleep backoff),
+ * "lockstep_logits" / "lockstep_dx" / "lockstep_dw" (wave lockstep of the
+ * persistent GEMM's clusters every N k-blocks so co-scheduled tiles share
+ * operand bands in L2; 0 = off; defaults 0 / 8 / 8),
  * "splits_dx" (split-K of the dX / A GEMM, whose K = V_k leaves few tile
  * waves: 0 = chosen from the wave quantisation (default), 1 = off, 2..4 =
  * forced; partial sums are added in split order, so results are deterministic),

@@ -95,6 +95,14 @@ struct SplitCfg {
   int force = 0;  // > 0: use exactly this many splits (tests); 0: choose by wave quantisation
 };
 
+// Wave-lockstep state owned by the caller (per stream, like SplitCfg):
+// counters for up to `capacity` (wave, epoch) pairs, reset by each launch.
+struct LockCfg {
+  int* counters = nullptr;
+  int64_t capacity = 0;
+  int epoch = 0;  // k-blocks per epoch; 0 = off
+};
+
 // Splits for a persistent GEMM of `tiles` tiles on `clusters` clusters and
 // num_kb k-blocks: the smallest S in 1..4 whose wave efficiency
 // tiles*S / (clusters * ceil(tiles*S / clusters)) is within 1% of the best,
@@ -133,7 +141,7 @@ inline int g_epi_wait = 1;                          // GemmGeom::epi_wait for su
 template <int CG, bool A_MN, bool B_MN, class Epi, int MC = 1, int NH = 1>
 inline void launch_gemm_t(const Operand& A, const Operand& B, int M, int N, int K, int raster,
                           const typename Epi::Params& ep, int num_sms, cudaStream_t st, int pol_a = -1,
-                          int pol_b = -1, SplitCfg* split = nullptr) {
+                          int pol_b = -1, SplitCfg* split = nullptr, const LockCfg* lock = nullptr) {
   using C = GemmCfg<CG, NH>;
   const CUtensorMap ta = A_MN ? make_tmap_bf16(A.ptr, uint64_t(M), uint64_t(K), uint64_t(A.ld), 64, 64)
                               : make_tmap_bf16(A.ptr, uint64_t(K), uint64_t(M), uint64_t(A.ld), 64, C::BM_CTA);
@@ -211,6 +219,19 @@ inline void launch_gemm_t(const Operand& A, const Operand& B, int M, int N, int 
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
+  if (lock != nullptr && lock->counters != nullptr && lock->epoch > 0) {
+    const int units = tiles * g.splits;
+    const int waves = (units + clusters - 1) / clusters;
+    const int max_nkb = (g.num_kb + g.splits - 1) / g.splits + 1;
+    const int stride = (max_nkb + lock->epoch - 1) / lock->epoch + 1;
+    if (waves > 1 && int64_t(waves) * stride <= lock->capacity) {
+      g.lockstep = lock->counters;
+      g.lock_epoch = lock->epoch;
+      g.lock_stride = stride;
+      cudaError_t me = cudaMemsetAsync(lock->counters, 0, size_t(waves) * size_t(stride) * sizeof(int), st);
+      if (me != cudaSuccess) throw std::runtime_error(std::string("lockstep memset: ") + cudaGetErrorString(me));
+    }
+  }
   typename Epi::Params epc = ep;
   prepare_store(epc, M, N);
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta, tb, g, epc);
@@ -221,11 +242,12 @@ inline void launch_gemm_t(const Operand& A, const Operand& B, int M, int N, int 
 template <class Epi>
 inline void launch_gemm(int cg, const Operand& A, const Operand& B, int M, int N, int K, int raster,
                         const typename Epi::Params& ep, int num_sms, cudaStream_t st, int pol_a = -1,
-                        int pol_b = -1, int mc = 1, int nh = 1, SplitCfg* split = nullptr) {
-#define VP_GEMM_CASE(CGV, AM, BM_, MCV, NHV)                                                                  \
-  if (cg == CGV && A.mn_major == AM && B.mn_major == BM_ && mc == MCV && nh == NHV) {                         \
-    launch_gemm_t<CGV, AM, BM_, Epi, MCV, NHV>(A, B, M, N, K, raster, ep, num_sms, st, pol_a, pol_b, split);  \
-    return;                                                                                                   \
+                        int pol_b = -1, int mc = 1, int nh = 1, SplitCfg* split = nullptr,
+                        const LockCfg* lock = nullptr) {
+#define VP_GEMM_CASE(CGV, AM, BM_, MCV, NHV)                                                                        \
+  if (cg == CGV && A.mn_major == AM && B.mn_major == BM_ && mc == MCV && nh == NHV) {                               \
+    launch_gemm_t<CGV, AM, BM_, Epi, MCV, NHV>(A, B, M, N, K, raster, ep, num_sms, st, pol_a, pol_b, split, lock);  \
+    return;                                                                                                         \
   }
   VP_GEMM_CASE(2, false, false, 1, 1)
   VP_GEMM_CASE(2, false, true, 1, 1)

@@ -109,6 +109,13 @@ struct vp_ctx_s {
   // splits_dx option: 0 = by wave quantisation, 1 = off, 2..4 = forced
   vp::SplitCfg split;
   int splits_dx = 0;
+  // wave lockstep per GEMM [logits, dX, dW]: epoch length in k-blocks (0 = off)
+  vp::LockCfg lock;
+  int lock_epoch[3] = {0, 8, 8};
+  const vp::LockCfg* lock_for(int i) {
+    lock.epoch = lock_epoch[i];
+    return lock.epoch > 0 ? &lock : nullptr;
+  }
   // tile shapes actually launched: 512-wide tiles and multicast need CTA pairs
   int eff_nh(int i) const { return cg == 2 ? nh[i] : 1; }
   int eff_mc(int i) const { return cg == 2 && eff_nh(i) == 1 ? mc : 1; }
@@ -240,7 +247,7 @@ void gemm_logits(vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* s, vp_state
   timed_gemm(c, 0, [&] {
     vp::launch_gemm<vp::EpiLogitStats>(c->cg, {b->X, b->ldx, false}, {s->W, s->ldw, false}, int(b->n_tok),
                                        int(st->rows), int(b->h), c->raster[0], ep, c->gemm_sms, c->stream,
-                                       c->pol[0], c->pol[0], c->eff_mc(0), c->eff_nh(0));
+                                       c->pol[0], c->pol[0], c->eff_mc(0), c->eff_nh(0), nullptr, c->lock_for(0));
   });
   ++c->launches;
 }
@@ -263,7 +270,8 @@ void gemm_dx(vp_ctx_s* c, vp_state_s* st, const vp_shard_t* s, float* out, int64
   timed_gemm(c, 2, [&] {
     vp::launch_gemm<vp::EpiStoreF32>(c->cg, {st->P, st->ldp, false}, {s->W, s->ldw, true}, int(st->n_tok),
                                      int(st->h), int(st->rows), c->raster[1], ep, c->gemm_sms, c->stream, c->pol[1],
-                                     c->pol[1], c->eff_mc(1), c->eff_nh(1), c->splits_dx == 1 ? nullptr : &c->split);
+                                     c->pol[1], c->eff_mc(1), c->eff_nh(1), c->splits_dx == 1 ? nullptr : &c->split,
+                                     c->lock_for(1));
   });
   ++c->launches;
 }
@@ -275,7 +283,7 @@ void gemm_dw(vp_ctx_s* c, vp_state_s* st, const void* Xop, int64_t ldx, float* o
   timed_gemm(c, 3, [&] {
     vp::launch_gemm<vp::EpiStoreF32>(c->cg, {st->P, st->ldp, true}, {Xop, ldx, true}, int(st->rows), int(st->h),
                                      int(st->n_tok), raster, ep, c->gemm_sms, c->stream, c->pol[2], c->pol[2],
-                                     c->eff_mc(2), c->eff_nh(2));
+                                     c->eff_mc(2), c->eff_nh(2), nullptr, c->lock_for(2));
   });
   ++c->launches;
 }
@@ -877,6 +885,8 @@ int vp_ctx_create(int device, vp_ctx_t* out) {
       c->stream = c->own_stream;
       VP_CUDA(cudaMalloc(&c->d_err, sizeof(int)));
       VP_CUDA(cudaMemset(c->d_err, 0, sizeof(int)));
+      c->lock.capacity = int64_t(1) << 20;
+      VP_CUDA(cudaMalloc(&c->lock.counters, size_t(c->lock.capacity) * sizeof(int)));
       c->split.max_tiles = 1 << 14;
       VP_CUDA(cudaMalloc(&c->split.flags, size_t(2 * c->split.max_tiles) * sizeof(int)));
       VP_CUDA(cudaMemset(c->split.flags, 0, size_t(2 * c->split.max_tiles) * sizeof(int)));
@@ -902,6 +912,7 @@ int vp_ctx_destroy(vp_ctx_t c) {
       b->release();
     if (c->d_err) cudaFree(c->d_err);
     if (c->split.flags) cudaFree(c->split.flags);
+    if (c->lock.counters) cudaFree(c->lock.counters);
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
     delete c;
   });
@@ -976,6 +987,9 @@ int vp_ctx_set_option(vp_ctx_t c, const char* key, int64_t value) {
       require(value >= 1 && value <= 64, "vp_ctx_set_option: comm_sms must be 1..64");
       require(c->comm == nullptr, "vp_ctx_set_option: comm_sms must be set before vp_ctx_comm_init");
       c->comm_sms = int(value);
+    } else if (k == "lockstep_logits" || k == "lockstep_dx" || k == "lockstep_dw") {
+      require(value >= 0 && value <= 4096, "vp_ctx_set_option: lockstep epoch must be in 0..4096 k-blocks");
+      c->lock_epoch[k == "lockstep_logits" ? 0 : k == "lockstep_dx" ? 1 : 2] = int(value);
     } else if (k == "splits_dx") {
       require(value >= 0 && value <= 4, "vp_ctx_set_option: splits_dx must be in 0..4");
       c->splits_dx = int(value);

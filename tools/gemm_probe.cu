@@ -83,6 +83,11 @@ int main(int argc, char** argv) {
   CK(cudaMemset(scfg.flags, 0, 2 * 16384 * sizeof(int)));
   scfg.max_tiles = 16384;
   scfg.force = split_dx > 0 ? split_dx : 0;
+  // VP_LOCKSTEP: wave-lockstep epoch (k-blocks, 0 = off)
+  vp::LockCfg lcfg;
+  lcfg.epoch = getenv("VP_LOCKSTEP") ? atoi(getenv("VP_LOCKSTEP")) : 0;
+  lcfg.capacity = int64_t(1) << 20;
+  CK(cudaMalloc(&lcfg.counters, size_t(lcfg.capacity) * sizeof(int)));
   auto run = [&] {
     if (kind == "k1") {
       vp::EpiLogitStats::Params ep{P,   V,   tm,  ts,  T,   nullptr, 0,   V,   yt,  tq,
@@ -91,15 +96,15 @@ int main(int argc, char** argv) {
       CK(cudaMemsetAsync(bad, 0, T * 4));
       CK(cudaMemsetAsync(cnt, 0, 8));
       vp::launch_gemm<vp::EpiLogitStats>(2, {X, h, false}, {W, h, false}, int(T), int(V), int(h), raster, ep, nsm, 0,
-                                         pa, pb, mc, nh);
+                                         pa, pb, mc, nh, nullptr, &lcfg);
     } else if (kind == "dx") {
       vp::EpiStoreF32::Params ep{out, h, nullptr, 0, nullptr};
       vp::launch_gemm<vp::EpiStoreF32>(2, {P, V, false}, {W, h, true}, int(T), int(h), int(V), raster, ep, nsm, 0, pa,
-                                       pb, mc, nh, split_dx ? &scfg : nullptr);
+                                       pb, mc, nh, split_dx ? &scfg : nullptr, &lcfg);
     } else if (kind == "dw") {
       vp::EpiStoreF32::Params ep{out, h, nullptr, 0, nullptr};
       vp::launch_gemm<vp::EpiStoreF32>(2, {P, V, true}, {X, h, true}, int(V), int(h), int(T), raster, ep, nsm, 0, pa,
-                                       pb, mc, nh);
+                                       pb, mc, nh, nullptr, &lcfg);
     } else {  // sq8192: plain 8192^3 K-major GEMM (W as an 8192 x 8192 slice), fp32 out
       vp::EpiStoreF32::Params ep{out, 8192, nullptr, 0, nullptr};
       vp::launch_gemm<vp::EpiStoreF32>(2, {W, 8192, false}, {W + int64_t(8192) * 8192, 8192, false}, 8192, 8192,
