@@ -136,7 +136,8 @@ struct Operand {
 };
 
 inline unsigned long long* g_gemm_prof = nullptr;  // set by probes: {clk0, t0, clk1, t1} of CTA 0
-inline int g_epi_wait = 1;                          // GemmGeom::epi_wait for subsequent launches
+inline int g_epi_wait = 1;
+inline int g_store_evict_first = 0;  // GemmGeom::store_evict_first for subsequent launches                          // GemmGeom::epi_wait for subsequent launches
 
 template <int CG, bool A_MN, bool B_MN, class Epi, int MC = 1, int NH = 1>
 inline void launch_gemm_t(const Operand& A, const Operand& B, int M, int N, int K, int raster,
@@ -160,6 +161,7 @@ inline void launch_gemm_t(const Operand& A, const Operand& B, int M, int N, int 
   g.pol_a = pol_a;
   g.pol_b = pol_b;
   g.prof = g_gemm_prof;
+  g.store_evict_first = g_store_evict_first;
   g.epi_wait = g_epi_wait;
   auto kern = gemm_sm100_kernel<CG, A_MN, B_MN, Epi, MC, NH>;
   static bool attr_done = false;

@@ -71,6 +71,7 @@ struct GemmGeom {
   int* lockstep = nullptr;
   int lock_epoch = 8;
   int lock_stride = 0;
+  int store_evict_first = 0;  // epilogue TMA stores with an L2 evict-first hint
 };
 
 __device__ __forceinline__ uint64_t make_policy(int p, bool dflt_first) {
@@ -155,8 +156,13 @@ struct Stager {
     const uint32_t r = threadIdx.x & 31;
     return box + r * 64u + ((uint32_t(q) ^ ((r >> 1) & 3u)) << 4);
   }
-  __device__ static __forceinline__ void put(const CUtensorMap* m, uint32_t box, int c0, int c1, bool add) {
+  // stores of streamed outputs (P, dW) carry an L2 evict-first hint so they
+  // do not displace the operand band the co-scheduled tiles re-read (X in K1)
+  uint64_t pol = 0;
+  bool hint = false;
+  __device__ __forceinline__ void put(const CUtensorMap* m, uint32_t box, int c0, int c1, bool add) const {
     if (add) ptx::tma_reduce_add_2d(m, box, c0, c1);
+    else if (hint) ptx::tma_store_2d_hint(m, box, c0, c1, pol);
     else ptx::tma_store_2d(m, box, c0, c1);
   }
   // store one box / two boxes written since the last flush (one bulk group)
@@ -508,6 +514,10 @@ __global__ void __launch_bounds__(384, 1)
     // 128 of the 256 accumulator columns of each N half.
     const int ew = warp - 4, quad = ew & 3, cgp = ew >> 2;
     Stager sg(stg + uint32_t(ew) * uint32_t(C::STG_WARP));
+    if (g.store_evict_first) {
+      sg.hint = true;
+      sg.pol = ptx::policy_evict_first();
+    }
     sg.probe = VP_GEMM_PROBE && g.prof != nullptr && blockIdx.x == 0 && ew == 0;
     const bool probe = sg.probe;
     uint32_t tc = 0;
