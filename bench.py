@@ -69,26 +69,35 @@ def measured_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled DURING the timed region."""
-    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+    """nvidia-smi clocks / throttle reasons sampled DURING the timed region.
+
+    The sampler process starts at construction (before the warm-up, so it is
+    already producing samples when the timed region begins); `with sampler:`
+    marks the timed region, and only samples whose nvidia-smi timestamps fall
+    inside it are summarised."""
+    Q = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, gpu: int):
         self.gpu = gpu
-        self.proc = None
-
-    def __enter__(self):
+        self.t0 = self.t1 = None
+        self.lines = []
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(gpu), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.proc = None
+        time.sleep(0.5)  # nvidia-smi start-up
+
+    def __enter__(self):
+        self.t0 = time.time()
         return self
 
     def __exit__(self, *a):
-        self.lines = []
+        self.t1 = time.time()
+        time.sleep(0.12)  # let the sample that covers the region's end arrive
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -98,11 +107,25 @@ class ClockSampler:
                 out = ""
             self.lines = [ln for ln in out.splitlines() if ln.strip()]
 
+    def _in_region(self):
+        import datetime
+        keep, near = [], None
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            try:
+                ts = datetime.datetime.strptime(f[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+            except (ValueError, IndexError):
+                continue
+            if self.t0 - 0.05 <= ts <= self.t1 + 0.05:
+                keep.append(f[1:])
+            elif ts < self.t0:
+                near = f[1:]
+        return keep or ([near] if near else [])
+
     def summary(self):
         sm, smax, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in getattr(self, "lines", []):
-            f = [x.strip() for x in ln.split(",")]
+        for f in self._in_region():
             if len(f) < 7:
                 continue
             try:
@@ -249,13 +272,14 @@ def run_ours(args):
         return vpd.max_over_ranks(x, device="cuda")
 
     # ---- device-resident throughput (value) ----
+    clk = ClockSampler(local)
     for _ in range(args.warmup):
         step()
     barrier()
     ctx.gemm_timing(True)
     launches0 = ctx.launches
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
+    with clk:
         barrier()
         ev0.record(stream)
         for _ in range(args.steps):
