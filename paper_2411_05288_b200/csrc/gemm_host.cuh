@@ -52,14 +52,15 @@ inline CUtensorMap make_tmap_bf16(const void* ptr, uint64_t inner, uint64_t oute
 // 2-D tensor map of the epilogue's TMA stores: row-major [outer x inner]
 // elements of `esize` bytes, SWIZZLE_64B boxes of [32 rows x 64 B].
 inline CUtensorMap make_store_map(const void* ptr, CUtensorMapDataType dt, int esize, uint64_t inner,
-                                  uint64_t outer, uint64_t ld) {
+                                  uint64_t outer, uint64_t ld, int row_bytes = 64) {
   CUtensorMap m;
   const cuuint64_t dims[2] = {inner, outer};
   const cuuint64_t strides[1] = {ld * uint64_t(esize)};
-  const cuuint32_t box[2] = {cuuint32_t(64 / esize), 32};
+  const cuuint32_t box[2] = {cuuint32_t(row_bytes / esize), 32};
   const cuuint32_t estr[2] = {1, 1};
   CUresult r = get_encode_fn()(&m, dt, 2, const_cast<void*>(ptr), dims, strides, box, estr,
-                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                               CU_TENSOR_MAP_INTERLEAVE_NONE,
+                               row_bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
                                CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled (store) failed: " + std::to_string(int(r)));
   return m;
@@ -83,7 +84,8 @@ inline void prepare_store(EpiStoreF32::Params& ep, int M, int N) {
 inline void prepare_store(EpiLogitStats::Params& ep, int M, int N) {
   ep.use_tma = tma_store_ok(ep.P, ep.ldp, 2);
   if (ep.use_tma)
-    ep.map = make_store_map(ep.P, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, uint64_t(N), uint64_t(M), uint64_t(ep.ldp));
+    ep.map = make_store_map(ep.P, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, uint64_t(N), uint64_t(M), uint64_t(ep.ldp),
+                            VP_P_BOX128 ? 128 : 64);
 }
 
 // Split-K state owned by the caller (one per stream: the flags are reset by

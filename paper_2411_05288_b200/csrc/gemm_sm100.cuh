@@ -36,6 +36,9 @@
 #ifndef VP_EPI_MODE
 #define VP_EPI_MODE 0  // probes only: 1 = TMEM loads only, 2 = nothing, 3 = K1 math without stores, 4 = K1 stores without math
 #endif
+#ifndef VP_P_BOX128
+#define VP_P_BOX128 1  // K1 stores P in 32 x 128 B SWIZZLE_128B boxes (half the TMA row segments; 0: 64 B boxes)
+#endif
 #ifndef VP_K1_POLY
 #define VP_K1_POLY 0  // 1: half of the K1 epilogue's exponentials on the FMA pipe (ptx::ex2_poly)
 #endif
@@ -160,6 +163,10 @@ struct Stager {
   // do not displace the operand band the co-scheduled tiles re-read (X in K1)
   uint64_t pol = 0;
   bool hint = false;
+  __device__ static __forceinline__ void put_static(const Stager& sg, const CUtensorMap* m, uint32_t box, int c0,
+                                                    int c1) {
+    sg.put(m, box, c0, c1, false);
+  }
   __device__ __forceinline__ void put(const CUtensorMap* m, uint32_t box, int c0, int c1, bool add) const {
     if (add) ptx::tma_reduce_add_2d(m, box, c0, c1);
     else if (hint) ptx::tma_store_2d_hint(m, box, c0, c1, pol);
@@ -869,7 +876,9 @@ struct EpiLogitStats {
     uint64_t sp2[2] = {ptx::f2pack(0.f, 0.f), ptx::f2pack(0.f, 0.f)};
     float mp[2] = {mx, mx};
     const uint64_t l2e2 = ptx::f2pack(kLog2e, kLog2e), nref2 = ptx::f2pack(-refs, -refs);
+#if !VP_P_BOX128
     uint32_t box0 = 0;  // first box of the pair being filled (TMA path)
+#endif
     tmem_chunks(taddr, nch, [&](uint32_t (&r)[32], int c) {
       const int nv = nvalid - c * 32;
       uint32_t pk[16];
@@ -929,6 +938,29 @@ struct EpiLogitStats {
 #else
       if (p.use_tma) {
 #endif
+#if VP_P_BOX128
+        // one 64-column bf16 box (32 rows x 128 B, SWIZZLE_128B) per two chunks,
+        // the warp's whole 4 KB staging area, single-buffered
+        if ((c & 1) == 0) {
+          if ((threadIdx.x & 31) == 0) ptx::bulk_wait_read<0>();
+          __syncwarp();
+        }
+        {
+          const uint32_t r = threadIdx.x & 31, q0 = uint32_t(c & 1) * 4u;
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            ptx::st_shared_v4(sg.base + r * 128u + (((q0 + uint32_t(q)) ^ (r & 7u)) << 4), pk[4 * q], pk[4 * q + 1],
+                              pk[4 * q + 2], pk[4 * q + 3]);
+        }
+        if ((c & 1) || c + 1 == nch) {
+          ptx::fence_proxy_async_smem();
+          __syncwarp();
+          if ((threadIdx.x & 31) == 0) {
+            Stager::put_static(sg, &p.map, sg.base, col0 + (c & ~1) * 32, row0);
+            ptx::bulk_commit();
+          }
+        }
+#else
         // one 32-column bf16 box per chunk, flushed in pairs (one fence per
         // two chunks); columns past N are clipped by the TMA unit
         const uint32_t box = sg.next();
@@ -938,6 +970,7 @@ struct EpiLogitStats {
         if (c & 1) sg.flush2(&p.map, box0, col0 + (c - 1) * 32, row0, box, col0 + c * 32, row0);
         else if (c + 1 == nch) sg.flush(&p.map, box, col0 + c * 32, row0);
         else box0 = box;
+#endif
       } else if (row_ok) {
         if (nv >= 32 && vec) {
           uint4* d4 = reinterpret_cast<uint4*>(dst + c * 32);

@@ -1,0 +1,2 @@
+#!/bin/bash
+for rep in 1 2; do for b in gemm_probe gemm_probe_b128; do echo "== $b"; VP_NH=2 timeout 60 ./tools/$b k1 0 0 0 30 | grep -E "ideal|issuer|TFLOP"; done; done
