@@ -79,7 +79,8 @@ inline void prepare_store(EpiStoreF32::Params& ep, int M, int N) {
   }
   ep.use_tma = tma_store_ok(ep.out, ep.ldo, 4);
   if (ep.use_tma)
-    ep.map = make_store_map(ep.out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, uint64_t(N), uint64_t(M), uint64_t(ep.ldo));
+    ep.map = make_store_map(ep.out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, uint64_t(N), uint64_t(M), uint64_t(ep.ldo),
+                            VP_F32_BOX128 ? 128 : 64);
 }
 inline void prepare_store(EpiLogitStats::Params& ep, int M, int N) {
   ep.use_tma = tma_store_ok(ep.P, ep.ldp, 2);

@@ -39,6 +39,9 @@
 #ifndef VP_P_BOX128
 #define VP_P_BOX128 1  // K1 stores P in 32 x 128 B SWIZZLE_128B boxes (half the TMA row segments; 0: 64 B boxes)
 #endif
+#ifndef VP_F32_BOX128
+#define VP_F32_BOX128 1  // fp32 epilogues store 32 x 128 B SWIZZLE_128B boxes (0: two 64 B boxes per chunk)
+#endif
 #ifndef VP_K1_POLY
 #define VP_K1_POLY 0  // 1: half of the K1 epilogue's exponentials on the FMA pipe (ptx::ex2_poly)
 #endif
@@ -746,6 +749,25 @@ struct EpiStoreF32 {
           for (int j = 0; j < 32; ++j)
             if (j < nv) mx = fmaxf(mx, __uint_as_float(r[j]));
         }
+#if VP_F32_BOX128
+        // one 32-column fp32 box per chunk (32 rows x 128 B, SWIZZLE_128B): the
+        // warp's whole 4 KB staging area, single-buffered
+        if ((threadIdx.x & 31) == 0) ptx::bulk_wait_read<0>();
+        __syncwarp();
+        {
+          const uint32_t rr = threadIdx.x & 31;
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            ptx::st_shared_v4(sg.base + rr * 128u + ((uint32_t(q) ^ (rr & 7u)) << 4), r[4 * q], r[4 * q + 1],
+                              r[4 * q + 2], r[4 * q + 3]);
+        }
+        ptx::fence_proxy_async_smem();
+        __syncwarp();
+        if ((threadIdx.x & 31) == 0) {
+          sg.put(&p.map, sg.base, col0 + c * 32, row0, add);
+          ptx::bulk_commit();
+        }
+#else
         // two 16-column fp32 boxes per chunk, one fence
         const uint32_t b0 = sg.next();
 #pragma unroll
@@ -755,6 +777,7 @@ struct EpiStoreF32 {
         for (int q = 0; q < 4; ++q)
           ptx::st_shared_v4(Stager::chunk(b1, q), r[16 + 4 * q], r[16 + 4 * q + 1], r[16 + 4 * q + 2], r[16 + 4 * q + 3]);
         sg.flush2(&p.map, b0, col0 + c * 32, row0, b1, col0 + c * 32 + 16, row0, add);
+#endif
       });
     } else {
       float* dst = p.out + int64_t(row) * p.ldo + col0;
