@@ -298,27 +298,50 @@ def run_ours(args):
         Xh = X.cpu().pin_memory()
         Lh = labels.cpu().pin_memory()
         loss_h = torch.empty(T, dtype=torch.float32).pin_memory()
-        Xd, Ld = torch.empty_like(X), torch.empty_like(labels)
-        step_e2e = Step(ctx, args.alg, vm.TokenBatch(Xd, Ld), shard, state, outs)
+        # Double-buffered inputs: step i+1's host->device copy runs on a copy
+        # stream while step i computes (what a training loop's prefetch does);
+        # every step's copy and its loss read-back stay inside the timed region.
+        copy_stream = torch.cuda.Stream()
+        bufs = [(torch.empty_like(X), torch.empty_like(labels)) for _ in range(2)]
+        steps_e2e = [Step(ctx, args.alg, vm.TokenBatch(xd, ld), shard, state, outs) for xd, ld in bufs]
+        ready = [torch.cuda.Event() for _ in range(2)]
+        consumed = [torch.cuda.Event() for _ in range(2)]
 
-        def e2e_step():
-            Xd.copy_(Xh, non_blocking=True)
-            Ld.copy_(Lh, non_blocking=True)
-            step_e2e()
+        def issue_copy(i):
+            b = i % 2
+            copy_stream.wait_event(consumed[b])  # step i-2 is done with this buffer
+            with torch.cuda.stream(copy_stream):
+                bufs[b][0].copy_(Xh, non_blocking=True)
+                bufs[b][1].copy_(Lh, non_blocking=True)
+            ready[b].record(copy_stream)
+
+        def run_step(i):
+            b = i % 2
+            stream.wait_event(ready[b])
+            steps_e2e[b]()
+            consumed[b].record(stream)
             loss_h.copy_(outs[0], non_blocking=True)
 
-        for _ in range(args.warmup):
-            e2e_step()
+        def e2e_steps(n):
+            copy_stream.wait_event(ev0)
+            issue_copy(0)
+            for i in range(n):
+                if i + 1 < n:
+                    issue_copy(i + 1)
+                run_step(i)
+
+        ev0.record(stream)
+        e2e_steps(args.warmup)
         barrier()
         ev0.record(stream)
-        for _ in range(args.steps):
-            e2e_step()
+        e2e_steps(args.steps)
         ev1.record(stream)
         barrier()
         ms_e2e = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
         e2e = {"value": T / (ms_e2e / 1e3), "unit": "tokens/s", "ms_per_step": ms_e2e,
                "h2d_bytes_per_step": Xh.numel() * 2 + Lh.numel() * 8, "d2h_bytes_per_step": loss_h.numel() * 4,
-               "path": "vp_run_%s via ctypes (C ABI), pinned host X/labels -> HBM, loss -> host" % args.alg}
+               "path": "vp_run_%s via ctypes (C ABI), pinned host X/labels -> HBM (double-buffered on a copy "
+                       "stream, overlapping the previous step), loss -> host" % args.alg}
 
     if rank != 0:
         ctx.close()

@@ -375,3 +375,22 @@ def test_split_k_dx_is_exact_to_tolerance_and_deterministic(splits):
         _, again = run_device(sctx, alg, batch, Wd, 2, 256, with_softmax=False)
         assert torch.equal(out.grad_x, again.grad_x), alg
     sctx.close()
+
+
+def test_gemm_schedule_options_do_not_change_results(ctx):
+    # wave lockstep, split-K choice and store boxes change only timing / the
+    # fixed accumulation order of split units; every setting must reproduce
+    # the default bits (lockstep) or the oracle (splits)
+    X, W, g = oracle.random_instance(2048, 1024, 64000, 8)
+    Xb, Wb, batch, Wd = device_case(X, W, g)
+    base, _ = run_device(ctx, "alg2", batch, Wd, 1, 1024, with_softmax=False)
+    for opts in ({"lockstep_dx": 0, "lockstep_dw": 0}, {"lockstep_logits": 8, "lockstep_dx": 2, "lockstep_dw": 32},
+                 {"store_evict_first": 1}):
+        octx = vm.Context(0)
+        for k, v in opts.items():
+            octx.set_option(k, v)
+        res, _ = run_device(octx, "alg2", batch, Wd, 1, 1024, with_softmax=False)
+        for key in ("loss", "grad_x", "grad_w"):
+            assert np.array_equal(res[key], base[key]), (opts, key)
+        octx.close()
+    vm.Context(0).set_option("store_evict_first", 0)  # process-wide option: restore
