@@ -88,7 +88,8 @@ int vp_ctx_sync(vp_ctx_t ctx);
 int vp_ctx_reserve(vp_ctx_t ctx, int64_t n_tok, int64_t h, int p);
 /* Options: "cta_group" (1 or 2, default 2), "gemm_sms" (SMs used by GEMMs),
  * "raster_{logits,dx,dw}" (tile order, see GemmGeom::raster),
- * "policy_{logits,dx,dw}" (TMA L2 policy: -1 default, 0 normal, 1 first, 2 last),
+ * "policy_{logits,dx,dw}" (TMA L2 policy of both operands: -1 per-epilogue default,
+ * 0 normal, 1 first, 2 last = the default), "policyb_{logits,dx,dw}" (B operand only),
  * "multicast" (1 = CTA-pair clusters, 2 = 4-CTA clusters sharing B by TMA multicast),
  * "nh_logits" / "nh_dx" / "nh_dw" (1 = 256x256 pair tiles, 2 = 256x512 pair tiles),
  * "force_collectives" (1 = use the NCCL group even with one rank; tests),
@@ -98,7 +99,7 @@ int vp_ctx_reserve(vp_ctx_t ctx, int64_t n_tok, int64_t h, int p);
  * "epi_wait" (GEMM epilogue wait: 0 try_wait loop, 1 nanosleep backoff),
  * "lockstep_logits" / "lockstep_dx" / "lockstep_dw" (wave lockstep of the
  * persistent GEMM's clusters every N k-blocks so co-scheduled tiles share
- * operand bands in L2; 0 = off; defaults 0 / 8 / 8),
+ * operand bands in L2; 0 = off; default 8 for all three),
  * "splits_dx" (split-K of the dX / A GEMM, whose K = V_k leaves few tile
  * waves: 0 = chosen from the wave quantisation (default), 1 = off, 2..4 =
  * forced; partial sums are added in split order, so results are deterministic),

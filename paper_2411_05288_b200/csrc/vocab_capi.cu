@@ -100,9 +100,12 @@ struct vp_ctx_s {
   int gemm_sms = 148;
   int cg = 2;
   // GEMM tile rasterisation and TMA L2 policy per GEMM [logits, dX, dW]
-  // (measured: evict_normal on both operands beats first/last hints)
+  // (measured with lockstep on: evict_last on both operands of all three
+  // GEMMs, +2.7% tokens/s over evict_normal, tools/experiments/combo_ab.sh)
   int raster[3] = {0, 16, -4};
-  int pol[3] = {0, 0, 0};
+  int pol[3] = {2, 2, 2};
+  int polb[3] = {-9, -9, -9};  // B-operand policy when set ("policyb_*"); -9 = same as pol
+  int pb(int i) const { return polb[i] == -9 ? pol[i] : polb[i]; }
   int mc = 1;  // CTA pairs per cluster sharing B by TMA multicast (1 or 2)
   int nh[3] = {2, 2, 2};  // N halves per tile (2 = 256 x 512 pair tiles) for [logits, dX, dW]
   // split-K of the dX GEMM (K = V_k, few waves): ordered, deterministic;
@@ -111,7 +114,7 @@ struct vp_ctx_s {
   int splits_dx = 0;
   // wave lockstep per GEMM [logits, dX, dW]: epoch length in k-blocks (0 = off)
   vp::LockCfg lock;
-  int lock_epoch[3] = {0, 8, 8};
+  int lock_epoch[3] = {8, 8, 8};
   const vp::LockCfg* lock_for(int i) {
     lock.epoch = lock_epoch[i];
     return lock.epoch > 0 ? &lock : nullptr;
@@ -247,7 +250,7 @@ void gemm_logits(vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* s, vp_state
   timed_gemm(c, 0, [&] {
     vp::launch_gemm<vp::EpiLogitStats>(c->cg, {b->X, b->ldx, false}, {s->W, s->ldw, false}, int(b->n_tok),
                                        int(st->rows), int(b->h), c->raster[0], ep, c->gemm_sms, c->stream,
-                                       c->pol[0], c->pol[0], c->eff_mc(0), c->eff_nh(0), nullptr, c->lock_for(0));
+                                       c->pol[0], c->pb(0), c->eff_mc(0), c->eff_nh(0), nullptr, c->lock_for(0));
   });
   ++c->launches;
 }
@@ -270,7 +273,7 @@ void gemm_dx(vp_ctx_s* c, vp_state_s* st, const vp_shard_t* s, float* out, int64
   timed_gemm(c, 2, [&] {
     vp::launch_gemm<vp::EpiStoreF32>(c->cg, {st->P, st->ldp, false}, {s->W, s->ldw, true}, int(st->n_tok),
                                      int(st->h), int(st->rows), c->raster[1], ep, c->gemm_sms, c->stream, c->pol[1],
-                                     c->pol[1], c->eff_mc(1), c->eff_nh(1), c->splits_dx == 1 ? nullptr : &c->split,
+                                     c->pb(1), c->eff_mc(1), c->eff_nh(1), c->splits_dx == 1 ? nullptr : &c->split,
                                      c->lock_for(1));
   });
   ++c->launches;
@@ -282,7 +285,7 @@ void gemm_dw(vp_ctx_s* c, vp_state_s* st, const void* Xop, int64_t ldx, float* o
   const int raster = c->raster[2];
   timed_gemm(c, 3, [&] {
     vp::launch_gemm<vp::EpiStoreF32>(c->cg, {st->P, st->ldp, true}, {Xop, ldx, true}, int(st->rows), int(st->h),
-                                     int(st->n_tok), raster, ep, c->gemm_sms, c->stream, c->pol[2], c->pol[2],
+                                     int(st->n_tok), raster, ep, c->gemm_sms, c->stream, c->pol[2], c->pb(2),
                                      c->eff_mc(2), c->eff_nh(2), nullptr, c->lock_for(2));
   });
   ++c->launches;
@@ -975,6 +978,12 @@ int vp_ctx_set_option(vp_ctx_t c, const char* key, int64_t value) {
         require(value >= -1 && value <= 2, "vp_ctx_set_option: policy must be -1..2");
         c->pol[idx] = int(value);
       }
+    } else if (k.rfind("policyb_", 0) == 0) {
+      const std::string which = k.substr(8);
+      const int idx = which == "logits" ? 0 : which == "dx" ? 1 : which == "dw" ? 2 : -1;
+      require(idx >= 0, "vp_ctx_set_option: policyb_ suffix must be logits, dx or dw");
+      require(value >= -1 && value <= 2, "vp_ctx_set_option: policy must be -1..2");
+      c->polb[idx] = int(value);
     } else if (k == "nh_logits" || k == "nh_dx" || k == "nh_dw") {
       require(value == 1 || value == 2, "vp_ctx_set_option: nh must be 1 or 2");
       require(value == 1 || c->cg == 2, "vp_ctx_set_option: 512-wide tiles need cta_group 2");
