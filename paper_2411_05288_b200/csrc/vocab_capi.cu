@@ -102,7 +102,7 @@ struct vp_ctx_s {
   // GEMM tile rasterisation and TMA L2 policy per GEMM [logits, dX, dW]
   // (measured with lockstep on: evict_last on both operands of all three
   // GEMMs, +2.7% tokens/s over evict_normal, tools/experiments/combo_ab.sh)
-  int raster[3] = {0, 16, -4};
+  int raster[3] = {16, 16, -4};  // logits: M-fastest in groups of 16 m-tiles (+1.3% with lockstep)
   int pol[3] = {2, 2, 2};
   int polb[3] = {-9, -9, -9};  // B-operand policy when set ("policyb_*"); -9 = same as pol
   int pb(int i) const { return polb[i] == -9 ? pol[i] : polb[i]; }

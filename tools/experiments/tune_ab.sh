@@ -1,0 +1,10 @@
+#!/bin/bash
+B="python bench.py --no-cpu-baseline --no-e2e --steps 10 --warmup 3"
+L4="--opt lockstep_logits=4 --opt lockstep_dx=4 --opt lockstep_dw=4"
+L16="--opt lockstep_logits=16 --opt lockstep_dx=16 --opt lockstep_dw=16"
+for rep in 1 2 3; do
+  for cfg in "" "$L4" "$L16" "--opt raster_dx=8" "--opt raster_dx=32" "--opt raster_logits=16" "--opt raster_dw=-8"; do
+    out=$(timeout 200 $B $cfg 2>/dev/null)
+    echo "$out" | python -c "import json,sys; d=json.loads(sys.stdin.read()); g=d['roofline']['gemms']; print('%-72s %8.0f tok/s %6.2f ms | logits %.2f dx %.2f dw %.2f | clk %s' % ('$cfg' or 'default', d['value'], d['ms_per_step'], g['logits']['avg_ms'], g['dx']['avg_ms'], g['dw']['avg_ms'], d['clocks']['sm_mhz']))"
+  done
+done
