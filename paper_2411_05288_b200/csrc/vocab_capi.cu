@@ -134,7 +134,7 @@ struct vp_ctx_s {
   double gemm_ms[4] = {0, 0, 0, 0};
   int64_t gemm_n[4] = {0, 0, 0, 0};
   // workspace
-  DevBuf inv, scale, xs, keys, gathered, packed, tmp_m, tmp_s;
+  DevBuf inv, scale, xs, gathered, packed, tmp_m, tmp_s, heads, counts;
 
   void activate() const {
     VP_CUDA(cudaSetDevice(device));
@@ -319,44 +319,23 @@ float* global_scale(vp_ctx_s* c, const vp_state_s* st, vp_stats_t g) {
   return sc;
 }
 
-// Sorted keys of the owned tokens of one shard (deterministic segments).
-unsigned long long* sorted_keys(vp_ctx_s* c, const int64_t* tok, int64_t n, int64_t rb, int64_t re, int* n_pad_out,
-                                int err_bit = 0) {
-  int n_pad = 1;
-  while (n_pad < n) n_pad <<= 1;
-  n_pad = std::max(n_pad, 2);
-  auto* keys = c->buf<unsigned long long>(c->keys, size_t(n_pad));
-  vp::k_make_keys<<<unsigned(ceil_div(n_pad, 256)), 256, 0, c->stream>>>(tok, int(n), n_pad, rb, re, keys,
-                                                                         c->d_err, err_bit);
-  VP_KCHECK();
-  const unsigned chunks = unsigned(ceil_div(n_pad, 2048));
-  vp::k_bitonic_shared<<<chunks, 1024, 0, c->stream>>>(keys, n_pad, 0, 1);
-  VP_KCHECK();
-  c->launches += 2;
-  for (int k = 4096; k <= n_pad; k <<= 1) {
-    for (int j = k >> 1; j >= 2048; j >>= 1) {
-      vp::k_bitonic_global<<<unsigned(ceil_div(n_pad, 256)), 256, 0, c->stream>>>(keys, n_pad, j, k);
-      VP_KCHECK();
-      ++c->launches;
-    }
-    vp::k_bitonic_shared<<<chunks, 1024, 0, c->stream>>>(keys, n_pad, k, 0);
-    VP_KCHECK();
-    ++c->launches;
-  }
-  *n_pad_out = n_pad;
-  return keys;
-}
-
-// dst[row] (+)= sign * src[i] over owned tokens, ascending i per row.
+// dst[row] (+)= sign * src[i] over owned tokens, ascending i per row
+// (sort-free: row heads + multiplicities, then one warp per row head).
 template <typename Src>
 void segment_scatter(vp_ctx_s* c, const int64_t* tok, int64_t n, int64_t rb, int64_t re, const Src* src, int64_t lds,
-                     int64_t h, float sign, float* dst, int64_t ldd, int accumulate) {
-  int n_pad = 0;
-  unsigned long long* keys = sorted_keys(c, tok, n, rb, re, &n_pad);
-  vp::k_segment_scatter<Src><<<unsigned(n_pad), 256, 0, c->stream>>>(keys, n_pad, src, lds, int(h), sign, dst, ldd,
-                                                                      accumulate);
+                     int64_t h, float sign, float* dst, int64_t ldd, int accumulate, int err_bit = 0) {
+  if (n == 0) return;
+  const int64_t rows = re - rb;
+  auto* head = c->buf<unsigned>(c->heads, size_t(rows));
+  auto* cnt = c->buf<int>(c->counts, size_t(rows));
+  VP_CUDA(cudaMemsetAsync(head, 0xFF, size_t(rows) * sizeof(unsigned), c->stream));
+  VP_CUDA(cudaMemsetAsync(cnt, 0, size_t(rows) * sizeof(int), c->stream));
+  vp::k_row_heads<<<c->grid_for(n, 256), 256, 0, c->stream>>>(tok, int(n), rb, re, head, cnt, c->d_err, err_bit);
   VP_KCHECK();
-  ++c->launches;
+  vp::k_scatter_rows<Src><<<unsigned(n), 256, 0, c->stream>>>(
+      tok, int(n), rb, re, head, cnt, src, lds, int(h), sign, dst, ldd, accumulate);
+  VP_KCHECK();
+  c->launches += 2;
 }
 
 // alg1_pass_S (VM.cpp:151-162): Y = X W_k^T with the fused stats epilogue
@@ -911,7 +890,8 @@ int vp_ctx_destroy(vp_ctx_t c) {
     if (c->ev_ready) cudaEventDestroy(c->ev_ready);
     if (c->ev_done) cudaEventDestroy(c->ev_done);
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
-    for (DevBuf* b : {&c->inv, &c->scale, &c->xs, &c->keys, &c->gathered, &c->packed, &c->tmp_m, &c->tmp_s})
+    for (DevBuf* b : {&c->inv, &c->scale, &c->xs, &c->gathered, &c->packed, &c->tmp_m, &c->tmp_s,
+                      &c->heads, &c->counts})
       b->release();
     if (c->d_err) cudaFree(c->d_err);
     if (c->split.flags) cudaFree(c->split.flags);
@@ -949,14 +929,11 @@ int vp_ctx_reserve(vp_ctx_t c, int64_t n_tok, int64_t h, int p) {
   return api([&] {
     require(c != nullptr && n_tok >= 1 && h >= 1 && p >= 1, "vp_ctx_reserve: bad arguments");
     c->activate();
-    int n_pad = 2;
-    while (n_pad < n_tok) n_pad <<= 1;
     c->buf<float>(c->inv, size_t(n_tok));
     c->buf<float>(c->scale, size_t(n_tok));
     c->buf<float>(c->tmp_m, size_t(n_tok));
     c->buf<float>(c->tmp_s, size_t(n_tok));
     c->buf<__nv_bfloat16>(c->xs, size_t(n_tok * h));
-    c->buf<unsigned long long>(c->keys, size_t(n_pad));
     c->buf<float>(c->packed, size_t(2 * n_tok));
     c->buf<float>(c->gathered, size_t(2 * n_tok * std::max(p, c->nranks)));
   });
@@ -1356,16 +1333,12 @@ int vp_input_backward(vp_ctx_t c, const void* grad, int64_t ldg, int grad_is_f32
                                 c->stream));
     }
     if (n_tok == 0) return;
-    int n_pad = 0;
-    unsigned long long* keys = sorted_keys(c, tokens, n_tok, s->row_begin, s->row_end, &n_pad, kErrInputBwd);
     if (grad_is_f32)
-      vp::k_segment_scatter<float><<<unsigned(n_pad), 256, 0, c->stream>>>(
-          keys, n_pad, static_cast<const float*>(grad), ldg, int(h), 1.f, gw, ldgw, 1);
+      segment_scatter(c, tokens, n_tok, s->row_begin, s->row_end, static_cast<const float*>(grad), ldg, h, 1.f, gw, ldgw,
+                      1, kErrInputBwd);
     else
-      vp::k_segment_scatter<__nv_bfloat16><<<unsigned(n_pad), 256, 0, c->stream>>>(
-          keys, n_pad, static_cast<const __nv_bfloat16*>(grad), ldg, int(h), 1.f, gw, ldgw, 1);
-    VP_KCHECK();
-    ++c->launches;
+      segment_scatter(c, tokens, n_tok, s->row_begin, s->row_end, static_cast<const __nv_bfloat16*>(grad), ldg, h, 1.f,
+                      gw, ldgw, 1, kErrInputBwd);
   });
 }
 
