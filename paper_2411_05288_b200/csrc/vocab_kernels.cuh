@@ -527,14 +527,28 @@ __device__ __forceinline__ void scatter_row(const int64_t* __restrict__ tok, int
   float* d = dst + r * ldd;
   if (c_tot == 1) {
     const Src* sp = src + int64_t(i) * lds;
-    for (int c = threadIdx.x * 4; c < h; c += 1024) {
-      float4 acc = accumulate ? *reinterpret_cast<const float4*>(d + c) : make_float4(0.f, 0.f, 0.f, 0.f);
-      const float4 v = load4(sp + c);
-      acc.x += sign * v.x;
-      acc.y += sign * v.y;
-      acc.z += sign * v.z;
-      acc.w += sign * v.w;
-      *reinterpret_cast<float4*>(d + c) = acc;
+    // four passes' loads in flight before any store (memory-level parallelism)
+    for (int c0 = threadIdx.x * 4; c0 < h; c0 += 4096) {
+      float4 acc[4], v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int c = c0 + u * 1024;
+        if (c < h) {
+          acc[u] = accumulate ? *reinterpret_cast<const float4*>(d + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+          v[u] = load4(sp + c);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int c = c0 + u * 1024;
+        if (c < h) {
+          acc[u].x += sign * v[u].x;
+          acc[u].y += sign * v[u].y;
+          acc[u].z += sign * v[u].z;
+          acc[u].w += sign * v[u].w;
+          *reinterpret_cast<float4*>(d + c) = acc[u];
+        }
+      }
     }
     return;
   }
