@@ -167,7 +167,12 @@ inline void launch_gemm_t(const Operand& A, const Operand& B, int M, int N, int 
   g.store_evict_first = g_store_evict_first;
   g.epi_wait = g_epi_wait;
   auto kern = gemm_sm100_kernel<CG, A_MN, B_MN, Epi, MC, NH>;
-  static bool attr_done = false;
+  // per device: the smem attribute and the occupancy query (contexts of one
+  // process may drive several GPUs)
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) dev = 0;
+  static bool attr_done_dev[64] = {};
+  bool& attr_done = attr_done_dev[dev];
   if (!attr_done) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
     if (e != cudaSuccess) throw std::runtime_error(std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e));
@@ -178,8 +183,9 @@ inline void launch_gemm_t(const Operand& A, const Operand& B, int M, int N, int 
   cudaLaunchConfig_t cfg = {};
   // persistent grid: no more clusters than can be co-resident (clusters of 4
   // cannot tile all 148 SMs: GPC packing leaves some idle)
-  static int max_active = -1;
-  if (max_active < 0) {
+  static int max_active_dev[64] = {};
+  int& max_active = max_active_dev[dev];
+  if (max_active <= 0) {
     cudaLaunchConfig_t q = {};
     q.gridDim = dim3(unsigned(num_sms / CL * CL), 1, 1);
     q.blockDim = dim3(C::THREADS, 1, 1);
