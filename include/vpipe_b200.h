@@ -100,9 +100,10 @@ int vp_ctx_reserve(vp_ctx_t ctx, int64_t n_tok, int64_t h, int p);
  * "lockstep_logits" / "lockstep_dx" / "lockstep_dw" (wave lockstep of the
  * persistent GEMM's clusters every N k-blocks so co-scheduled tiles share
  * operand bands in L2; 0 = off; default 8 for all three),
- * "splits_dx" (split-K of the dX / A GEMM, whose K = V_k leaves few tile
- * waves: 0 = chosen from the wave quantisation (default), 1 = off, 2..4 =
- * forced; partial sums are added in split order, so results are deterministic),
+ * "splits_dx" / "splits_dw" (split-K of the dX / A GEMM, whose K = V_k leaves
+ * few tile waves, and of the dW GEMM for small shards: 0 = chosen from the wave
+ * quantisation (default), 1 = off, 2..4 = forced; partial sums are added in
+ * split order, so results are deterministic),
  * "tma_store" (1 = GEMM epilogues store through smem staging + TMA, the
  * default; 0 = per-thread st.global; process-wide),
  * "accumulate_grad_w" (1 = the T passes add dW_k into grad_w: gradient

@@ -109,7 +109,8 @@ struct LockCfg {
 // Splits for a persistent GEMM of `tiles` tiles on `clusters` clusters and
 // num_kb k-blocks: the smallest S in 1..4 whose wave efficiency
 // tiles*S / (clusters * ceil(tiles*S / clusters)) is within 1% of the best,
-// keeping >= 16 k-blocks per split; S = 1 unless that gains > 2%.
+// keeping >= 128 k-blocks per split (shorter units are epilogue-bound: dW of
+// an 8-way shard split 3 ways ran 20% slower); S = 1 unless that gains > 2%.
 inline int choose_splits(int tiles, int clusters, int num_kb) {
   auto eff = [&](int S) {
     const double w = double(tiles) * S / clusters;
@@ -118,7 +119,7 @@ inline int choose_splits(int tiles, int clusters, int num_kb) {
   int best = 1;
   double be = eff(1);
   for (int S = 2; S <= 4; ++S)
-    if (num_kb / S >= 16 && eff(S) > be + 0.02) {
+    if (num_kb / S >= 128 && eff(S) > be + 0.02) {
       best = S;
       be = eff(S);
     }

@@ -111,7 +111,7 @@ struct vp_ctx_s {
   // split-K of the dX GEMM (K = V_k, few waves): ordered, deterministic;
   // splits_dx option: 0 = by wave quantisation, 1 = off, 2..4 = forced
   vp::SplitCfg split;
-  int splits_dx = 0;
+  int splits_dx = 0, splits_dw = 0;
   // wave lockstep per GEMM [logits, dX, dW]: epoch length in k-blocks (0 = off)
   vp::LockCfg lock;
   int lock_epoch[3] = {8, 8, 8};
@@ -283,10 +283,12 @@ void gemm_dx(vp_ctx_s* c, vp_state_s* st, const vp_shard_t* s, float* out, int64
 void gemm_dw(vp_ctx_s* c, vp_state_s* st, const void* Xop, int64_t ldx, float* out, int64_t ldo) {
   vp::EpiStoreF32::Params ep{out, ldo, nullptr, 0, nullptr, c->accumulate_dw ? 1 : 0};
   const int raster = c->raster[2];
+  c->split.force = c->splits_dw;  // (few-wave shards, e.g. V/8 rows: 13.5 waves -> 3 splits)
   timed_gemm(c, 3, [&] {
     vp::launch_gemm<vp::EpiStoreF32>(c->cg, {st->P, st->ldp, true}, {Xop, ldx, true}, int(st->rows), int(st->h),
                                      int(st->n_tok), raster, ep, c->gemm_sms, c->stream, c->pol[2], c->pb(2),
-                                     c->eff_mc(2), c->eff_nh(2), nullptr, c->lock_for(2));
+                                     c->eff_mc(2), c->eff_nh(2), c->splits_dw == 1 ? nullptr : &c->split,
+                                     c->lock_for(2));
   });
   ++c->launches;
 }
@@ -979,9 +981,9 @@ int vp_ctx_set_option(vp_ctx_t c, const char* key, int64_t value) {
     } else if (k == "store_evict_first") {
       require(value == 0 || value == 1, "vp_ctx_set_option: store_evict_first must be 0 or 1");
       vp::g_store_evict_first = int(value);
-    } else if (k == "splits_dx") {
-      require(value >= 0 && value <= 4, "vp_ctx_set_option: splits_dx must be in 0..4");
-      c->splits_dx = int(value);
+    } else if (k == "splits_dx" || k == "splits_dw") {
+      require(value >= 0 && value <= 4, "vp_ctx_set_option: splits_dx / splits_dw must be in 0..4");
+      (k == "splits_dx" ? c->splits_dx : c->splits_dw) = int(value);
     } else if (k == "tma_store") {
       require(value == 0 || value == 1, "vp_ctx_set_option: tma_store must be 0 or 1");
       vp::g_tma_store = int(value);

@@ -360,7 +360,7 @@ def test_memcheck_of_a_ragged_alg2_step():
 
 
 @pytest.mark.parametrize("splits", [1, 2, 3, 4])
-def test_split_k_dx_is_exact_to_tolerance_and_deterministic(splits):
+def test_split_k_dx_dw_is_exact_to_tolerance_and_deterministic(splits):
     # The dX / A GEMM (K = V_k) may be split over K into ordered partial sums
     # (option splits_dx); every split count must meet the parity bar and give
     # identical bits on a re-run.
@@ -369,11 +369,13 @@ def test_split_k_dx_is_exact_to_tolerance_and_deterministic(splits):
     ref = oracle.oracle_output_layer(Xb, g, Wb, want_softmax=False)
     sctx = vm.Context(0)
     sctx.set_option("splits_dx", splits)
+    sctx.set_option("splits_dw", splits)
     for alg in ALGS:
         res, out = run_device(sctx, alg, batch, Wd, 2, 256, with_softmax=False)
         assert_parity(res, ref, f"splits={splits} {alg}")
         _, again = run_device(sctx, alg, batch, Wd, 2, 256, with_softmax=False)
         assert torch.equal(out.grad_x, again.grad_x), alg
+        assert torch.equal(out.grad_w_full(), again.grad_w_full()), alg
     sctx.close()
 
 

@@ -1,0 +1,8 @@
+#!/bin/bash
+B="python bench.py --no-cpu-baseline --no-e2e --steps 10 --warmup 3"
+for rep in 1 2 3; do
+  for cfg in "" "--opt epi_wait=0" "--opt splits_dx=3" "--opt raster_dw=-2"; do
+    out=$(timeout 200 $B $cfg 2>/dev/null)
+    echo "$out" | python -c "import json,sys; d=json.loads(sys.stdin.read()); g=d['roofline']['gemms']; print('%-30s %8.0f tok/s %6.2f ms | logits %.2f dx %.2f dw %.2f | clk %s' % ('$cfg' or 'default', d['value'], d['ms_per_step'], g['logits']['avg_ms'], g['dx']['avg_ms'], g['dw']['avg_ms'], d['clocks']['sm_mhz']))"
+  done
+done
