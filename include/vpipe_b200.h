@@ -104,6 +104,9 @@ int vp_ctx_reserve(vp_ctx_t ctx, int64_t n_tok, int64_t h, int p);
  * few tile waves, and of the dW GEMM for small shards: 0 = chosen from the wave
  * quantisation (default), 1 = off, 2..4 = forced; partial sums are added in
  * split order, so results are deterministic),
+ * "cooperative" (1 = persistent GEMMs launched cooperatively, so the whole grid
+ * is co-resident, which their cross-CTA waits rely on when kernels of other
+ * streams hold SMs; default 1; process-wide),
  * "tma_store" (1 = GEMM epilogues store through smem staging + TMA, the
  * default; 0 = per-thread st.global; process-wide),
  * "accumulate_grad_w" (1 = the T passes add dW_k into grad_w: gradient

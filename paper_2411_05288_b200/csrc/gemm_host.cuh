@@ -140,8 +140,9 @@ struct Operand {
 };
 
 inline unsigned long long* g_gemm_prof = nullptr;  // set by probes: {clk0, t0, clk1, t1} of CTA 0
-inline int g_epi_wait = 1;
-inline int g_store_evict_first = 0;  // GemmGeom::store_evict_first for subsequent launches                          // GemmGeom::epi_wait for subsequent launches
+inline int g_epi_wait = 1;            // GemmGeom::epi_wait for subsequent launches
+inline int g_store_evict_first = 0;  // GemmGeom::store_evict_first for subsequent launches
+inline int g_cooperative = 1;        // cooperative (co-resident) launches of the persistent GEMMs
 
 template <int CG, bool A_MN, bool B_MN, class Epi, int MC = 1, int NH = 1>
 inline void launch_gemm_t(const Operand& A, const Operand& B, int M, int N, int K, int raster,
@@ -224,13 +225,19 @@ inline void launch_gemm_t(const Operand& A, const Operand& B, int M, int N, int 
   cfg.blockDim = dim3(C::THREADS, 1, 1);
   cfg.dynamicSmemBytes = C::SMEM_BYTES;
   cfg.stream = st;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = CL;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
+  // Cooperative launch: the whole persistent grid is guaranteed co-resident.
+  // The kernel's cross-CTA waits (K1's row reference, ordered split-K units,
+  // wave lockstep) rely on it; without it, kernels of other streams holding
+  // SMs could leave a waited-on cluster unscheduled.
+  at[1].id = cudaLaunchAttributeCooperative;
+  at[1].val.cooperative = g_cooperative;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   if (lock != nullptr && lock->counters != nullptr && lock->epoch > 0) {
     const int units = tiles * g.splits;
     const int waves = (units + clusters - 1) / clusters;

@@ -978,6 +978,9 @@ int vp_ctx_set_option(vp_ctx_t c, const char* key, int64_t value) {
     } else if (k == "lockstep_logits" || k == "lockstep_dx" || k == "lockstep_dw") {
       require(value >= 0 && value <= 4096, "vp_ctx_set_option: lockstep epoch must be in 0..4096 k-blocks");
       c->lock_epoch[k == "lockstep_logits" ? 0 : k == "lockstep_dx" ? 1 : 2] = int(value);
+    } else if (k == "cooperative") {
+      require(value == 0 || value == 1, "vp_ctx_set_option: cooperative must be 0 or 1");
+      vp::g_cooperative = int(value);
     } else if (k == "store_evict_first") {
       require(value == 0 || value == 1, "vp_ctx_set_option: store_evict_first must be 0 or 1");
       vp::g_store_evict_first = int(value);
