@@ -5,6 +5,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -869,6 +870,14 @@ int vp_ctx_create(int device, vp_ctx_t* out) {
       c->stream = c->own_stream;
       VP_CUDA(cudaMalloc(&c->d_err, sizeof(int)));
       VP_CUDA(cudaMemset(c->d_err, 0, sizeof(int)));
+      // Under Nsight Compute / Systems (they set NV_NSIGHT_INJECTION_* in the
+      // target) launch the GEMMs non-cooperatively: ncu's kernel replay cannot
+      // relaunch cooperative grids.  The kernels are identical; only the
+      // co-residency guarantee against other streams' kernels is dropped while
+      // profiling.
+      if (std::getenv("NV_NSIGHT_INJECTION_TRANSPORT_TYPE") != nullptr ||
+          std::getenv("CUDA_INJECTION64_PATH") != nullptr)
+        vp::g_cooperative = 0;
       c->lock.capacity = int64_t(1) << 20;
       VP_CUDA(cudaMalloc(&c->lock.counters, size_t(c->lock.capacity) * sizeof(int)));
       c->split.max_tiles = 1 << 14;
