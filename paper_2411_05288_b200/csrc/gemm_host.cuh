@@ -71,12 +71,7 @@ inline int g_tma_store = 1;  // epilogue stores through TMA when the output allo
 inline bool tma_store_ok(const void* p, int64_t ld, int esize) {
   return g_tma_store && (reinterpret_cast<uintptr_t>(p) & 15) == 0 && (ld * esize) % 16 == 0;
 }
-inline int g_f32_store_mode = 1;  // EpiStoreF32: 1 = TMA staging, 2 = direct coalesced (16x256b TMEM loads)
 inline void prepare_store(EpiStoreF32::Params& ep, int M, int N) {
-  if (g_tma_store && g_f32_store_mode == 2) {
-    ep.use_tma = 2;
-    return;
-  }
   ep.use_tma = tma_store_ok(ep.out, ep.ldo, 4);
   if (ep.use_tma)
     ep.map = make_store_map(ep.out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, uint64_t(N), uint64_t(M), uint64_t(ep.ldo),

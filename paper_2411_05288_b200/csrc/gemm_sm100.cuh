@@ -633,10 +633,10 @@ struct EpiStoreF32 {
     int64_t ld_stats;
     const float* row_scale;  // optional per-row factor applied on store
     int accumulate = 0;      // out += D instead of out = D (gradient accumulation)
-    // 0: per-row st.global from the 32x32b TMEM layout; 1: smem staging +
-    // TMA store through `map` (fp32 [M x N], 32 x 16 boxes, SWIZZLE_64B);
-    // 2: direct coalesced st.global from the 16x256b TMEM layout (no smem:
-    // the mainloop already uses most of the SM's shared-memory bandwidth)
+    // 0: per-row st.global (unaligned outputs); 1: smem staging + TMA store
+    // through `map` (fp32 [M x N], 32 x 32 boxes, SWIZZLE_128B).  (A direct
+    // coalesced store from the 16x256b TMEM layout measured slower: dW 92 ->
+    // 85% of MMA-ideal cycles.)
     int use_tma = 0;
     CUtensorMap map;
   };
@@ -644,76 +644,6 @@ struct EpiStoreF32 {
   struct Pre {
     float rs;
   };
-  // mode 2: this warp's 32 rows x nvalid columns, 16 rows per TMEM load pass
-  __device__ static void store16(const Params& p, const GemmGeom& g, uint32_t taddr, int row, int col0, int nb,
-                                 const Pre& pre, bool add, int nvalid) {
-    const int lane = threadIdx.x & 31, rq = row - lane;  // warp's first row
-    const int rsub = lane >> 2, csub = 2 * (lane & 3);
-    const bool vec = ((p.ldo & 1) == 0) && ((reinterpret_cast<uintptr_t>(p.out) & 7) == 0);
-    const int nch = (nvalid + 31) / 32;
-#pragma unroll 1
-    for (int lh = 0; lh < 2; ++lh) {
-      float rs[2], mx[2] = {-INFINITY, -INFINITY};
-      int rows[2];
-#pragma unroll
-      for (int hi = 0; hi < 2; ++hi) {
-        const int rl = 16 * lh + 8 * hi + rsub;  // row within the warp's 32
-        rows[hi] = rq + rl;
-        rs[hi] = __shfl_sync(0xffffffffu, pre.rs, rl);
-      }
-      const uint32_t ta = taddr + (uint32_t(16 * lh) << 16);
-      uint32_t ra[16], rb[16];
-      auto body = [&](uint32_t (&r)[16], int cc) {
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const int c = cc * 32 + 8 * k + csub;  // column within the call
-#pragma unroll
-          for (int hi = 0; hi < 2; ++hi) {
-            const float v0 = __uint_as_float(r[4 * k + 2 * hi]) * rs[hi];
-            const float v1 = __uint_as_float(r[4 * k + 2 * hi + 1]) * rs[hi];
-            if (p.tile_max) {
-              if (c < nvalid) mx[hi] = fmaxf(mx[hi], v0);
-              if (c + 1 < nvalid) mx[hi] = fmaxf(mx[hi], v1);
-            }
-            if (rows[hi] >= g.M || c >= nvalid) continue;
-            float* d = p.out + int64_t(rows[hi]) * p.ldo + col0 + c;
-            if (vec && c + 1 < nvalid) {
-              if (add) ptx::red_add_v2(d, v0, v1);
-              else *reinterpret_cast<float2*>(d) = make_float2(v0, v1);
-            } else {
-              d[0] = add ? d[0] + v0 : v0;
-              if (c + 1 < nvalid) d[1] = add ? d[1] + v1 : v1;
-            }
-          }
-        }
-      };
-      ptx::tmem_ld16x256_x4(ta, ra);
-      ptx::tmem_ld_wait();
-      ptx::tmem_pin16(ra);
-#pragma unroll 1
-      for (int cc = 0; cc < nch; cc += 2) {
-        if (cc + 1 < nch) ptx::tmem_ld16x256_x4(ta + (cc + 1) * 32, rb);
-        body(ra, cc);
-        if (cc + 1 >= nch) break;
-        ptx::tmem_ld_wait();
-        ptx::tmem_pin16(rb);
-        if (cc + 2 < nch) ptx::tmem_ld16x256_x4(ta + (cc + 2) * 32, ra);
-        body(rb, cc + 1);
-        if (cc + 2 < nch) {
-          ptx::tmem_ld_wait();
-          ptx::tmem_pin16(ra);
-        }
-      }
-      if (p.tile_max) {
-#pragma unroll
-        for (int hi = 0; hi < 2; ++hi) {
-          mx[hi] = fmaxf(mx[hi], __shfl_xor_sync(0xffffffffu, mx[hi], 1));
-          mx[hi] = fmaxf(mx[hi], __shfl_xor_sync(0xffffffffu, mx[hi], 2));
-          if ((lane & 3) == 0 && rows[hi] < g.M) p.tile_max[int64_t(nb) * p.ld_stats + rows[hi]] = mx[hi];
-        }
-      }
-    }
-  }
   __device__ static Pre prepare(const Params& p, const GemmGeom& g, int row, int /*tile_col0*/) {
     return Pre{(p.row_scale && row < g.M) ? p.row_scale[row] : 1.f};
   }
@@ -726,10 +656,6 @@ struct EpiStoreF32 {
     const bool add = p.accumulate != 0 || split_add;
     float mx = -INFINITY;
     const int row0 = row - int(threadIdx.x & 31);
-    if (p.use_tma == 2) {
-      store16(p, g, taddr, row, col0, nb, pre, add, nvalid);
-      return;
-    }
     if (p.use_tma) {
       tmem_chunks(taddr, nch, [&](uint32_t (&r)[32], int c) {
         if (p.row_scale) {

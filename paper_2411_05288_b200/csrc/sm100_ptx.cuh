@@ -279,26 +279,6 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
         "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
       : "r"(taddr));
 }
-// 16 lanes x 4 x 256 bits (.16x256b.x4): thread t gets, for repetition k
-// (columns col + 8k .. +7): r[4k], r[4k+1] = lane (base + t/4), columns
-// 8k + 2(t%4), +1; r[4k+2], r[4k+3] = lane (base + t/4 + 8), same columns
-// (CUTLASS SM100_TMEM_LOAD_16dp256b1x layout).  Four threads hold 8
-// consecutive columns of a row: 32-byte coalesced fp32 stores.
-__device__ __forceinline__ void tmem_ld16x256_x4(uint32_t taddr, uint32_t (&r)[16]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.16x256b.x4.b32 "
-      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-      : "r"(taddr));
-}
-__device__ __forceinline__ void tmem_pin16(uint32_t (&r)[16]) {
-#pragma unroll
-  for (int j = 0; j < 16; ++j) asm volatile("" : "+r"(r[j]));
-}
-__device__ __forceinline__ void red_add_v2(float* addr, float a, float b) {
-  asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(addr), "f"(a), "f"(b) : "memory");
-}
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 // After tcgen05.wait::ld: re-define the destination registers at this point
 // so no use of them can be scheduled above the wait.

@@ -49,7 +49,6 @@ int main(int argc, char** argv) {
   const int64_t T = 8192, h = 4096, V = argc > 6 ? atoll(argv[6]) : 256000;
   int nsm = 0;
   if (getenv("VP_TMA_STORE")) vp::g_tma_store = atoi(getenv("VP_TMA_STORE"));
-  if (getenv("VP_F32_STORE")) vp::g_f32_store_mode = atoi(getenv("VP_F32_STORE"));
   CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0));
   __nv_bfloat16 *X, *W, *P;
   float* out;

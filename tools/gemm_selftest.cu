@@ -270,7 +270,6 @@ static void bench_stats(int cg, int M, int N, int K, int nsm) {
 int main(int argc, char** argv) {
   int nsm = 0;
   if (getenv("VP_TMA_STORE")) vp::g_tma_store = atoi(getenv("VP_TMA_STORE"));
-  if (getenv("VP_F32_STORE")) vp::g_f32_store_mode = atoi(getenv("VP_F32_STORE"));
   CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0));
   const bool do_bench = argc > 1 && std::string(argv[1]) == "bench";
   if (argc > 1 && std::string(argv[1]) == "one") {  // one 8192^3 GEMM: one <cg>
