@@ -11,5 +11,5 @@ timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
   python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > /dev/null 2>&1; echo launches_rc=$?
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:gemm_sm100 -s 3 -c 3 \
   -o gpurun_out/${R}_gemms python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-graph --opt cooperative=0 > gpurun_out/${R}_ncu.log 2>&1; echo ncu_rc=$?
-timeout 300 ncu --set full --clock-control none --import-source on -k regex:"k_input_forward|k_segment_scatter" -s 6 -c 2 \
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:"k_input_forward|k_scatter_rows" -s 6 -c 2 \
   -o gpurun_out/${R}_input python bench.py --workload input --steps 1 --warmup 3 --no-e2e > gpurun_out/${R}_ncu_input.log 2>&1; echo ncu_input_rc=$?
