@@ -322,6 +322,8 @@ float* global_scale(vp_ctx_s* c, const vp_state_s* st, vp_stats_t g) {
   return sc;
 }
 
+int g_scatter_threads = 256;  // threads per block of k_scatter_rows (option "scatter_threads"; 64/128/256 measured equal)
+
 // dst[row] (+)= sign * src[i] over owned tokens, ascending i per row
 // (sort-free: row heads + multiplicities, then one warp per row head).
 template <typename Src>
@@ -335,7 +337,7 @@ void segment_scatter(vp_ctx_s* c, const int64_t* tok, int64_t n, int64_t rb, int
   VP_CUDA(cudaMemsetAsync(cnt, 0, size_t(rows) * sizeof(int), c->stream));
   vp::k_row_heads<<<c->grid_for(n, 256), 256, 0, c->stream>>>(tok, int(n), rb, re, head, cnt, c->d_err, err_bit);
   VP_KCHECK();
-  vp::k_scatter_rows<Src><<<unsigned(n), 256, 0, c->stream>>>(
+  vp::k_scatter_rows<Src><<<unsigned(n), g_scatter_threads, 0, c->stream>>>(
       tok, int(n), rb, re, head, cnt, src, lds, int(h), sign, dst, ldd, accumulate);
   VP_KCHECK();
   c->launches += 2;
@@ -987,6 +989,9 @@ int vp_ctx_set_option(vp_ctx_t c, const char* key, int64_t value) {
     } else if (k == "lockstep_logits" || k == "lockstep_dx" || k == "lockstep_dw") {
       require(value >= 0 && value <= 4096, "vp_ctx_set_option: lockstep epoch must be in 0..4096 k-blocks");
       c->lock_epoch[k == "lockstep_logits" ? 0 : k == "lockstep_dx" ? 1 : 2] = int(value);
+    } else if (k == "scatter_threads") {
+      require(value == 64 || value == 128 || value == 256, "vp_ctx_set_option: scatter_threads must be 64, 128 or 256");
+      g_scatter_threads = int(value);
     } else if (k == "cooperative") {
       require(value == 0 || value == 1, "vp_ctx_set_option: cooperative must be 0 or 1");
       vp::g_cooperative = int(value);

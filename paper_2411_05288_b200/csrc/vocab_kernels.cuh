@@ -528,11 +528,12 @@ __device__ __forceinline__ void scatter_row(const int64_t* __restrict__ tok, int
   if (c_tot == 1) {
     const Src* sp = src + int64_t(i) * lds;
     // four passes' loads in flight before any store (memory-level parallelism)
-    for (int c0 = threadIdx.x * 4; c0 < h; c0 += 4096) {
+    const int pass = int(blockDim.x) * 4;  // columns per pass
+    for (int c0 = threadIdx.x * 4; c0 < h; c0 += 4 * pass) {
       float4 acc[4], v[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const int c = c0 + u * 1024;
+        const int c = c0 + u * pass;
         if (c < h) {
           acc[u] = accumulate ? *reinterpret_cast<const float4*>(d + c) : make_float4(0.f, 0.f, 0.f, 0.f);
           v[u] = load4(sp + c);
@@ -540,7 +541,7 @@ __device__ __forceinline__ void scatter_row(const int64_t* __restrict__ tok, int
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const int c = c0 + u * 1024;
+        const int c = c0 + u * pass;
         if (c < h) {
           acc[u].x += sign * v[u].x;
           acc[u].y += sign * v[u].y;
@@ -585,7 +586,7 @@ __device__ __forceinline__ void scatter_row(const int64_t* __restrict__ tok, int
     __syncthreads();
     const int m = s_m;
     if (m == 0) break;  // (counts and ids disagree: cannot happen)
-    for (int c = threadIdx.x * 4; c < h; c += 1024) {
+    for (int c = threadIdx.x * 4; c < h; c += int(blockDim.x) * 4) {
       float4 acc = (first && !accumulate) ? make_float4(0.f, 0.f, 0.f, 0.f) : *reinterpret_cast<const float4*>(d + c);
       for (int q = 0; q < m; ++q) {
         const float4 v = load4(src + int64_t(list[q]) * lds + c);
