@@ -298,7 +298,7 @@ def run_ours(args):
 
     # ---- the same step replayed as a CUDA graph (reported beside value) ----
     graph = None
-    if not args.no_graph:
+    if not args.no_graph and world == 1:  # (multi-rank graph capture of NCCL calls: not exercised this round)
         try:
             g = vm.capture(ctx, step)
             for _ in range(args.warmup):
