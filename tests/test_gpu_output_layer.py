@@ -396,3 +396,16 @@ def test_gemm_schedule_options_do_not_change_results(ctx):
             assert np.array_equal(res[key], base[key]), (opts, key)
         octx.close()
     vm.Context(0).set_option("store_evict_first", 0)  # process-wide option: restore
+
+
+@pytest.mark.parametrize("T", [1, 3, 129])
+def test_tiny_and_ragged_token_counts(ctx, T):
+    # one token, a few tokens, one past a 128-row block: every GEMM has a
+    # single partial M tile (and the wave lockstep / split machinery sees one wave)
+    X, W, g = oracle.random_instance(T, 64, 600, 17)
+    Xb, Wb, batch, Wd = device_case(X, W, g)
+    ref = oracle.oracle_output_layer(Xb, g, Wb)
+    for alg in ALGS:
+        for p in (1, 2):
+            res, _ = run_device(ctx, alg, batch, Wd, p, 64)
+            assert_parity(res, ref, f"T={T} {alg} p={p}")
