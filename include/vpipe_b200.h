@@ -96,7 +96,9 @@ int vp_ctx_reserve(vp_ctx_t ctx, int64_t n_tok, int64_t h, int p);
  * "overlap_c1" (1 = vp_run_alg2 overlaps the dX / loss all-reduce with pass T
  * on a high-priority comm stream; default 1), "comm_sms" (SMs left to NCCL
  * during the overlap and NCCL's maxCTAs; set before vp_ctx_comm_init),
- * "epi_wait" (GEMM epilogue wait: 0 try_wait loop, 1 nanosleep backoff),
+ * "epi_wait" (GEMM epilogue wait: 0 try_wait loop, 1 nanosleep backoff;
+ * process-wide), "store_evict_first" (1 = epilogue TMA stores with an L2
+ * evict-first hint; default 0; process-wide),
  * "lockstep_logits" / "lockstep_dx" / "lockstep_dw" (wave lockstep of the
  * persistent GEMM's clusters every N k-blocks so co-scheduled tiles share
  * operand bands in L2; 0 = off; default 8 for all three),
