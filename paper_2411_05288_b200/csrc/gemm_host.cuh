@@ -30,6 +30,8 @@ inline PFN_encodeTiled get_encode_fn() {
   return fn;
 }
 
+inline int g_l2_promotion = 3;  // operand tensor maps: 0 none, 1 64 B, 2 128 B, 3 256 B (default)
+
 // 2-D bf16 tensor map over a row-major [outer x inner] matrix with leading
 // dimension `ld` (elements), SWIZZLE_128B boxes of [box_outer x box_inner].
 // Out-of-bounds elements of a box read as zero.
@@ -44,7 +46,11 @@ inline CUtensorMap make_tmap_bf16(const void* ptr, uint64_t inner, uint64_t oute
   const cuuint32_t estr[2] = {1, 1};
   CUresult r = get_encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box,
                                estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                               g_l2_promotion == 0   ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                               : g_l2_promotion == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                               : g_l2_promotion == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                                                     : CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed: " + std::to_string(int(r)));
   return m;
 }

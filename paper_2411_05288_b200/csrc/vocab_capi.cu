@@ -992,6 +992,9 @@ int vp_ctx_set_option(vp_ctx_t c, const char* key, int64_t value) {
     } else if (k == "scatter_threads") {
       require(value == 64 || value == 128 || value == 256, "vp_ctx_set_option: scatter_threads must be 64, 128 or 256");
       g_scatter_threads = int(value);
+    } else if (k == "l2_promotion") {
+      require(value >= 0 && value <= 3, "vp_ctx_set_option: l2_promotion must be 0..3");
+      vp::g_l2_promotion = int(value);
     } else if (k == "cooperative") {
       require(value == 0 || value == 1, "vp_ctx_set_option: cooperative must be 0 or 1");
       vp::g_cooperative = int(value);

@@ -1,0 +1,6 @@
+#!/bin/bash
+B="python bench.py --no-cpu-baseline --no-e2e --no-graph --steps 10 --warmup 3"
+for rep in 1 2 3; do for cfg in "" "--opt l2_promotion=2" "--opt l2_promotion=0"; do
+  out=$(timeout 200 $B $cfg 2>/dev/null)
+  echo "$out" | python -c "import json,sys; d=json.loads(sys.stdin.read()); g=d['roofline']['gemms']; print('%-26s %8.0f tok/s %6.3f ms | logits %.3f dx %.3f dw %.3f | clk %s' % ('$cfg' or 'default', d['value'], d['ms_per_step'], g['logits']['avg_ms'], g['dx']['avg_ms'], g['dw']['avg_ms'], d['clocks']['sm_mhz']))"
+done; done
