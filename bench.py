@@ -448,6 +448,9 @@ def run_input(args):
     row_begin, row_end = vpd.shard_rows(V, world, rank)
     rows = row_end - row_begin
     ctx = vm.Context(local)
+    for kv in args.opt:
+        key, val = kv.split("=")
+        ctx.set_option(key, int(val))
     if world > 1:
         vpd.init_comm(ctx)
     gen = torch.Generator(device="cuda").manual_seed(1234)
