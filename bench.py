@@ -13,6 +13,8 @@ them); total work is fixed as N grows ("strong" scaling).
   python bench.py [--gpus N --steps K --warmup W]          # our sm_100a path
   python bench.py --impl reference [...]                    # reference CPU path
   torchrun --nproc-per-node N bench.py --gpus N [...]       # N > 1
+  torchrun --nproc-per-node N bench.py --gpus N --dry-run   # N ranks on the visible GPU(s):
+                                                            # loopback collectives, same code path
 
 Prints ONE JSON line on rank 0.
 """
@@ -54,6 +56,12 @@ def parse():
     ap.add_argument("--cpu-sample-vocab", type=int, default=64000)
     ap.add_argument("--opt", action="append", default=[],
                     help="library option key=value (vp_ctx_set_option), e.g. raster_dx=16")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="N>1 without N GPUs: ranks share the visible GPU(s) (round-robin) and exchange through the "
+                         "library's loopback backend (CUDA IPC mailboxes) instead of NCCL; torch.distributed runs on "
+                         "gloo.  Exercises the whole multi-rank path; the timing is not a scaling number.")
+    ap.add_argument("--ids", choices=["uniform", "zipf"], default="uniform",
+                    help="input workload: token-id distribution (zipf: s=1.1 over the vocabulary)")
     return ap.parse_args()
 
 
@@ -165,22 +173,45 @@ def cpu_reference_sample(T_s: int, h: int, V_s: int, p: int, reps: int = 1):
     return times, oracle.num_threads()
 
 
+def host_info():
+    """Host cores the CPU legs ran on (nproc, model name from lscpu)."""
+    info = {"nproc": os.cpu_count()}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            k, _, v = ln.partition(":")
+            if k.strip() in ("Model name", "Socket(s)", "Core(s) per socket", "Thread(s) per core", "CPU(s)"):
+                info[k.strip()] = v.strip()
+    except Exception:
+        pass
+    return info
+
+
+def cpu_sample_shape(args, V):
+    """The bounded CPU sample both CPU legs (--impl reference and cpu_baseline)
+    time: the same T_s tokens x V_s vocab rows, so the two agree."""
+    T_s, V_s = args.cpu_sample_tokens, min(args.cpu_sample_vocab, V)
+    p = max(1, args.gpus)
+    while V_s % p:
+        V_s -= 1
+    return T_s, V_s, p
+
+
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return  # rank 0 alone runs the CPU reference
     T, h, V = args.tokens, args.hidden, args.vocab
-    T_s, V_s = 16, min(args.cpu_sample_vocab, V)
-    p = max(1, args.gpus)
-    while V_s % p:
-        V_s -= 1
+    if args.workload == "input":
+        return run_reference_input(args)
+    T_s, V_s, p = cpu_sample_shape(args, V)
     times, cores = cpu_reference_sample(T_s, h, V_s, p, reps=args.warmup + args.steps)
     timed = times[args.warmup:]
     t = sum(timed) / len(timed)
     scale = V / V_s  # cost is linear in V (three T x h x V GEMMs + T x V elementwise)
     value = T_s / (t * scale)
     sample = (f"run_alg2 (fp64 CPU oracle restating VM.cpp:328-361) on {T_s} tokens x {V_s} of {V} vocab rows, "
-              f"h={h}, p={p}; tokens/s scaled by {V_s}/{V} (cost linear in V)")
+              f"h={h}, p={p}; tokens/s scaled by {V_s}/{V} (cost linear in V); host {host_info()}")
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
@@ -226,6 +257,22 @@ class Step:
             check(rc)
 
 
+def setup_rank(args, world, local):
+    """This rank's GPU and process group: NCCL, one GPU per rank (the real
+    run), or --dry-run: ranks round-robin over the visible GPUs, gloo for
+    torch.distributed and the library's loopback backend for the data path."""
+    import torch
+    import torch.distributed as dist
+    dev = local % torch.cuda.device_count() if args.dry_run else local
+    torch.cuda.set_device(dev)
+    if world > 1:
+        if args.dry_run:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return dev
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -236,21 +283,19 @@ def run_ours(args):
     rank, world, local = vpd.env()
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
-    torch.cuda.set_device(local)
+    dev = setup_rank(args, world, local)
     # a side stream as the current stream: the library runs on it, and it can
     # be captured into a CUDA graph (the legacy default stream cannot)
     torch.cuda.set_stream(torch.cuda.Stream())
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     T, h, V = args.tokens, args.hidden, args.vocab
     row_begin, row_end = vpd.shard_rows(vm.pad_vocab_size(V, world) if V % world else V, world, rank)
     rows = row_end - row_begin
-    ctx = vm.Context(local, cta_group=args.cta_group)
+    ctx = vm.Context(dev, cta_group=args.cta_group)
     for kv in args.opt:
         k, v = kv.split("=")
         ctx.set_option(k, int(v))
     if world > 1:
-        vpd.init_comm(ctx)
+        vpd.init_comm(ctx, loopback=args.dry_run)
     ctx.reserve(T, h, world)
 
     # synthetic inputs of the named shape (X~N(0,1), W~N(0,0.02^2), seed 1234)
@@ -268,15 +313,16 @@ def run_ours(args):
     stream = torch.cuda.current_stream()
 
     def barrier():
+        torch.cuda.synchronize()
         if world > 1:
-            dist.barrier(device_ids=[local])
+            dist.barrier() if args.dry_run else dist.barrier(device_ids=[local])
         torch.cuda.synchronize()
 
     def max_over_ranks(x: float) -> float:
-        return vpd.max_over_ranks(x, device="cuda")
+        return vpd.max_over_ranks(x, device=None if args.dry_run else "cuda")
 
     # ---- device-resident throughput (value) ----
-    clk = ClockSampler(local)
+    clk = ClockSampler(dev)
     for _ in range(args.warmup):
         step()
     barrier()
@@ -400,11 +446,13 @@ def run_ours(args):
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        T_s, V_s = args.cpu_sample_tokens, min(args.cpu_sample_vocab, V)
-        times, cores = cpu_reference_sample(T_s, h, V_s, 1)
-        cpu = {"value": T_s / (times[0] * V / V_s), "unit": "tokens/s", "cores": cores, "kind": "port",
+        T_s, V_s, p_s = cpu_sample_shape(args, V)  # the --impl reference arm's sample
+        times, cores = cpu_reference_sample(T_s, h, V_s, p_s, reps=3)
+        t_s = statistics.mean(times[1:])
+        cpu = {"value": T_s / (t_s * V / V_s), "unit": "tokens/s", "cores": cores, "kind": "port",
                "sample": (f"CPU oracle run_alg2 (fp64, restates VM.cpp:328-361) on {T_s} tokens x {V_s} of {V} "
-                          f"vocab rows, h={h}, {times[0]:.1f} s; tokens/s scaled by {V_s}/{V}")}
+                          f"vocab rows, h={h}, p={p_s}, mean of 2 after 1 warm-up: {t_s:.1f} s; tokens/s scaled by {V_s}/{V} "
+                          f"(the --impl reference arm's sample); host {host_info()}")}
 
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
@@ -419,20 +467,84 @@ def run_ours(args):
             "l2": "inputs larger than L2 every step (W_k %.0f MB, P %.0f MB per GPU)" % (
                 rows * h * 2 / 1e6, T * rows * 2 / 1e6)},
         "e2e": e2e, "graph": graph, "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu,
-        "clocks": clk.summary(),
+        "clocks": clk.summary(), "comm": ctx.comm_backend,
     }
+    if args.dry_run:
+        line["dry_run"] = ("N ranks shared %d visible GPU(s) through the loopback backend: a functional run of the "
+                           "multi-rank path, not a scaling measurement" % torch.cuda.device_count())
     print(json.dumps(line), flush=True)
     ctx.close()
     if world > 1:
         dist.destroy_process_group()
 
 
+def input_ids(T, V, kind, gen):
+    """Token ids of the input workload: uniform, or Zipf(s=1.1) over the
+    vocabulary (rank k drawn with p ~ 1/k^1.1; ranks mapped to ids by a fixed
+    random permutation, so hot rows land on every shard)."""
+    import torch
+    if kind == "uniform":
+        return torch.randint(0, V, (T,), device="cuda", generator=gen)
+    k = torch.arange(1, V + 1, device="cuda", dtype=torch.float64)
+    probs = (1.0 / k.pow(1.1)).float()
+    ranks = torch.multinomial(probs, T, replacement=True, generator=gen)
+    perm = torch.randperm(V, device="cuda", generator=gen)
+    return perm[ranks]
+
+
+def cpu_input_sample(T, V, h):
+    """The reference's input layer (oracle input_forward + input_backward, fp64,
+    VM.cpp:227-251) on a T_s-token x V_s-row sample with the workload's
+    tokens-per-row density (cost per token then transfers); returns
+    (tokens/s, sample description, threads)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import numpy as np
+
+    import oracle
+    V_s = min(V, 16000)
+    T_s = max(1, round(T * V_s / V))
+    rng = np.random.default_rng(1234)
+    tok = rng.integers(0, V_s, T_s)
+    W = rng.standard_normal((V_s, h)) * 0.02
+    grad = rng.standard_normal((T_s, h))
+    times = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        oracle.input_forward(tok, W, 0)
+        oracle.input_backward(grad, tok, V_s, 0)
+        times.append(time.perf_counter() - t0)
+    t = statistics.mean(times[1:])
+    return T_s / t, (f"oracle input_forward + input_backward (fp64, VM.cpp:227-251) on {T_s} ids over {V_s} rows "
+                     f"(the workload's ids/row density {T / V:.3f}), h={h}, mean of 2 after 1 warm-up: {t:.2f} s; "
+                     f"host {host_info()}"), 1
+
+
+def run_reference_input(args):
+    T = args.tokens if args.tokens != 8192 else 16384
+    h, V = args.hidden, args.vocab
+    vals = []
+    for _ in range(max(1, args.steps)):
+        v, sample, cores = cpu_input_sample(T, V, h)
+        vals.append(v)
+    value = statistics.mean(vals)
+    line = {"metric": "input-layer fwd+bwd tokens/s at V=256k,h=4096 (BASELINE configs[3])", "value": value,
+            "unit": "tokens/s", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": T / value * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": {"workload": "reference CPU path: vocab-parallel input embedding", "tokens": T, "hidden": h,
+                       "vocab": V},
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "port", "sample": sample},
+            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "gpu_launches": 0}
+    print(json.dumps(line), flush=True)
+
+
 def run_input(args):
     """BASELINE configs[3]: V=256000, h=4096, 16384 token ids.  One step =
     input_forward of this rank's shard (masked 16-byte-vector gather) + the
-    sum all-reduce across ranks (NCCL) + input_backward (deterministic
-    sort + ordered segmented scatter-add, accumulated into the rank's
-    embedding-gradient buffer as in training)."""
+    sum all-reduce across ranks + input_backward (deterministic ascending-i
+    scatter-add, accumulated into the rank's embedding-gradient buffer as in
+    training)."""
     import torch
     import torch.distributed as dist
 
@@ -440,21 +552,19 @@ def run_input(args):
     from paper_2411_05288_b200 import vocab_math as vm
 
     rank, world, local = vpd.env()
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = setup_rank(args, world, local)
     T = args.tokens if args.tokens != 8192 else 16384
     h, V = args.hidden, args.vocab
     row_begin, row_end = vpd.shard_rows(V, world, rank)
     rows = row_end - row_begin
-    ctx = vm.Context(local)
+    ctx = vm.Context(dev)
     for kv in args.opt:
         key, val = kv.split("=")
         ctx.set_option(key, int(val))
     if world > 1:
-        vpd.init_comm(ctx)
+        vpd.init_comm(ctx, loopback=args.dry_run)
     gen = torch.Generator(device="cuda").manual_seed(1234)
-    tok = torch.randint(0, V, (T,), device="cuda", generator=gen)
+    tok = input_ids(T, V, args.ids, gen)
     grad = torch.randn(T, h, device="cuda", generator=gen).to(torch.bfloat16)
     gen.manual_seed(1235 + rank)
     W_k = (torch.randn(rows, h, device="cuda", generator=gen) * 0.02).to(torch.bfloat16)
@@ -464,6 +574,15 @@ def run_input(args):
     stream = torch.cuda.current_stream()
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
     fwd_ms, bwd_ms = [], []
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier() if args.dry_run else dist.barrier(device_ids=[local])
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        return vpd.max_over_ranks(x, device=None if args.dry_run else "cuda")
 
     def step(timed=False):
         if timed:
@@ -481,16 +600,15 @@ def run_input(args):
     ctx.sync()
     launches0 = ctx.launches
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier(device_ids=[local])
+    clk = ClockSampler(dev)
+    with clk:
+        barrier()
         e0.record(stream)
         for _ in range(args.steps):
             step()
         e1.record(stream)
-        torch.cuda.synchronize()
-    ms = vpd.max_over_ranks(e0.elapsed_time(e1) / args.steps, device="cuda")
+        barrier()
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
     launches = ctx.launches - launches0
     for _ in range(3):  # per-phase split (separate, un-timed for the headline)
         step(timed=True)
@@ -500,31 +618,51 @@ def run_input(args):
     ctx.sync()
     e2e = None
     if not args.no_e2e:
+        # ids + grad_out from pinned host memory every step, double-buffered on
+        # a copy stream (step i+1's copies overlap step i, as a training loop's
+        # prefetch does); one embedding row read back per step
         tok_h = tok.cpu().pin_memory()
         grad_h = grad.cpu().pin_memory()
         out_h = torch.empty(h, dtype=torch.bfloat16).pin_memory()
-        tok_d, grad_d = torch.empty_like(tok), torch.empty_like(grad)
+        copy_stream = torch.cuda.Stream()
+        bufs = [(torch.empty_like(tok), torch.empty_like(grad)) for _ in range(2)]
+        ready = [torch.cuda.Event() for _ in range(2)]
+        consumed = [torch.cuda.Event() for _ in range(2)]
 
-        def e2e_step():
-            tok_d.copy_(tok_h, non_blocking=True)
-            grad_d.copy_(grad_h, non_blocking=True)
-            vm.input_forward(ctx, tok_d, shard, out=emb)
-            vm.allreduce_sum(ctx, emb)
-            vm.input_backward(ctx, grad_d, tok_d, shard, out=dE, accumulate=True)
-            out_h.copy_(emb[0], non_blocking=True)
+        def issue_copy(i):
+            b = i % 2
+            copy_stream.wait_event(consumed[b])
+            with torch.cuda.stream(copy_stream):
+                bufs[b][0].copy_(tok_h, non_blocking=True)
+                bufs[b][1].copy_(grad_h, non_blocking=True)
+            ready[b].record(copy_stream)
 
-        for _ in range(args.warmup):
-            e2e_step()
-        torch.cuda.synchronize()
+        def e2e_steps(n):
+            copy_stream.wait_event(e0)
+            issue_copy(0)
+            for i in range(n):
+                if i + 1 < n:
+                    issue_copy(i + 1)
+                b = i % 2
+                stream.wait_event(ready[b])
+                vm.input_forward(ctx, bufs[b][0], shard, out=emb)
+                vm.allreduce_sum(ctx, emb)
+                vm.input_backward(ctx, bufs[b][1], bufs[b][0], shard, out=dE, accumulate=True)
+                consumed[b].record(stream)
+                out_h.copy_(emb[0], non_blocking=True)
+
         e0.record(stream)
-        for _ in range(args.steps):
-            e2e_step()
+        e2e_steps(args.warmup)
+        barrier()
+        e0.record(stream)
+        e2e_steps(args.steps)
         e1.record(stream)
-        torch.cuda.synchronize()
-        me = vpd.max_over_ranks(e0.elapsed_time(e1) / args.steps, device="cuda")
+        barrier()
+        me = max_over_ranks(e0.elapsed_time(e1) / args.steps)
         e2e = {"value": T / (me / 1e3), "unit": "tokens/s", "ms_per_step": me,
                "h2d_bytes_per_step": tok_h.numel() * 8 + grad_h.numel() * 2, "d2h_bytes_per_step": h * 2,
-               "path": "vp_input_forward / vp_allreduce_sum / vp_input_backward via ctypes; ids + grad from pinned host"}
+               "path": "vp_input_forward / vp_allreduce_sum / vp_input_backward via ctypes; ids + grad from pinned "
+                       "host (double-buffered on a copy stream, overlapping the previous step)"}
     if rank != 0:
         ctx.close()
         if world > 1:
@@ -532,19 +670,25 @@ def run_input(args):
         return
     peaks = measured_peaks()
     hbm = peaks.get("hbm_gbs") if peaks else 6650.0
-    owned = T / world
-    fwd_bytes = 8 * T + 2 * h * owned + 2 * h * T        # ids, owned rows read, full [T x h] written
-    bwd_bytes = 8 * T + 2 * h * owned + 8 * h * owned    # ids, owned grad rows, fp32 dE row RMW
+    owned_ids = int(((tok >= row_begin) & (tok < row_end)).sum().item())
+    owned_rows = int(torch.unique(tok[(tok >= row_begin) & (tok < row_end)]).numel())
+    fwd_bytes = 8 * T + 2 * h * owned_ids + 2 * h * T            # ids, owned rows read, full [T x h] written
+    bwd_bytes = 8 * T + 2 * h * owned_ids + 8 * h * owned_rows   # ids, owned grad rows, fp32 dE row RMW
     f_ms, b_ms = statistics.median(fwd_ms), statistics.median(bwd_ms)
     dom = "input_forward" if f_ms >= b_ms else "input_backward"
     achieved = (fwd_bytes / (f_ms / 1e3) if dom == "input_forward" else bwd_bytes / (b_ms / 1e3)) / 1e9
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        v, sample, cores = cpu_input_sample(T, V, h)
+        cpu = {"value": v, "unit": "tokens/s", "cores": cores, "kind": "port", "sample": sample}
     line = {
         "metric": "input-layer fwd+bwd tokens/s at V=256k,h=4096 (BASELINE configs[3])", "value": T / (ms / 1e3),
         "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
-        "data": "synthetic (uniform ids, W~N(0,0.02^2), grad~N(0,1), seed 1234)",
+        "data": f"synthetic ({args.ids} ids, W~N(0,0.02^2), grad~N(0,1), seed 1234)",
         "config": {"workload": "vocab-parallel input embedding: masked gather + all-reduce fwd, deterministic "
                                "scatter-add bwd (accumulating)", "tokens": T, "hidden": h, "vocab": V,
+                   "ids": args.ids, "owned_ids": owned_ids, "distinct_rows": owned_rows,
                    "vocab_rows_per_gpu": rows, "parallelism": f"vocab{world}"},
         "e2e": e2e, "gpu_launches": launches,
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
@@ -552,7 +696,7 @@ def run_input(args):
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback",
                      "phase_ms": {"forward+allreduce": f_ms, "backward": b_ms},
                      "bytes_per_launch": {"input_forward": fwd_bytes, "input_backward": bwd_bytes}},
-        "cpu_baseline": None, "clocks": clk.summary(),
+        "cpu_baseline": cpu, "clocks": clk.summary(), "comm": ctx.comm_backend,
     }
     print(json.dumps(line), flush=True)
     ctx.close()

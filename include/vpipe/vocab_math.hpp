@@ -119,8 +119,10 @@ struct ShardState {
   std::shared_ptr<detail::DeviceState> dev;
 
   // On-demand materialisations of the reference's fields.
+  Matrix Y() const;              // local logits [n_tok x V/p] (recomputed: one GEMM)
   Matrix softmax_local() const;  // [n_tok x V/p], rows sum to 1
   Matrix A() const;              // [n_tok x h] (alg2 only)
+  Matrix B() const;              // G_k W_k [n_tok x h] (alg2 only)
 };
 
 struct GlobalStats {  // VM.hpp:45-48
@@ -146,8 +148,8 @@ struct ShardGrads {  // VM.hpp:63-66
 };
 
 // Monolithic output layer (VM.hpp:68-74): on the device this is the p = 1
-// Algorithm-2 path.  logit_shift is a CPU-oracle test hook; passing one
-// throws std::invalid_argument (the device path has no logit injection).
+// Algorithm-2 path.  logit_shift (VM.cpp:41-43) is added per row to the
+// logits inside the K1 epilogue (vp_ctx_set_logit_shift).
 OutputResult oracle_output_layer(const TokenBatch& batch, const Matrix& W, const Vector* logit_shift = nullptr);
 
 std::vector<EmbeddingShard> shard_weights(const Matrix& W, int p);
@@ -184,6 +186,18 @@ struct RandomInstance {  // VM.hpp:125-128
 
 // Bit-identical to the reference generator (VM.cpp:253-270).
 RandomInstance random_instance(std::int64_t n_tok, std::int64_t h, std::int64_t V, std::uint64_t seed);
+
+// Where run_naive / run_alg1 / run_alg2 place their p shards (an extension;
+// env VPIPE_PLACEMENT=auto|local|spread|loopback sets the initial value):
+//   Local    all p shards on one GPU (VPIPE_DEVICE, default 0), one context;
+//   Spread   shard k on GPU k, one context per GPU joined by NCCL, each rank
+//            driven from its own host thread (the reference's p devices);
+//   Loopback p contexts on one GPU joined by the loopback backend (the
+//            multi-rank code paths on a single GPU);
+//   Auto     Spread when p <= visible GPUs (and p > 1), else Local.
+enum class Placement { Auto, Local, Spread, Loopback };
+void set_placement(Placement p);
+Placement placement();
 
 OutputResult run_naive(const TokenBatch& batch, const Matrix& W, int p);
 OutputResult run_alg1(const TokenBatch& batch, const Matrix& W, int p, double fault_scale = 1.0);

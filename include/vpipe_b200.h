@@ -19,8 +19,10 @@
  *     workspace.
  *   - Return codes: VP_OK, VP_EINVAL (the reference's std::invalid_argument,
  *     same message text, retrievable with vp_last_error()), VP_ECUDA,
- *     VP_ENCCL.  Errors found on the device (negative token ids, VM.cpp:232,
- *     :247) are reported by the next vp_ctx_sync() as VP_EINVAL.
+ *     VP_ENCCL (collective backend, NCCL or loopback).  Errors found on the
+ *     device (negative token ids, VM.cpp:232, :247; labels outside [0, V),
+ *     VM.cpp:18, checked by the loss, C1 and naive kernels, negative labels
+ *     also by pass T) are reported by the next vp_ctx_sync() as VP_EINVAL.
  *   - Sharding: shard k owns vocab rows [row_begin, row_end) (VM.cpp:65-80).
  *     A context either drives several shards on ONE device (functions take
  *     arrays of n shard states; the reference's in-process "collectives"
@@ -113,10 +115,17 @@ int vp_ctx_reserve(vp_ctx_t ctx, int64_t n_tok, int64_t h, int p);
  * scatter-add; default 256; process-wide),
  * "tma_store" (1 = GEMM epilogues store through smem staging + TMA, the
  * default; 0 = per-thread st.global; process-wide),
+ * "debug_logit_scale_ppm" (fault injection for verification tools: pass-S
+ * logits scaled by 1 + ppm * 1e-6; 0 = off),
  * "accumulate_grad_w" (1 = the T passes add dW_k into grad_w: gradient
  * accumulation, or tied input/output embeddings sharing the shard's buffer
  * with vp_input_backward(accumulate=1); R/PAPER.md:333). */
 int vp_ctx_set_option(vp_ctx_t ctx, const char* key, int64_t value);
+/* The reference's per-row logit_shift test hook (VM.cpp:41-43,
+ * oracle_output_layer's `logit_shift`): subsequent pass-S logits are
+ * Y[i, :] + shift[i] (device fp32 [n_tok], kept by pointer; NULL clears it).
+ * Softmax, loss and gradients are shift-invariant (test_vocab_math.cpp:74-84). */
+int vp_ctx_set_logit_shift(vp_ctx_t ctx, const float* shift);
 /* Number of kernels this context has launched (evidence counter). */
 int64_t vp_ctx_launch_count(vp_ctx_t ctx);
 /* Per-GEMM CUDA-event timing on the launching stream.  Returns (and resets)
@@ -125,10 +134,28 @@ int64_t vp_ctx_launch_count(vp_ctx_t ctx);
  * [3] dW (K4) — then enables (enable=1) or disables timing.  Synchronises. */
 int vp_ctx_gemm_timing(vp_ctx_t ctx, int enable, double* ms_out4, int64_t* count_out4);
 
-/* NCCL group: rank 0 creates the id, every rank calls comm_init with it. */
+/* Collective group of a context (one shard per rank).  Rank 0 creates an id,
+ * every rank calls vp_ctx_comm_init with it (the id travels by the caller's
+ * own bootstrap: torch.distributed, MPI, a file).
+ *   vp_comm_unique_id    NCCL (ncclGetUniqueId): production, one rank per GPU.
+ *   vp_comm_loopback_id  loopback backend: ranks may share one GPU (threads
+ *                        of one process or processes of one node); device
+ *                        mailboxes + a host rendezvous.  It runs every
+ *                        nranks > 1 code path of the library on a single GPU.
+ *                        Not capturable into CUDA graphs.  Ranks sharing a
+ *                        GPU split its SMs for the persistent GEMMs.
+ * vp_ctx_comm_init dispatches on the kind of id. */
 int vp_comm_unique_id(void* id128);
+int vp_comm_loopback_id(void* id128);
 int vp_ctx_comm_init(vp_ctx_t ctx, int nranks, int rank, const void* id128);
+/* One process driving n contexts (ctxs[k] becomes rank k; drive each rank
+ * from its own host thread afterwards).  Distinct devices: NCCL, all ranks
+ * initialised from this thread in one group (ncclCommInitAll's pattern);
+ * contexts sharing a device: the loopback backend. */
+int vp_comm_init_all(vp_ctx_t* ctxs, int n);
 int vp_ctx_comm_info(vp_ctx_t ctx, int* nranks, int* rank);
+/* "nccl", "loopback" or "none". */
+const char* vp_ctx_comm_backend(vp_ctx_t ctx);
 
 /* ---- shard state (ShardState, VM.hpp:34-43) ----------------------------- */
 /* Device buffers for one shard: P = exp(Y - m_tile) in bf16 [n_tok x rows]
@@ -180,6 +207,12 @@ int vp_output_loss(vp_ctx_t ctx, const vp_state_t* states, const vp_shard_t* sha
 /* softmax columns of one shard (assemble_forward, VM.cpp:281-286), fp32
  * [n_tok x rows] — parity/debug materialisation only. */
 int vp_shard_softmax(vp_ctx_t ctx, vp_state_t st, vp_stats_t stats, float* out, int64_t ldo);
+/* ShardState::Y (VM.hpp:35) on demand: fp32 logits X W_k^T [n_tok x rows]
+ * (one GEMM; pass S itself never stores them).  Debug / parity only. */
+int vp_shard_logits(vp_ctx_t ctx, const vp_batch_t* batch, const vp_shard_t* shard, float* out, int64_t ldo);
+/* ShardState::B (VM.hpp:41) on demand: B[i, :] = W_k[g_i - row_begin, :] for
+ * owned labels, else 0; fp32 [n_tok x h].  Debug / parity only. */
+int vp_shard_label_rows(vp_ctx_t ctx, const vp_batch_t* batch, const vp_shard_t* shard, float* out, int64_t ldo);
 /* naive_partitioned_output (VM.cpp:103-149): 3 barriers, stores and
  * re-reads fp32 logits. grad_w[k] is shard k's [rows_k x h] block. */
 int vp_naive_partitioned_output(vp_ctx_t ctx, const vp_batch_t* batch, const vp_shard_t* shards,

@@ -40,9 +40,15 @@ SIGNATURES = {
     "vp_ctx_reserve": (c_int, [c_void_p, c_int64, c_int64, c_int]),
     "vp_ctx_set_option": (c_int, [c_void_p, c_char_p, c_int64]),
     "vp_ctx_launch_count": (c_int64, [c_void_p]),
+    "vp_ctx_set_logit_shift": (c_int, [c_void_p, c_void_p]),
+    "vp_shard_logits": (c_int, [c_void_p, POINTER(vp_batch_t), POINTER(vp_shard_t), c_void_p, c_int64]),
+    "vp_shard_label_rows": (c_int, [c_void_p, POINTER(vp_batch_t), POINTER(vp_shard_t), c_void_p, c_int64]),
     "vp_ctx_gemm_timing": (c_int, [c_void_p, c_int, POINTER(ctypes.c_double), POINTER(c_int64)]),
     "vp_comm_unique_id": (c_int, [c_void_p]),
+    "vp_comm_loopback_id": (c_int, [c_void_p]),
     "vp_ctx_comm_init": (c_int, [c_void_p, c_int, c_int, c_void_p]),
+    "vp_comm_init_all": (c_int, [POINTER(c_void_p), c_int]),
+    "vp_ctx_comm_backend": (c_char_p, [c_void_p]),
     "vp_ctx_comm_info": (c_int, [c_void_p, POINTER(c_int), POINTER(c_int)]),
     "vp_state_create": (c_int, [c_void_p, c_int64, c_int64, c_int64, POINTER(c_void_p)]),
     "vp_state_destroy": (c_int, [c_void_p]),

@@ -784,6 +784,11 @@ struct EpiLogitStats {
     int2* fix_list;         // [ceil(M/32) x tiles_n]
     int use_tma = 0;        // P stored through `map` (bf16 [M x N], 32 x 32 boxes, SWIZZLE_64B)
     CUtensorMap map;
+    // logits y = acc * logit_scale + logit_shift[row]: the reference's per-row
+    // logit_shift test hook (VM.cpp:41-43; null = 0) and a fault-injection
+    // scale (1 = off).  Folded into the exponent: no extra pass.
+    const float* logit_shift = nullptr;
+    float logit_scale = 1.f;
   };
   // max of the valid columns and the label logit (first pass of a two-pass tile)
   __device__ static void scan(uint32_t taddr, int nvalid, int lb, float& mx, float& yt, bool& has_t) {
@@ -811,11 +816,13 @@ struct EpiLogitStats {
   // One pass over the 256 accumulator columns of this row: P = bf16(e^{Y - ref}),
   // s = sum e^{Y - ref}; with track = true it also takes the tile max and the
   // label logit (the single-pass path, where ref = r_i is known up front).
+  // ref and shift are in logit space (y = acc * logit_scale + shift); mx / yt
+  // are tracked in accumulator space.
   __device__ static void emit(const Params& p, uint32_t taddr, int row, bool row_ok, int col0, int nvalid,
-                              float ref, int lb, bool track, float& mx, float& yt, bool& has_t, float& sum,
-                              Stager& sg) {
-    constexpr float kLog2e = 1.4426950408889634f;
-    const float refs = ref * kLog2e;
+                              float ref, float shift, int lb, bool track, float& mx, float& yt, bool& has_t,
+                              float& sum, Stager& sg) {
+    const float kLog2e = 1.4426950408889634f * p.logit_scale;
+    const float refs = (ref - shift) * 1.4426950408889634f;
     sum = 0.f;
     const int row0 = row - int(threadIdx.x & 31);
     __nv_bfloat16* dst = p.P + int64_t(row) * p.ldp + col0;
@@ -947,6 +954,7 @@ struct EpiLogitStats {
     int64_t label;
     int flag;
     float ref;
+    float shift;
   };
   __device__ static int load_flag(const Params& p, int row) {
     int f;
@@ -954,9 +962,10 @@ struct EpiLogitStats {
     return f;
   }
   __device__ static Pre prepare(const Params& p, const GemmGeom& g, int row, int tile_col0) {
-    Pre r{-1, 0, 0.f};
+    Pre r{-1, 0, 0.f, 0.f};
     if (row < g.M) {
       if (p.labels) r.label = p.labels[row];
+      if (p.logit_shift) r.shift = p.logit_shift[row];
       if (tile_col0 != 0) {
         r.flag = load_flag(p, row);
         if (r.flag) r.ref = p.row_ref[row];
@@ -996,6 +1005,8 @@ struct EpiLogitStats {
       // two passes: this tile is its own reference (the j = 0 tile defines r_i;
       // an early tile whose row reference is not published yet falls back)
       scan(taddr, nvalid, lb, mx, yt, has_t);
+      mx = mx * p.logit_scale + pre.shift;  // accumulator -> logit space
+      yt = yt * p.logit_scale + pre.shift;
       ref = mx;
       if (nb == 0) {
         // r_i = first-tile max + kRefLift: later tiles overflow-check against
@@ -1012,19 +1023,21 @@ struct EpiLogitStats {
       } else {
         own = true;
       }
-      float m2;
-      emit(p, taddr, row, row_ok, col0, nvalid, ref, lb, false, m2, yt, has_t, sum, sg);
+      float m2 = -INFINITY, y2 = 0.f;
+      emit(p, taddr, row, row_ok, col0, nvalid, ref, pre.shift, lb, false, m2, y2, has_t, sum, sg);
     } else {
       // single pass against the published row reference
       ref = row_ok ? pref : 0.f;
-      emit(p, taddr, row, row_ok, col0, nvalid, ref, lb, true, mx, yt, has_t, sum, sg);
+      emit(p, taddr, row, row_ok, col0, nvalid, ref, pre.shift, lb, true, mx, yt, has_t, sum, sg);
+      mx = mx * p.logit_scale + pre.shift;  // accumulator -> logit space
+      yt = yt * p.logit_scale + pre.shift;
       bad = row_ok && (mx - ref > kMaxRefGap);  // e^{Y - r} overflowed: redo against the tile max
       if (__ballot_sync(0xffffffffu, bad)) {
         if (bad) ref = mx;
         // the first pass's P boxes must land before they are overwritten
         if (p.use_tma) sg.drain();
-        float m2;
-        emit(p, taddr, row, row_ok, col0, nvalid, ref, lb, false, m2, yt, has_t, sum, sg);
+        float m2 = -INFINITY, y2 = 0.f;
+        emit(p, taddr, row, row_ok, col0, nvalid, ref, pre.shift, lb, false, m2, y2, has_t, sum, sg);
       }
     }
     if (row_ok) {

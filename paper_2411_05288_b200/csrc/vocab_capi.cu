@@ -7,11 +7,15 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/vpipe_b200.h"
+#include "comm.h"
+#include "common.h"
 #include "gemm_host.cuh"
 #include "vocab_kernels.cuh"
 #include "vocab_program.h"
@@ -20,28 +24,9 @@ namespace {
 
 thread_local std::string g_last_error;
 
-struct CudaError : std::runtime_error {
-  using std::runtime_error::runtime_error;
-};
-struct NcclError : std::runtime_error {
-  using std::runtime_error::runtime_error;
-};
-
-#define VP_CUDA(x)                                                                                   \
-  do {                                                                                               \
-    cudaError_t e_ = (x);                                                                            \
-    if (e_ != cudaSuccess) throw CudaError(std::string(#x) + ": " + cudaGetErrorString(e_));        \
-  } while (0)
-#define VP_NCCL(x)                                                                                   \
-  do {                                                                                               \
-    ncclResult_t r_ = (x);                                                                           \
-    if (r_ != ncclSuccess) throw NcclError(std::string(#x) + ": " + ncclGetErrorString(r_));        \
-  } while (0)
-#define VP_KCHECK() VP_CUDA(cudaGetLastError())
-
-inline void require(bool cond, const char* msg) {
-  if (!cond) throw std::invalid_argument(msg);
-}
+using vp::CudaError;
+using vp::NcclError;
+using vp::require;
 
 template <class F>
 int api(F&& f) {
@@ -63,13 +48,18 @@ int api(F&& f) {
   }
 }
 
-// Grow-only device buffer.
+// Grow-only device buffer.  A buffer that grows is retired, not freed, until
+// the context is destroyed: a CUDA graph captured earlier keeps the old
+// pointer and stays valid (its workspace use is internal to the captured
+// calls, so a replay reads what it wrote).  No cudaFree on a hot path either
+// (cudaFree synchronises the device).
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
+  std::vector<void*> retired;
   void* get(size_t need) {
     if (need > bytes) {
-      if (p) VP_CUDA(cudaFree(p));
+      if (p) retired.push_back(p);
       p = nullptr;
       VP_CUDA(cudaMalloc(&p, need));
       bytes = need;
@@ -78,12 +68,15 @@ struct DevBuf {
   }
   void release() {
     if (p) cudaFree(p);
+    for (void* q : retired) cudaFree(q);
+    retired.clear();
     p = nullptr;
     bytes = 0;
   }
 };
 
-constexpr int kErrInputFwd = 1, kErrInputBwd = 2;
+// deferred device-side argument errors (d_err bits), reported by vp_ctx_sync
+constexpr int kErrInputFwd = 1, kErrInputBwd = 2, kErrLabel = 4;
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
@@ -123,8 +116,10 @@ struct vp_ctx_s {
   // tile shapes actually launched: 512-wide tiles and multicast need CTA pairs
   int eff_nh(int i) const { return cg == 2 ? nh[i] : 1; }
   int eff_mc(int i) const { return cg == 2 && eff_nh(i) == 1 ? mc : 1; }
-  ncclComm_t comm = nullptr;
+  std::unique_ptr<vp::Comm> comm;  // NCCL or loopback (comm.h); null = no group
   int nranks = 1, rank = 0;
+  bool gemm_sms_set = false;  // "gemm_sms" given explicitly (else a colocated share)
+  int64_t vocab_cache_key = -1, vocab_cache = -1;  // global V of the group (label checks)
   int* d_err = nullptr;
   int64_t launches = 0;
   // optional per-GEMM event timing (bench instrumentation): kind -> events
@@ -135,7 +130,7 @@ struct vp_ctx_s {
   double gemm_ms[4] = {0, 0, 0, 0};
   int64_t gemm_n[4] = {0, 0, 0, 0};
   // workspace
-  DevBuf inv, scale, xs, gathered, packed, tmp_m, tmp_s, heads, counts;
+  DevBuf inv, scale, xs, gathered, packed, tmp_m, tmp_s, heads, counts, vtmp;
 
   void activate() const {
     VP_CUDA(cudaSetDevice(device));
@@ -149,10 +144,16 @@ struct vp_ctx_s {
   cudaEvent_t ev_ready = nullptr, ev_done = nullptr;
   bool overlap_c1 = true, reduce_pending = false;
   int comm_sms = 8;
+  // K1 logits y = acc * logit_scale + logit_shift[row] (the reference's
+  // logit_shift test hook, VM.cpp:41-43, and a fault-injection scale)
+  const float* logit_shift = nullptr;
+  float logit_scale = 1.f;
   // dW passes add into grad_w instead of overwriting it (gradient accumulation
   // across microbatches; tied input/output embeddings sharing one dE/dW buffer)
   bool accumulate_dw = false;
   bool distributed() const { return comm != nullptr && (nranks > 1 || force_collectives); }
+  // the NCCL / loopback group; callers check distributed() first
+  vp::Comm& cm() const { return *comm; }
   template <class T>
   T* buf(DevBuf& b, size_t count) {
     return static_cast<T*>(b.get(count * sizeof(T)));
@@ -209,6 +210,11 @@ void check_shard(const vp_shard_t* s, int64_t h) {
   require(aligned16(s->W), "EmbeddingShard: W must be 16-byte aligned");
 }
 
+// dW outputs: the one-hot scatter after the dW GEMM stores float4 rows
+void check_grad_w(const float* gw, int64_t ldgw, int64_t h, const char* msg) {
+  require(gw != nullptr && ldgw >= h && ldgw % 4 == 0 && aligned16(gw), msg);
+}
+
 void check_state(const vp_state_s* st, const vp_batch_t* b, const vp_shard_t* s) {
   require(st != nullptr, "ShardState: null state");
   require(st->n_tok == b->n_tok, "ShardState: n_tok mismatch");
@@ -248,6 +254,8 @@ void gemm_logits(vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* s, vp_state
                                b->labels,   s->row_begin, s->row_end,   st->ytgt,         st->tile_q,
                                st->row_ref, st->ref_flag, st->row_bad,  st->counters,     st->bad_list,
                                st->counters + 1, st->fix_list};
+  ep.logit_shift = c->logit_shift;
+  ep.logit_scale = c->logit_scale;
   timed_gemm(c, 0, [&] {
     vp::launch_gemm<vp::EpiLogitStats>(c->cg, {b->X, b->ldx, false}, {s->W, s->ldw, false}, int(b->n_tok),
                                        int(st->rows), int(b->h), c->raster[0], ep, c->gemm_sms, c->stream,
@@ -392,6 +400,27 @@ const __nv_bfloat16* scaled_x(vp_ctx_s* c, const vp_batch_t* b, const float* sc)
   return xs;
 }
 
+// The group's vocabulary size V (labels must lie in [0, V), VM.cpp:18): the
+// largest row_end of the local shards, or, in a group, of every rank's shard
+// (one max all-reduce per shard layout, cached).
+int64_t global_vocab(vp_ctx_s* c, const vp_shard_t* shards, int n) {
+  int64_t V = 0;
+  for (int k = 0; k < n; ++k) V = std::max(V, shards[k].row_end);
+  if (!c->distributed()) return V;
+  if (c->vocab_cache_key == V) return c->vocab_cache;
+  require(V < (int64_t(1) << 24), "vocab size must be < 2^24");
+  float* d = c->buf<float>(c->vtmp, 1);
+  const float f = float(V);
+  VP_CUDA(cudaMemcpyAsync(d, &f, sizeof(float), cudaMemcpyHostToDevice, c->stream));
+  c->cm().all_reduce(d, d, 1, vp::DType::F32, vp::RedOp::Max, c->stream);
+  float g = 0.f;
+  VP_CUDA(cudaMemcpyAsync(&g, d, sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+  VP_CUDA(cudaStreamSynchronize(c->stream));
+  c->vocab_cache_key = V;
+  c->vocab_cache = int64_t(g);
+  return c->vocab_cache;
+}
+
 void merge_stats(vp_ctx_s* c, const vp_state_t* states, int n, double fault_scale, vp_stats_t out) {
   require(n >= 1 && states != nullptr, "merge_max_sum: empty input");
   require(out.m != nullptr && out.sum != nullptr, "merge_max_sum: null output");
@@ -407,7 +436,7 @@ void merge_stats(vp_ctx_s* c, const vp_state_t* states, int n, double fault_scal
     vp::k_pack_stats<<<unsigned(ceil_div(T, 256)), 256, 0, c->stream>>>(states[0]->m_loc, states[0]->s_loc, int(T),
                                                                         packed);
     VP_KCHECK();
-    VP_NCCL(ncclAllGather(packed, gathered, size_t(2 * T), ncclFloat32, c->comm, c->stream));
+    c->cm().all_gather(packed, gathered, size_t(2 * T), vp::DType::F32, c->stream);
     vp::k_merge_stats<<<unsigned(ceil_div(T, 256)), 256, 0, c->stream>>>(
         gathered, gathered + T, c->nranks, 2 * T, int(T), float(fault_scale), out.m, out.sum);
     VP_KCHECK();
@@ -437,6 +466,7 @@ void alg1_T(vp_ctx_s* c, vp_state_s* st, vp_stats_t g, const vp_batch_t* b, cons
   check_state(st, b, s);
   require(st->has_S && st->form == kLocal, "alg1_pass_T: state/stats length mismatch");
   require(g.m && g.sum, "alg1_pass_T: null stats");
+  check_grad_w(gw, ldgw, b->h, "alg1_pass_T: grad_w needs ldgw >= h, ldgw % 4 == 0 and a 16-byte aligned base");
   const float* sc = global_scale(c, st, g);
   gemm_dx(c, st, s, gx, ldgx, sc);
   vp::k_sub_label_rows<<<c->grid_for(st->n_tok * st->h / 2, 256), 256, 0, c->stream>>>(
@@ -446,7 +476,7 @@ void alg1_T(vp_ctx_s* c, vp_state_s* st, vp_stats_t g, const vp_batch_t* b, cons
   ++c->launches;
   gemm_dw(c, st, scaled_x(c, b, sc), b->h, gw, ldgw);
   segment_scatter(c, b->labels, b->n_tok, s->row_begin, s->row_end, static_cast<const __nv_bfloat16*>(b->X), b->ldx,
-                  b->h, -1.f, gw, ldgw, 1);
+                  b->h, -1.f, gw, ldgw, 1, kErrLabel);
 }
 
 // alg2_pass_T (VM.cpp:213-225): dW_k = softmax'^T (c (.) X) - G_k^T X
@@ -457,10 +487,11 @@ void alg2_T(vp_ctx_s* c, vp_state_s* st, vp_stats_t g, const vp_batch_t* b, cons
   check_state(st, b, s);
   require(st->has_S && st->form == kLocal, "alg2_pass_T: state/stats length mismatch");
   require(g.m && g.sum, "alg2_pass_T: null stats");
+  check_grad_w(gw, ldgw, b->h, "alg2_pass_T: grad_w needs ldgw >= h, ldgw % 4 == 0 and a 16-byte aligned base");
   const float* sc = global_scale(c, st, g);
   gemm_dw(c, st, scaled_x(c, b, sc), b->h, gw, ldgw);
   segment_scatter(c, b->labels, b->n_tok, s->row_begin, s->row_end, static_cast<const __nv_bfloat16*>(b->X), b->ldx,
-                  b->h, -1.f, gw, ldgw, 1);
+                  b->h, -1.f, gw, ldgw, 1, kErrLabel);
 }
 
 void alg2_C1(vp_ctx_s* c, const vp_state_t* states, const vp_shard_t* shards, int n, const vp_batch_t* b,
@@ -473,7 +504,7 @@ void alg2_C1(vp_ctx_s* c, const vp_state_t* states, const vp_shard_t* shards, in
     check_shard(&shards[k], b->h);
     check_state(states[k], b, &shards[k]);
   }
-  require(gx != nullptr && ldgx >= b->h && ldgx % 4 == 0, "alg2_barrier_C1: bad grad_x buffer");
+  require(gx != nullptr && ldgx >= b->h && ldgx % 4 == 0 && aligned16(gx), "alg2_barrier_C1: bad grad_x buffer");
   merge_stats(c, states, n, fault_scale, out);
   vp::CombineShards S{};
   S.p = n;
@@ -487,13 +518,14 @@ void alg2_C1(vp_ctx_s* c, const vp_state_t* states, const vp_shard_t* shards, in
     S.ml[k] = states[k]->m_loc;
     S.sl[k] = states[k]->s_loc;
   }
+  const int64_t V = global_vocab(c, shards, n);
   vp::k_alg2_combine<<<c->grid_for(b->n_tok * b->h / 4, 256), 256, 0, c->stream>>>(
-      S, out.m, out.sum, b->labels, int(b->n_tok), int(b->h), gx, ldgx);
+      S, out.m, out.sum, b->labels, int(b->n_tok), int(b->h), gx, ldgx, V, c->d_err, kErrLabel);
   VP_KCHECK();
   ++c->launches;
   if (c->distributed() && reduce) {
     require(ldgx == b->h, "alg2_barrier_C1: grad_x must be dense (ldgx == h) for the all-reduce");
-    VP_NCCL(ncclAllReduce(gx, gx, size_t(b->n_tok * b->h), ncclFloat32, ncclSum, c->comm, c->stream));
+    c->cm().all_reduce(gx, gx, size_t(b->n_tok * b->h), vp::DType::F32, vp::RedOp::Sum, c->stream);
   }
 }
 
@@ -508,12 +540,13 @@ void loss_of(vp_ctx_s* c, const vp_state_t* states, const vp_shard_t* shards, in
     S.rb[k] = shards[k].row_begin;
     S.re[k] = shards[k].row_end;
   }
+  const int64_t V = global_vocab(c, shards, n);
   vp::k_loss<<<unsigned(ceil_div(b->n_tok, 256)), 256, 0, c->stream>>>(S, g.m, g.sum, b->labels, int(b->n_tok),
-                                                                       loss);
+                                                                       loss, V, c->d_err, kErrLabel);
   VP_KCHECK();
   ++c->launches;
   if (c->distributed() && reduce)
-    VP_NCCL(ncclAllReduce(loss, loss, size_t(b->n_tok), ncclFloat32, ncclSum, c->comm, c->stream));
+    c->cm().all_reduce(loss, loss, size_t(b->n_tok), vp::DType::F32, vp::RedOp::Sum, c->stream);
 }
 
 void reduce_partials(vp_ctx_s* c, float* const* partials, int n, int64_t T, int64_t h, int64_t ld, float* gx,
@@ -522,7 +555,7 @@ void reduce_partials(vp_ctx_s* c, float* const* partials, int n, int64_t T, int6
   require(ld == h && ldgx == h, "reduce_grad_x: partials and grad_x must be dense [n_tok x h]");
   if (c->distributed()) {
     require(n == 1, "reduce_grad_x: one partial per rank in an NCCL group");
-    VP_NCCL(ncclAllReduce(partials[0], gx, size_t(T * h), ncclFloat32, ncclSum, c->comm, c->stream));
+    c->cm().all_reduce(partials[0], gx, size_t(T * h), vp::DType::F32, vp::RedOp::Sum, c->stream);
     return;
   }
   require(n <= vp::kMaxLocalShards, "reduce_grad_x: too many partials");
@@ -539,10 +572,10 @@ void reduce_partials(vp_ctx_s* c, float* const* partials, int n, int64_t T, int6
 void fork_allreduces(vp_ctx_s* c, float* gx, int64_t n_gx, float* loss, int64_t n_loss) {
   VP_CUDA(cudaEventRecord(c->ev_ready, c->stream));
   VP_CUDA(cudaStreamWaitEvent(c->comm_stream, c->ev_ready, 0));
-  VP_NCCL(ncclGroupStart());
-  VP_NCCL(ncclAllReduce(gx, gx, size_t(n_gx), ncclFloat32, ncclSum, c->comm, c->comm_stream));
-  VP_NCCL(ncclAllReduce(loss, loss, size_t(n_loss), ncclFloat32, ncclSum, c->comm, c->comm_stream));
-  VP_NCCL(ncclGroupEnd());
+  c->cm().group_start();
+  c->cm().all_reduce(gx, gx, size_t(n_gx), vp::DType::F32, vp::RedOp::Sum, c->comm_stream);
+  c->cm().all_reduce(loss, loss, size_t(n_loss), vp::DType::F32, vp::RedOp::Sum, c->comm_stream);
+  c->cm().group_end();
   VP_CUDA(cudaEventRecord(c->ev_done, c->comm_stream));
   c->reduce_pending = true;
 }
@@ -592,7 +625,7 @@ void run_alg(int alg, vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* shards
     }
     if (c->distributed()) {
       require(ldgx == b->h, "run_alg1: grad_x must be dense for the all-reduce");
-      VP_NCCL(ncclAllReduce(gx, gx, size_t(b->n_tok * b->h), ncclFloat32, ncclSum, c->comm, c->stream));
+      c->cm().all_reduce(gx, gx, size_t(b->n_tok * b->h), vp::DType::F32, vp::RedOp::Sum, c->stream);
     } else {
       reduce_partials(c, partials.data(), n, b->n_tok, b->h, b->h, gx, ldgx);
     }
@@ -608,6 +641,7 @@ void naive(vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* shards, const vp_
   const int64_t T = b->n_tok;
   for (int k = 0; k < n; ++k) {
     check_shard(&shards[k], b->h);
+    check_grad_w(gw[k], ldgw, b->h, "naive: grad_w needs ldgw >= h, ldgw % 4 == 0 and a 16-byte aligned base");
     check_state(states[k], b, &shards[k]);
     vp_state_s* st = states[k];
     if (!st->Y) VP_CUDA(cudaMalloc(&st->Y, size_t(T * st->rows) * sizeof(float)));
@@ -623,7 +657,7 @@ void naive(vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* shards, const vp_
     ++c->launches;
   }
   if (c->distributed()) {
-    VP_NCCL(ncclAllReduce(states[0]->m_loc, out.m, size_t(T), ncclFloat32, ncclMax, c->comm, c->stream));
+    c->cm().all_reduce(states[0]->m_loc, out.m, size_t(T), vp::DType::F32, vp::RedOp::Max, c->stream);
   } else {
     vp::StatsParts parts{};
     parts.p = n;
@@ -643,7 +677,7 @@ void naive(vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* shards, const vp_
     ++c->launches;
   }
   if (c->distributed()) {
-    VP_NCCL(ncclAllReduce(states[0]->s_loc, out.sum, size_t(T), ncclFloat32, ncclSum, c->comm, c->stream));
+    c->cm().all_reduce(states[0]->s_loc, out.sum, size_t(T), vp::DType::F32, vp::RedOp::Sum, c->stream);
   } else {
     vp::PartialPtrs S{};
     S.p = n;
@@ -673,11 +707,11 @@ void naive(vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* shards, const vp_
     ++c->launches;
     gemm_dw(c, st, b->X, b->ldx, gw[k], ldgw);
     segment_scatter(c, b->labels, T, shards[k].row_begin, shards[k].row_end,
-                    static_cast<const __nv_bfloat16*>(b->X), b->ldx, b->h, -1.f, gw[k], ldgw, 1);
+                    static_cast<const __nv_bfloat16*>(b->X), b->ldx, b->h, -1.f, gw[k], ldgw, 1, kErrLabel);
   }
   loss_of(c, states, shards, n, out, b, loss);
   if (c->distributed()) {
-    VP_NCCL(ncclAllReduce(gx, gx, size_t(T * b->h), ncclFloat32, ncclSum, c->comm, c->stream));
+    c->cm().all_reduce(gx, gx, size_t(T * b->h), vp::DType::F32, vp::RedOp::Sum, c->stream);
   } else {
     reduce_partials(c, partials.data(), n, T, b->h, b->h, gx, ldgx);
   }
@@ -729,7 +763,7 @@ void run_program(vp_ctx_s* c, const vp::Program& prog, const vp_batch_t* batches
   auto st = [&](int ls, int i) { return states[size_t(ls) * size_t(n) + size_t(i)]; };
   for (int ls = 0; ls < nsh; ++ls) {
     check_shard(&shards[ls], batches[0].h);
-    require(gw[ls] != nullptr && ldgw >= batches[0].h, "vp_program_run: bad grad_w");
+    check_grad_w(gw[ls], ldgw, batches[0].h, "vp_program_run: bad grad_w");
     const int64_t rows = shards[ls].row_end - shards[ls].row_begin;
     VP_CUDA(cudaMemsetAsync(gw[ls], 0, size_t(rows * ldgw) * sizeof(float), c->stream));
     for (int i = 0; i < n; ++i) check_state(st(ls, i), &batches[i], &shards[ls]);
@@ -771,8 +805,8 @@ void run_program(vp_ctx_s* c, const vp::Program& prog, const vp_batch_t* batches
       if (k == vp::PKind::C0) {
         // broadcast of the last stage's output (X_i) to every device
         if (dist)
-          VP_NCCL(ncclBroadcast(b->X, const_cast<void*>(b->X), size_t(T * b->ldx), ncclBfloat16, p - 1, c->comm,
-                                c->stream));
+          c->cm().broadcast(b->X, const_cast<void*>(b->X), size_t((T - 1) * b->ldx + b->h), vp::DType::BF16, p - 1,
+                            c->stream);  // the logical extent of X: (T-1) ldx + h elements
       } else if (k == vp::PKind::C1) {
         if (alg2) {
           alg2_C1(c, sts.data(), shards, nsh, b, 1.0, stats[i], gx[i], ldgx, /*reduce=*/!overlap);
@@ -791,11 +825,11 @@ void run_program(vp_ctx_s* c, const vp::Program& prog, const vp_batch_t* batches
           if (overlap) {
             VP_CUDA(cudaEventRecord(c->ev_ready, c->stream));
             VP_CUDA(cudaStreamWaitEvent(c->comm_stream, c->ev_ready, 0));
-            VP_NCCL(ncclAllReduce(gx[i], gx[i], size_t(T * h), ncclFloat32, ncclSum, c->comm, c->comm_stream));
+            c->cm().all_reduce(gx[i], gx[i], size_t(T * h), vp::DType::F32, vp::RedOp::Sum, c->comm_stream);
             VP_CUDA(cudaEventRecord(c->ev_done, c->comm_stream));
             c->reduce_pending = true;
           } else {
-            VP_NCCL(ncclAllReduce(gx[i], gx[i], size_t(T * h), ncclFloat32, ncclSum, c->comm, c->stream));
+            c->cm().all_reduce(gx[i], gx[i], size_t(T * h), vp::DType::F32, vp::RedOp::Sum, c->stream);
           }
         } else {
           std::vector<float*> parts(static_cast<size_t>(nsh));
@@ -834,6 +868,23 @@ void run_program(vp_ctx_s* c, const vp::Program& prog, const vp_batch_t* batches
   }
   restore();
   join_allreduces(c);
+}
+
+// Installs a communicator on a context: the comm stream / events of the
+// barrier overlap, and, when several ranks share this GPU (loopback), a
+// 1/colocated share of its SMs for the persistent GEMMs so the co-located
+// grids fit side by side (their cross-CTA waits need every CTA resident).
+void attach_comm(vp_ctx_s* c, std::unique_ptr<vp::Comm> comm) {
+  c->nranks = comm->nranks;
+  c->rank = comm->rank;
+  const int share = comm->colocated();
+  c->comm = std::move(comm);
+  if (share > 1 && !c->gemm_sms_set) c->gemm_sms = std::max(2, c->num_sms / share / 2 * 2);
+  int lo = 0, hi = 0;
+  VP_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  VP_CUDA(cudaStreamCreateWithPriority(&c->comm_stream, cudaStreamNonBlocking, hi));
+  VP_CUDA(cudaEventCreateWithFlags(&c->ev_ready, cudaEventDisableTiming));
+  VP_CUDA(cudaEventCreateWithFlags(&c->ev_done, cudaEventDisableTiming));
 }
 
 }  // namespace
@@ -898,7 +949,7 @@ int vp_ctx_destroy(vp_ctx_t c) {
     if (!c) return;
     c->activate();
     cudaStreamSynchronize(c->stream);
-    if (c->comm) ncclCommDestroy(c->comm);
+    c->comm.reset();
     if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
     if (c->ev_ready) cudaEventDestroy(c->ev_ready);
     if (c->ev_done) cudaEventDestroy(c->ev_done);
@@ -932,6 +983,7 @@ int vp_ctx_sync(vp_ctx_t c) {
     VP_CUDA(cudaMemcpy(&err, c->d_err, sizeof(int), cudaMemcpyDeviceToHost));
     if (err) {
       VP_CUDA(cudaMemset(c->d_err, 0, sizeof(int)));
+      if (err & kErrLabel) throw std::invalid_argument("TokenBatch: label out of range");
       if (err & kErrInputFwd) throw std::invalid_argument("input_forward: token out of range");
       throw std::invalid_argument("input_backward: token out of range");
     }
@@ -1010,6 +1062,10 @@ int vp_ctx_set_option(vp_ctx_t c, const char* key, int64_t value) {
     } else if (k == "epi_wait") {
       require(value == 0 || value == 1, "vp_ctx_set_option: epi_wait must be 0 or 1");
       vp::g_epi_wait = int(value);
+    } else if (k == "debug_logit_scale_ppm") {
+      // fault injection (verification tools): K1 logits scaled by 1 + ppm * 1e-6
+      require(value > -1000000 && value <= 1000000, "vp_ctx_set_option: debug_logit_scale_ppm out of range");
+      c->logit_scale = float(1.0 + double(value) * 1e-6);
     } else if (k == "force_collectives") {
       c->force_collectives = value != 0;
     } else if (k == "multicast") {
@@ -1019,6 +1075,7 @@ int vp_ctx_set_option(vp_ctx_t c, const char* key, int64_t value) {
     } else if (k == "gemm_sms") {
       require(value >= 2 && value <= c->num_sms, "vp_ctx_set_option: gemm_sms out of range");
       c->gemm_sms = int(value);
+      c->gemm_sms_set = true;
     } else {
       throw std::invalid_argument("vp_ctx_set_option: unknown option " + k);
     }
@@ -1026,6 +1083,13 @@ int vp_ctx_set_option(vp_ctx_t c, const char* key, int64_t value) {
 }
 
 int64_t vp_ctx_launch_count(vp_ctx_t c) { return c ? c->launches : -1; }
+
+int vp_ctx_set_logit_shift(vp_ctx_t c, const float* shift) {
+  return api([&] {
+    require(c != nullptr, "vp_ctx_set_logit_shift: null context");
+    c->logit_shift = shift;
+  });
+}
 
 int vp_ctx_gemm_timing(vp_ctx_t c, int enable, double* ms_out, int64_t* count_out) {
   return api([&] {
@@ -1062,25 +1126,86 @@ int vp_comm_unique_id(void* id128) {
   });
 }
 
+int vp_comm_loopback_id(void* id128) {
+  return api([&] {
+    require(id128 != nullptr, "vp_comm_loopback_id: null output");
+    vp::make_loopback_id(id128);
+  });
+}
+
 int vp_ctx_comm_init(vp_ctx_t c, int nranks, int rank, const void* id128) {
   return api([&] {
     require(c != nullptr && id128 != nullptr, "vp_ctx_comm_init: null argument");
     require(nranks >= 1 && rank >= 0 && rank < nranks, "vp_ctx_comm_init: bad rank");
     require(c->comm == nullptr, "vp_ctx_comm_init: already initialised");
     c->activate();
-    ncclUniqueId id;
-    std::memcpy(&id, id128, sizeof(id));
-    ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
-    cfg.maxCTAs = c->comm_sms;  // NCCL runs beside the persistent GEMMs on the SMs they leave free
-    VP_NCCL(ncclCommInitRankConfig(&c->comm, nranks, id, rank, &cfg));
-    c->nranks = nranks;
-    c->rank = rank;
-    int lo = 0, hi = 0;
-    VP_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-    VP_CUDA(cudaStreamCreateWithPriority(&c->comm_stream, cudaStreamNonBlocking, hi));
-    VP_CUDA(cudaEventCreateWithFlags(&c->ev_ready, cudaEventDisableTiming));
-    VP_CUDA(cudaEventCreateWithFlags(&c->ev_done, cudaEventDisableTiming));
+    attach_comm(c, vp::is_loopback_id(id128) ? vp::make_loopback_comm(nranks, rank, id128, c->device)
+                                              : vp::make_nccl_comm(nranks, rank, id128, c->comm_sms));
   });
+}
+
+int vp_comm_init_all(vp_ctx_t* ctxs, int n) {
+  return api([&] {
+    require(ctxs != nullptr && n >= 1, "vp_comm_init_all: no contexts");
+    std::vector<int> devs;
+    for (int k = 0; k < n; ++k) {
+      require(ctxs[k] != nullptr, "vp_comm_init_all: null context");
+      require(ctxs[k]->comm == nullptr, "vp_ctx_comm_init: already initialised");
+      devs.push_back(ctxs[k]->device);
+    }
+    std::vector<int> sorted = devs;
+    std::sort(sorted.begin(), sorted.end());
+    const bool distinct = std::adjacent_find(sorted.begin(), sorted.end()) == sorted.end();
+    std::vector<std::unique_ptr<vp::Comm>> comms(static_cast<size_t>(n));
+    if (distinct) {
+      // one NCCL rank per GPU, created from this thread in one group (the
+      // ncclCommInitAll pattern, with each rank's maxCTAs config)
+      ncclUniqueId id;
+      VP_NCCL(ncclGetUniqueId(&id));
+      std::vector<ncclComm_t> raw(static_cast<size_t>(n), nullptr);
+      VP_NCCL(ncclGroupStart());
+      for (int k = 0; k < n; ++k) {
+        ctxs[k]->activate();
+        ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+        cfg.maxCTAs = ctxs[k]->comm_sms;
+        const ncclResult_t r = ncclCommInitRankConfig(&raw[size_t(k)], n, id, k, &cfg);
+        if (r != ncclSuccess) {
+          ncclGroupEnd();
+          throw NcclError(std::string("ncclCommInitRankConfig: ") + ncclGetErrorString(r));
+        }
+      }
+      VP_NCCL(ncclGroupEnd());
+      for (int k = 0; k < n; ++k) comms[size_t(k)] = vp::wrap_nccl_comm(raw[size_t(k)], n, k);
+    } else {
+      // ranks sharing a GPU: the loopback backend (its join is a rendezvous,
+      // so every rank joins from its own thread)
+      char id[128];
+      vp::make_loopback_id(id);
+      std::vector<std::string> errs(static_cast<size_t>(n));
+      std::vector<std::thread> th;
+      for (int k = 0; k < n; ++k)
+        th.emplace_back([&, k] {
+          try {
+            ctxs[k]->activate();
+            comms[size_t(k)] = vp::make_loopback_comm(n, k, id, ctxs[k]->device);
+          } catch (const std::exception& e) {
+            errs[size_t(k)] = e.what();
+          }
+        });
+      for (auto& t : th) t.join();
+      for (const auto& e : errs)
+        if (!e.empty()) throw NcclError("vp_comm_init_all: " + e);
+    }
+    for (int k = 0; k < n; ++k) {
+      ctxs[k]->activate();
+      attach_comm(ctxs[k], std::move(comms[size_t(k)]));
+    }
+  });
+}
+
+const char* vp_ctx_comm_backend(vp_ctx_t c) {
+  if (c == nullptr) return "";
+  return c->comm ? c->comm->backend() : "none";
 }
 
 int vp_ctx_comm_info(vp_ctx_t c, int* nranks, int* rank) {
@@ -1293,6 +1418,39 @@ int vp_shard_softmax(vp_ctx_t c, vp_state_t st, vp_stats_t g, float* out, int64_
   });
 }
 
+int vp_shard_logits(vp_ctx_t c, const vp_batch_t* b, const vp_shard_t* s, float* out, int64_t ldo) {
+  return api([&] {
+    require(c != nullptr && out != nullptr, "logits: null argument");
+    check_batch(b, false);
+    check_shard(s, b->h);
+    const int64_t rows = s->row_end - s->row_begin;
+    require(ldo >= rows, "logits: ldo < rows");
+    c->activate();
+    vp::EpiStoreF32::Params ep{out, ldo, nullptr, 0, nullptr};
+    timed_gemm(c, 1, [&] {
+      vp::launch_gemm<vp::EpiStoreF32>(c->cg, {b->X, b->ldx, false}, {s->W, s->ldw, false}, int(b->n_tok), int(rows),
+                                       int(b->h), c->raster[0], ep, c->gemm_sms, c->stream, c->pol[0], c->pol[0],
+                                       c->eff_mc(0));
+    });
+    ++c->launches;
+  });
+}
+
+int vp_shard_label_rows(vp_ctx_t c, const vp_batch_t* b, const vp_shard_t* s, float* out, int64_t ldo) {
+  return api([&] {
+    require(c != nullptr && out != nullptr, "label rows: null argument");
+    check_batch(b);
+    check_shard(s, b->h);
+    require(ldo >= b->h, "label rows: ldo < h");
+    c->activate();
+    vp::k_label_rows<<<c->grid_for(b->n_tok * b->h / 2, 256), 256, 0, c->stream>>>(
+        static_cast<const __nv_bfloat16*>(s->W), s->ldw, s->row_begin, s->row_end, b->labels, int(b->n_tok),
+        int(b->h), out, ldo);
+    VP_KCHECK();
+    ++c->launches;
+  });
+}
+
 int vp_naive_partitioned_output(vp_ctx_t c, const vp_batch_t* b, const vp_shard_t* shards, const vp_state_t* states,
                                 int n, vp_stats_t out, float* loss, float* gx, int64_t ldgx, float* const* gw,
                                 int64_t ldgw) {
@@ -1346,7 +1504,7 @@ int vp_input_backward(vp_ctx_t c, const void* grad, int64_t ldg, int grad_is_f32
     require(c != nullptr && gw != nullptr && tokens != nullptr && grad != nullptr, "input_backward: null argument");
     require(n_tok >= 0, "input_backward: grad/token length mismatch");
     check_shard(s, h);
-    require(h % 8 == 0 && ldg >= h && ldg % 8 == 0 && ldgw >= h && ldgw % 4 == 0,
+    require(h % 8 == 0 && ldg >= h && ldg % 8 == 0 && ldgw >= h && ldgw % 4 == 0 && aligned16(gw) && aligned16(grad),
             "input_backward: h/ld must be multiples of 8");
     c->activate();
     const int64_t rows = s->row_end - s->row_begin;
@@ -1370,8 +1528,8 @@ int vp_allreduce_sum(vp_ctx_t c, void* buf, int64_t count, int dtype) {
     require(dtype == 0 || dtype == 1, "allreduce: dtype must be 0 (fp32) or 1 (bf16)");
     if (!c->distributed()) return;
     c->activate();
-    VP_NCCL(ncclAllReduce(buf, buf, size_t(count), dtype == 0 ? ncclFloat32 : ncclBfloat16, ncclSum, c->comm,
-                          c->stream));
+    c->cm().all_reduce(buf, buf, size_t(count), dtype == 0 ? vp::DType::F32 : vp::DType::BF16, vp::RedOp::Sum,
+                       c->stream);
   });
 }
 
@@ -1436,6 +1594,8 @@ int vp_ctx_capture_begin(vp_ctx_t c) {
     require(c != nullptr, "vp_ctx_capture_begin: null context");
     require(c->stream != nullptr, "vp_ctx_capture_begin: the legacy default stream cannot be captured");
     require(!c->timing, "vp_ctx_capture_begin: disable GEMM timing before capturing");
+    require(!c->comm || c->comm->capturable(),
+            "vp_ctx_capture_begin: the loopback backend's host rendezvous cannot be captured");
     c->activate();
     VP_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
   });

@@ -273,12 +273,13 @@ struct CombineShards {
 };
 __global__ void k_alg2_combine(CombineShards S, const float* __restrict__ mg, const float* __restrict__ sg,
                                const int64_t* __restrict__ labels, int n, int h, float* __restrict__ gx,
-                               int64_t ldgx) {
+                               int64_t ldgx, int64_t V, int* __restrict__ err, int err_bit) {
   const int hv = h / 4;
   const int64_t total = int64_t(n) * hv;
   for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < total; t += int64_t(gridDim.x) * blockDim.x) {
     const int i = int(t / hv), c = int(t - int64_t(i) * hv) * 4;
     const int64_t g = labels[i];
+    if (c == 0 && (g < 0 || (V >= 0 && g >= V))) atomicOr(err, err_bit);  // VM.cpp:18
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int k = 0; k < S.p; ++k) {
       const float sc = S.sl[k][i] * expf(S.ml[k][i] - mg[i]) / sg[i];
@@ -329,6 +330,24 @@ __global__ void k_sub_label_rows(float* __restrict__ gx, int64_t ldgx, const __n
   }
 }
 
+// B_k = G_k W_k (VM.hpp:41, alg2_pass_S VM.cpp:186-190): out[i,:] = W_k[g_i - rb,:]
+// if shard k owns g_i, else 0 (debug materialisation; C1 gathers these rows
+// sparsely instead).  fp32 out, 2 columns per thread.
+__global__ void k_label_rows(const __nv_bfloat16* __restrict__ W, int64_t ldw, int64_t rb, int64_t re,
+                             const int64_t* __restrict__ labels, int n, int h, float* __restrict__ out,
+                             int64_t ldo) {
+  const int hv = h / 2;
+  const int64_t total = int64_t(n) * hv;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < total; t += int64_t(gridDim.x) * blockDim.x) {
+    const int i = int(t / hv), c = int(t - int64_t(i) * hv) * 2;
+    const int64_t g = labels[i];
+    float2 w = make_float2(0.f, 0.f);
+    if (g >= rb && g < re) w = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(W + (g - rb) * ldw + c));
+    out[int64_t(i) * ldo + c] = w.x;
+    out[int64_t(i) * ldo + c + 1] = w.y;
+  }
+}
+
 // loss_i = m_i + log(sum_i) - y_tgt_i at the shard owning g_i (VM.cpp:287-292);
 // rows owned by none of the given shards get 0 (summed across ranks).
 struct LossShards {
@@ -336,11 +355,15 @@ struct LossShards {
   int64_t rb[kMaxLocalShards], re[kMaxLocalShards];
   int p;
 };
+// A label outside [0, V) (V < 0: unknown upper bound) raises err_bit in *err
+// (the reference's "TokenBatch: label out of range", VM.cpp:18).
 __global__ void k_loss(LossShards S, const float* __restrict__ mg, const float* __restrict__ sg,
-                       const int64_t* __restrict__ labels, int n, float* __restrict__ loss) {
+                       const int64_t* __restrict__ labels, int n, float* __restrict__ loss, int64_t V,
+                       int* __restrict__ err, int err_bit) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int64_t g = labels[i];
+  if (g < 0 || (V >= 0 && g >= V)) atomicOr(err, err_bit);
   float out = 0.f;
   for (int k = 0; k < S.p; ++k)
     if (g >= S.rb[k] && g < S.re[k]) out = mg[i] + logf(sg[i]) - S.yt[k][i];

@@ -7,9 +7,14 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <exception>
+#include <map>
+#include <mutex>
 #include <random>
 #include <stdexcept>
 #include <string>
+#include <thread>
+#include <vector>
 
 #include "vpipe/vocab_math.hpp"
 #include "vpipe_b200.h"
@@ -48,18 +53,35 @@ void cuda_check(cudaError_t e) {
   if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA: ") + cudaGetErrorString(e));
 }
 
+// Fault injection for verification tools (env VPIPE_INJECT_K1_FAULT_PPM: the
+// pass-S logits of every context this API creates are scaled by 1 + ppm*1e-6).
+void configure(vp_ctx_t c) {
+  if (const char* f = std::getenv("VPIPE_INJECT_K1_FAULT_PPM"))
+    check(vp_ctx_set_option(c, "debug_logit_scale_ppm", std::atoll(f)));
+}
+
+int default_device() {
+  const char* dev = std::getenv("VPIPE_DEVICE");
+  return dev ? std::atoi(dev) : 0;
+}
+
 struct Ctx {
   vp_ctx_t c = nullptr;
   Ctx() {
-    const char* dev = std::getenv("VPIPE_DEVICE");
-    check(vp_ctx_create(dev ? std::atoi(dev) : 0, &c));
+    check(vp_ctx_create(default_device(), &c));
+    configure(c);
   }
   ~Ctx() {
     if (c) vp_ctx_destroy(c);
   }
 };
 
+// The context of a rank thread of a group run (see run_group), else the
+// process-wide single-device context.
+thread_local vp_ctx_t t_ctx = nullptr;
+
 vp_ctx_t ctx() {
+  if (t_ctx) return t_ctx;
   static Ctx g;
   return g.c;
 }
@@ -133,8 +155,15 @@ Vector download_vec(const void* dptr, int64_t n) {
 struct DeviceShard {
   DevPtr W;
   int64_t h = 0, ldw = 0;
+  int device = -1;
   vp_shard_t desc{};
 };
+
+int current_device() {
+  int d = 0;
+  cuda_check(cudaGetDevice(&d));
+  return d;
+}
 
 struct DeviceBatch {
   DevPtr X, labels;
@@ -153,12 +182,13 @@ struct DeviceState {
 };
 
 std::shared_ptr<DeviceShard> device_shard(const EmbeddingShard& s) {
-  if (s.dev && s.dev->h == s.W.cols()) return s.dev;
+  if (s.dev && s.dev->h == s.W.cols() && s.dev->device == current_device()) return s.dev;
   if (s.W.rows() != s.rows()) throw std::invalid_argument("EmbeddingShard: W rows != row_end - row_begin");
   auto d = std::make_shared<DeviceShard>();
   d->h = s.W.cols();
   d->ldw = pad8(d->h);
   d->W = upload_bf16(s.W, d->ldw);
+  d->device = current_device();
   d->desc.W = d->W->p;
   d->desc.ldw = d->ldw;
   d->desc.row_begin = s.row_begin;
@@ -236,11 +266,101 @@ void fetch_local(ShardState* st) {
   st->sum_local = download_vec(s, st->dev->n_tok);
 }
 
-// Full drivers: shards simulated on the one device, softmax assembled.
-OutputResult run(int alg, const TokenBatch& batch, const Matrix& W, int p, double fault_scale) {
+// ---- placement of run_naive / run_alg1 / run_alg2's p shards ---------------
+Placement& placement_ref() {
+  static Placement p = [] {
+    const char* e = std::getenv("VPIPE_PLACEMENT");
+    const std::string v = e ? e : "auto";
+    if (v == "local") return Placement::Local;
+    if (v == "spread") return Placement::Spread;
+    if (v == "loopback") return Placement::Loopback;
+    return Placement::Auto;
+  }();
+  return p;
+}
+
+int visible_devices() {
+  int n = 0;
+  cuda_check(cudaGetDeviceCount(&n));
+  return n;
+}
+
+Placement resolve(int p) {
+  const Placement want = placement_ref();
+  if (p == 1 || want == Placement::Local) return Placement::Local;
+  if (want == Placement::Spread) {
+    if (p > visible_devices()) throw std::invalid_argument("placement Spread: p exceeds the visible GPUs");
+    return Placement::Spread;
+  }
+  if (want == Placement::Loopback) return Placement::Loopback;
+  return visible_devices() >= p ? Placement::Spread : Placement::Local;  // Auto
+}
+
+// p contexts joined into one group (vp_comm_init_all): NCCL when they sit on
+// p distinct GPUs, the loopback backend when all share one.  Cached per
+// (placement, p): communicator set-up costs far more than a call.
+struct Group {
+  std::vector<vp_ctx_t> ctxs;
+  std::vector<int> devs;
+  ~Group() {
+    for (vp_ctx_t c : ctxs) vp_ctx_destroy(c);
+  }
+};
+
+Group& group(Placement pl, int p) {
+  static std::mutex mu;
+  static auto& cache = *new std::map<std::pair<int, int>, std::unique_ptr<Group>>();  // never destroyed (exit order)
+  std::lock_guard<std::mutex> lk(mu);
+  auto& g = cache[{int(pl), p}];
+  if (!g) {
+    auto ng = std::make_unique<Group>();
+    for (int k = 0; k < p; ++k) {
+      const int dev = pl == Placement::Spread ? k : default_device();
+      vp_ctx_t c = nullptr;
+      check(vp_ctx_create(dev, &c));
+      ng->ctxs.push_back(c);
+      ng->devs.push_back(dev);
+      configure(c);
+    }
+    check(vp_comm_init_all(ng->ctxs.data(), p));
+    g = std::move(ng);
+  }
+  return *g;
+}
+
+// One rank of a group run: its thread drives ctx on its device.
+struct RankScope {
+  explicit RankScope(vp_ctx_t c, int dev) {
+    t_ctx = c;
+    cuda_check(cudaSetDevice(dev));
+  }
+  ~RankScope() { t_ctx = nullptr; }
+};
+
+void download_into_rows(const void* dptr, int64_t rows, int64_t h, int64_t ld, Matrix* dst, int64_t row0) {
+  const Matrix g = download_f32(dptr, rows, h, ld);
+  std::memcpy(dst->row_ptr(row0), g.data(), sizeof(double) * size_t(rows * h));
+}
+
+void download_softmax_cols(vp_state_t st, const vp_stats_t& stats, int64_t n, int64_t rows, int64_t col0,
+                           Matrix* dst) {
+  DevMem sm(size_t(n * rows) * 4);
+  check(vp_shard_softmax(ctx(), st, stats, static_cast<float*>(sm.p), rows));
+  const Matrix s = download_f32(sm.p, n, rows, rows);
+  for (int64_t i = 0; i < n; ++i) std::memcpy(dst->row_ptr(i) + col0, s.row_ptr(i), sizeof(double) * size_t(rows));
+}
+
+int call_driver(int alg, vp_ctx_t c, const vp_batch_t* b, const vp_shard_t* sd, const vp_state_t* st, int n,
+                double fault_scale, vp_stats_t stats, float* loss, float* gx, int64_t ldgx, float* const* gw,
+                int64_t ldgw) {
+  if (alg == 0) return vp_naive_partitioned_output(c, b, sd, st, n, stats, loss, gx, ldgx, gw, ldgw);
+  if (alg == 1) return vp_run_alg1(c, b, sd, st, n, fault_scale, stats, loss, gx, ldgx, gw, ldgw);
+  return vp_run_alg2(c, b, sd, st, n, fault_scale, stats, loss, gx, ldgx, gw, ldgw);
+}
+
+// Full drivers, local placement: every shard on the one device, softmax assembled.
+OutputResult run_local(int alg, const TokenBatch& batch, const Matrix& W, int p, double fault_scale) {
   const auto shards = shard_weights(W, p);
-  if (alg == 0) check_batch(batch, W.rows());
-  if (batch.X.cols() != W.cols()) throw std::invalid_argument("oracle_output_layer: X/W hidden dim mismatch");
   auto b = device_batch(batch.X, &batch.labels);
   const int64_t n = batch.X.rows(), h = batch.X.cols(), ld = b->desc.h;
   std::vector<ShardState> states;
@@ -258,32 +378,74 @@ OutputResult run(int alg, const TokenBatch& batch, const Matrix& W, int p, doubl
   }
   DeviceStats stats(n);
   DevMem loss(size_t(n) * 4), gx(size_t(n * ld) * 4);
-  float* gxp = static_cast<float*>(gx.p);
-  if (alg == 0)
-    check(vp_naive_partitioned_output(ctx(), &b->desc, sd.data(), st.data(), p, stats.desc,
-                                      static_cast<float*>(loss.p), gxp, ld, gwp.data(), ld));
-  else if (alg == 1)
-    check(vp_run_alg1(ctx(), &b->desc, sd.data(), st.data(), p, fault_scale, stats.desc, static_cast<float*>(loss.p),
-                      gxp, ld, gwp.data(), ld));
-  else
-    check(vp_run_alg2(ctx(), &b->desc, sd.data(), st.data(), p, fault_scale, stats.desc, static_cast<float*>(loss.p),
-                      gxp, ld, gwp.data(), ld));
+  check(call_driver(alg, ctx(), &b->desc, sd.data(), st.data(), p, fault_scale, stats.desc,
+                    static_cast<float*>(loss.p), static_cast<float*>(gx.p), ld, gwp.data(), ld));
   OutputResult out;
   out.loss = download_vec(loss.p, n);
   out.grad_x = download_f32(gx.p, n, h, ld);
   out.grad_w.resize(W.rows(), h);
   out.softmax.resize(n, W.rows());
   for (size_t k = 0; k < shards.size(); ++k) {
-    const int64_t rows = shards[k].rows();
-    const Matrix g = download_f32(gwp[k], rows, h, ld);
-    std::memcpy(out.grad_w.row_ptr(shards[k].row_begin), g.data(), sizeof(double) * size_t(rows * h));
-    DevMem sm(size_t(n * rows) * 4);
-    check(vp_shard_softmax(ctx(), st[k], stats.desc, static_cast<float*>(sm.p), rows));
-    const Matrix s = download_f32(sm.p, n, rows, rows);
-    for (int64_t i = 0; i < n; ++i)
-      std::memcpy(out.softmax.row_ptr(i) + shards[k].row_begin, s.row_ptr(i), sizeof(double) * size_t(rows));
+    download_into_rows(gwp[k], shards[k].rows(), h, ld, &out.grad_w, shards[k].row_begin);
+    download_softmax_cols(st[k], stats.desc, n, shards[k].rows(), shards[k].row_begin, &out.softmax);
   }
   return out;
+}
+
+// Full drivers, one rank per shard: rank k's thread drives context k of the
+// group (its own GPU under Spread, GPU VPIPE_DEVICE under Loopback) with ONE
+// shard, so the library's collective paths do the exchanges (stats
+// all-gather, dX / loss all-reduce) — the reference's single-process view of
+// p devices (VM.hpp:106, :136-140).
+OutputResult run_group(int alg, const TokenBatch& batch, const Matrix& W, int p, double fault_scale, Group& g) {
+  const auto shards = shard_weights(W, p);
+  const int64_t n = batch.X.rows(), h = batch.X.cols();
+  OutputResult out;
+  out.grad_w.resize(W.rows(), h);
+  out.softmax.resize(n, W.rows());
+  std::vector<std::exception_ptr> errs(static_cast<size_t>(p));
+  std::vector<std::thread> th;
+  for (int k = 0; k < p; ++k)
+    th.emplace_back([&, k] {
+      try {
+        RankScope scope(g.ctxs[size_t(k)], g.devs[size_t(k)]);
+        auto b = device_batch(batch.X, &batch.labels);
+        const int64_t ld = b->desc.h, rows = shards[size_t(k)].rows();
+        auto ds = device_shard(shards[size_t(k)]);
+        ShardState state = make_state(b, ds, h, rows);
+        vp_state_t st = state.dev->st;
+        DeviceStats stats(n);
+        DevMem loss(size_t(n) * 4), gx(size_t(n * ld) * 4), gw(size_t(rows * ld) * 4);
+        float* gwp = static_cast<float*>(gw.p);
+        check(call_driver(alg, ctx(), &b->desc, &ds->desc, &st, 1, fault_scale, stats.desc,
+                          static_cast<float*>(loss.p), static_cast<float*>(gx.p), ld, &gwp, ld));
+        if (k == 0) {  // every rank holds the same loss and grad_x
+          out.loss = download_vec(loss.p, n);
+          out.grad_x = download_f32(gx.p, n, h, ld);
+        }
+        download_into_rows(gwp, rows, h, ld, &out.grad_w, shards[size_t(k)].row_begin);
+        download_softmax_cols(st, stats.desc, n, rows, shards[size_t(k)].row_begin, &out.softmax);
+        sync();
+      } catch (...) {
+        errs[size_t(k)] = std::current_exception();
+      }
+    });
+  for (auto& t : th) t.join();
+  for (auto& e : errs)
+    if (e) std::rethrow_exception(e);
+  return out;
+}
+
+OutputResult run(int alg, const TokenBatch& batch, const Matrix& W, int p, double fault_scale) {
+  if (p < 1) throw std::invalid_argument("shard_weights: p must be >= 1");
+  if (W.rows() % p != 0) throw std::invalid_argument("shard_weights: V not divisible by p");
+  if (alg == 0) check_batch(batch, W.rows());
+  if (batch.X.cols() != W.cols()) throw std::invalid_argument("oracle_output_layer: X/W hidden dim mismatch");
+  if (batch.X.rows() < 1) throw std::invalid_argument("TokenBatch: empty X");
+  if (int64_t(batch.labels.size()) != batch.X.rows()) throw std::invalid_argument("TokenBatch: labels/X row mismatch");
+  const Placement pl = resolve(p);
+  if (pl == Placement::Local) return run_local(alg, batch, W, p, fault_scale);
+  return run_group(alg, batch, W, p, fault_scale, group(pl, p));
 }
 
 }  // namespace detail
@@ -314,12 +476,42 @@ Matrix ShardState::A() const {
   return download_f32(a, dev->n_tok, dev->h_true, lda);
 }
 
+Matrix ShardState::Y() const {
+  if (!dev) throw std::invalid_argument("ShardState: no device state");
+  DevMem out(size_t(dev->n_tok * dev->rows) * 4);
+  check(vp_shard_logits(ctx(), &dev->batch->desc, &dev->shard->desc, static_cast<float*>(out.p), dev->rows));
+  return download_f32(out.p, dev->n_tok, dev->rows, dev->rows);
+}
+
+Matrix ShardState::B() const {
+  if (!dev) throw std::invalid_argument("ShardState: no device state");
+  if (!has_grad_terms) throw std::invalid_argument("alg2_barrier_C1: A/B terms missing");
+  if (!dev->batch->desc.labels) throw std::invalid_argument("ShardState: B needs the batch labels");
+  const int64_t ld = dev->batch->desc.h;
+  DevMem out(size_t(dev->n_tok * ld) * 4);
+  check(vp_shard_label_rows(ctx(), &dev->batch->desc, &dev->shard->desc, static_cast<float*>(out.p), ld));
+  return download_f32(out.p, dev->n_tok, dev->h_true, ld);
+}
+
+void set_placement(Placement p) { placement_ref() = p; }
+Placement placement() { return placement_ref(); }
+
 OutputResult oracle_output_layer(const TokenBatch& batch, const Matrix& W, const Vector* logit_shift) {
   check_batch(batch, W.rows());
   if (batch.X.cols() != W.cols()) throw std::invalid_argument("oracle_output_layer: X/W hidden dim mismatch");
-  if (logit_shift != nullptr)
-    throw std::invalid_argument("oracle_output_layer: logit_shift is a CPU-oracle test hook (not on device)");
-  return run(2, batch, W, 1, 1.0);
+  if (logit_shift == nullptr) return run_local(2, batch, W, 1, 1.0);
+  // the per-row logit shift hook (VM.cpp:41-43), applied in the K1 epilogue
+  if (logit_shift->size() != batch.X.rows()) throw std::invalid_argument("oracle_output_layer: logit_shift size mismatch");
+  DevPtr d = upload_f32(logit_shift->data(), 1, logit_shift->size(), logit_shift->size());
+  check(vp_ctx_set_logit_shift(ctx(), static_cast<const float*>(d->p)));
+  try {
+    OutputResult r = run_local(2, batch, W, 1, 1.0);
+    check(vp_ctx_set_logit_shift(ctx(), nullptr));
+    return r;
+  } catch (...) {
+    vp_ctx_set_logit_shift(ctx(), nullptr);
+    throw;
+  }
 }
 
 std::vector<EmbeddingShard> shard_weights(const Matrix& W, int p) {  // VM.cpp:65-80

@@ -39,10 +39,13 @@ def broadcast_bytes(payload: bytes | None, src: int = 0) -> bytes:
     return obj[0]
 
 
-def init_comm(ctx) -> None:
-    """Create the context's NCCL group: rank 0 makes the unique id, every rank joins."""
+def init_comm(ctx, loopback: bool = False) -> None:
+    """Create the context's collective group: rank 0 makes the id, every rank
+    joins.  NCCL by default; loopback=True joins the library's loopback
+    backend instead (ranks may share a GPU: dry runs of N ranks on fewer GPUs)."""
     rank, world = dist.get_rank(), dist.get_world_size()
-    uid = broadcast_bytes(ctx.unique_id() if rank == 0 else None)
+    mk = ctx.loopback_id if loopback else ctx.unique_id
+    uid = broadcast_bytes(mk() if rank == 0 else None)
     ctx.comm_init(world, rank, uid)
 
 
@@ -53,3 +56,53 @@ def max_over_ranks(x: float, device=None) -> float:
     t = torch.tensor([x], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+# ---------------------------------------------------------------------------
+# One process driving a whole group (C++-style single-process multi-rank):
+# contexts on distinct GPUs get NCCL, contexts sharing a GPU the loopback
+# backend (vp_comm_init_all).  Each rank is then driven from its own host
+# thread, on its own stream (ctypes releases the GIL during library calls).
+# ---------------------------------------------------------------------------
+def local_group(p: int, devices=None):
+    """p contexts (rank k on devices[k], default: all on the current GPU),
+    each on a fresh stream, joined into one group."""
+    from . import vocab_math as vm
+    devices = list(devices) if devices is not None else [torch.cuda.current_device()] * p
+    if len(devices) != p:
+        raise ValueError("local_group: one device per rank")
+    ctxs = []
+    for d in devices:
+        with torch.cuda.device(d):
+            s = torch.cuda.Stream(d)
+            with torch.cuda.stream(s):
+                ctxs.append(vm.Context(d))
+    vm.init_group(ctxs)
+    return ctxs
+
+
+def run_ranks(ctxs, fn):
+    """Runs fn(rank, ctx) for every rank concurrently (one thread per rank, on
+    the rank's device and stream); returns the results in rank order and
+    re-raises the first rank's exception."""
+    import threading
+    out = [None] * len(ctxs)
+    err = [None] * len(ctxs)
+
+    def body(k):
+        c = ctxs[k]
+        try:
+            with torch.cuda.device(c.device), torch.cuda.stream(c.stream):
+                out[k] = fn(k, c)
+        except BaseException as e:  # noqa: BLE001 - reported to the caller
+            err[k] = e
+
+    th = [threading.Thread(target=body, args=(k,)) for k in range(len(ctxs))]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for e in err:
+        if e is not None:
+            raise e
+    return out

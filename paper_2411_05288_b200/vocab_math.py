@@ -51,11 +51,13 @@ class Context:
         check(self.lib.vp_ctx_create(self.device, ctypes.byref(h)))
         self.handle = h
         with torch.cuda.device(self.device):
-            self.use_stream(torch.cuda.current_stream())
+            self.stream = torch.cuda.current_stream()
+            self.use_stream(self.stream)
         if cta_group != 2:
             self.set_option("cta_group", cta_group)
 
     def use_stream(self, stream: torch.cuda.Stream) -> None:
+        self.stream = stream
         check(self.lib.vp_ctx_set_stream(self.handle, ctypes.c_void_p(stream.cuda_stream)))
 
     def set_option(self, key: str, value: int) -> None:
@@ -87,6 +89,17 @@ class Context:
         check(_lib.load().vp_comm_unique_id(buf))
         return buf.raw
 
+    @staticmethod
+    def loopback_id() -> bytes:
+        """Id of a loopback group (ranks may share one GPU; see vpipe_b200.h)."""
+        buf = ctypes.create_string_buffer(128)
+        check(_lib.load().vp_comm_loopback_id(buf))
+        return buf.raw
+
+    @property
+    def comm_backend(self) -> str:
+        return self.lib.vp_ctx_comm_backend(self.handle).decode()
+
     def comm_init(self, nranks: int, rank: int, uid: bytes) -> None:
         buf = ctypes.create_string_buffer(uid, 128)
         check(self.lib.vp_ctx_comm_init(self.handle, nranks, rank, buf))
@@ -108,6 +121,13 @@ class Context:
             self.close()
         except Exception:
             pass
+
+
+def init_group(ctxs: Sequence["Context"]) -> None:
+    """vp_comm_init_all: ctxs[k] becomes rank k of one group — NCCL when the
+    contexts sit on distinct GPUs, the loopback backend when some share one."""
+    arr = (ctypes.c_void_p * len(ctxs))(*[c.handle.value for c in ctxs])
+    check(_lib.load().vp_comm_init_all(arr, len(ctxs)))
 
 
 @dataclass
@@ -420,6 +440,38 @@ def run_alg2(ctx: Context, batch: TokenBatch, shards: Sequence[EmbeddingShard], 
              states=None, outputs=None, with_softmax: bool = False) -> OutputResult:
     """VM.cpp:328-361."""
     return _run("vp_run_alg2", ctx, batch, shards, fault_scale, states, outputs, with_softmax)
+
+
+def oracle_output_layer(ctx: Context, batch: TokenBatch, W: torch.Tensor, logit_shift: Optional[torch.Tensor] = None,
+                        with_softmax: bool = False) -> OutputResult:
+    """VM.cpp:31-63: the monolithic layer (p = 1, Algorithm 2).  logit_shift
+    (fp32 [n_tok], VM.cpp:41-43) is added per row to the logits in the K1
+    epilogue; the results are shift-invariant."""
+    if logit_shift is not None:
+        _need_cuda(logit_shift, torch.float32, "logit_shift")
+        if logit_shift.numel() != batch.X.shape[0]:
+            raise ValueError("oracle_output_layer: logit_shift size mismatch")
+    check(ctx.lib.vp_ctx_set_logit_shift(ctx.handle, _p(logit_shift)))
+    try:
+        return run_alg2(ctx, batch, shard_weights(W, 1), with_softmax=with_softmax)
+    finally:
+        check(ctx.lib.vp_ctx_set_logit_shift(ctx.handle, _p(None)))
+
+
+def shard_logits(ctx: Context, batch: TokenBatch, shard: EmbeddingShard) -> torch.Tensor:
+    """ShardState::Y (VM.hpp:35) on demand: fp32 X W_k^T [n_tok, rows] (one GEMM)."""
+    out = torch.empty(batch.X.shape[0], shard.rows(), dtype=torch.float32, device=_dev(ctx))
+    b, s = batch.c(), shard.c()
+    check(ctx.lib.vp_shard_logits(ctx.handle, ctypes.byref(b), ctypes.byref(s), _p(out), out.stride(0)))
+    return out
+
+
+def shard_label_rows(ctx: Context, batch: TokenBatch, shard: EmbeddingShard) -> torch.Tensor:
+    """ShardState::B (VM.hpp:41) on demand: fp32 G_k W_k [n_tok, h]."""
+    out = torch.empty(batch.X.shape[0], batch.X.shape[1], dtype=torch.float32, device=_dev(ctx))
+    b, s = batch.c(), shard.c()
+    check(ctx.lib.vp_shard_label_rows(ctx.handle, ctypes.byref(b), ctypes.byref(s), _p(out), out.stride(0)))
+    return out
 
 
 def run_naive(ctx: Context, batch: TokenBatch, shards: Sequence[EmbeddingShard], **kw) -> OutputResult:

@@ -15,6 +15,42 @@
 
 using namespace vpipe;
 
+// The independent checker: the fp64 CPU oracle (oracle/liboracle.so, test
+// infrastructure) on the bf16-rounded operands the device computes with.
+extern "C" int or_oracle_output_layer(const double* X, const double* W, const int64_t* labels, int64_t n_tok,
+                                      int64_t h, int64_t V, const double* logit_shift, double* softmax,
+                                      double* loss, double* gx, double* gw);
+
+static double bf16_round(double v) {  // double -> float -> bf16 (RNE), as the drop-in uploads
+  float f = float(v);
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  u += 0x7fffu + ((u >> 16) & 1u);
+  u &= 0xffff0000u;
+  std::memcpy(&f, &u, 4);
+  return f;
+}
+
+static Matrix rounded(const Matrix& M) {
+  Matrix r(M.rows(), M.cols());
+  for (int64_t i = 0; i < M.size(); ++i) r.data()[i] = bf16_round(M.data()[i]);
+  return r;
+}
+
+static OutputResult cpu_oracle(const TokenBatch& batch, const Matrix& W, const Vector* shift = nullptr) {
+  const int64_t n = batch.X.rows(), h = batch.X.cols(), V = W.rows();
+  const Matrix Xb = rounded(batch.X), Wb = rounded(W);
+  OutputResult r;
+  r.softmax.resize(n, V);
+  r.loss.resize(n);
+  r.grad_x.resize(n, h);
+  r.grad_w.resize(V, h);
+  if (or_oracle_output_layer(Xb.data(), Wb.data(), batch.labels.data(), n, h, V, shift ? shift->data() : nullptr,
+                             r.softmax.data(), r.loss.data(), r.grad_x.data(), r.grad_w.data()) != 0)
+    throw std::runtime_error("cpu oracle failed");
+  return r;
+}
+
 static int failures = 0;
 static void check(bool ok, const std::string& what) {
   std::printf("[%s] %s\n", ok ? "PASS" : "FAIL", what.c_str());
@@ -53,16 +89,58 @@ int main() {
           "hand instance loss");
     check(std::fabs(r.grad_x(0, 0) - (e / (1.0 + e) - 1.0) * w) < 1e-3, "hand instance grad_x");
   }
-  {  // test_vocab_math.cpp:74-84 — the logit_shift hook is CPU-oracle only
+  {  // test_vocab_math.cpp:74-84 — per-row logit shift invariance (K1 epilogue hook)
     const RandomInstance inst = random_instance(5, 3, 6, 7);
-    Vector shift = Vector::Constant(5, 1.0);
-    bool threw = false;
-    try {
-      oracle_output_layer(inst.batch, inst.W, &shift);
-    } catch (const std::invalid_argument&) {
-      threw = true;
+    const OutputResult base = oracle_output_layer(inst.batch, inst.W);
+    Vector shift(5);
+    shift(0) = 3.0;
+    shift(1) = -40.0;
+    shift(2) = 0.5;
+    shift(3) = 17.0;
+    shift(4) = -2.25;
+    const OutputResult shifted = oracle_output_layer(inst.batch, inst.W, &shift);
+    check(shifted.softmax.maxAbsDiff(base.softmax) < 4e-3 && shifted.loss.maxAbsDiff(base.loss) < 1e-3 &&
+              rel_l2(shifted.grad_x, base.grad_x) < 1e-2,
+          "logit_shift: softmax / loss / grad_x invariant under per-row shifts");
+    check(close_results(shifted, cpu_oracle(inst.batch, inst.W, &shift)), "logit_shift: device == CPU oracle");
+  }
+  {  // ShardState::Y and ::B (VM.hpp:35, :41) materialised on demand
+    const RandomInstance inst = random_instance(9, 16, 24, 5);
+    const auto shards = shard_weights(inst.W, 3);
+    const ShardState st = alg2_pass_S(inst.batch, shards[1]);
+    const Matrix Y = st.Y(), B = st.B();
+    const Matrix Xb = rounded(inst.batch.X), Wb = rounded(inst.W);
+    double ye = 0, be = 0;
+    for (int64_t i = 0; i < 9; ++i) {
+      for (int64_t v = 0; v < shards[1].rows(); ++v) {
+        double y = 0;
+        for (int64_t j = 0; j < 16; ++j) y += Xb(i, j) * Wb(shards[1].row_begin + v, j);
+        ye = std::max(ye, std::fabs(Y(i, v) - y));
+      }
+      const int64_t g = inst.batch.labels[size_t(i)];
+      for (int64_t j = 0; j < 16; ++j) be = std::max(be, std::fabs(B(i, j) - (shards[1].owns(g) ? Wb(g, j) : 0.0)));
     }
-    check(threw, "logit_shift hook rejected on device (invalid_argument)");
+    check(Y.rows() == 9 && Y.cols() == 8 && ye < 1e-4, "ShardState::Y == X W_k^T (fp32 logits)");
+    check(B.rows() == 9 && B.cols() == 16 && be == 0.0, "ShardState::B == G_k W_k (owned label rows)");
+  }
+  {  // the drop-in's monolithic layer against the independent CPU oracle
+    const RandomInstance inst = random_instance(24, 40, 72, 11);
+    check(close_results(oracle_output_layer(inst.batch, inst.W), cpu_oracle(inst.batch, inst.W)),
+          "oracle_output_layer (device, p = 1) == CPU oracle");
+  }
+  {  // p ranks on one GPU through the loopback backend (Placement::Loopback):
+     // the library's multi-rank paths, one context + host thread per shard
+    const RandomInstance inst = random_instance(16, 24, 64, 21);
+    const OutputResult ref = cpu_oracle(inst.batch, inst.W);
+    set_placement(Placement::Loopback);
+    bool ok = true;
+    for (int p : {2, 4}) {
+      ok = ok && close_results(run_naive(inst.batch, inst.W, p), ref);
+      ok = ok && close_results(run_alg1(inst.batch, inst.W, p), ref);
+      ok = ok && close_results(run_alg2(inst.batch, inst.W, p), ref);
+    }
+    set_placement(Placement::Auto);
+    check(ok, "Placement::Loopback: naive/alg1/alg2 at p = 2, 4 ranks == CPU oracle");
   }
   {  // test_vocab_math.cpp:86-106 — sharded pipelines vs the monolithic layer
     int bad = 0, total = 0;
@@ -74,19 +152,19 @@ int main() {
               if (V % p) continue;
               for (uint64_t seed : {0u, 1u}) {
                 const RandomInstance inst = random_instance(b * s, h, V, seed);
-                const OutputResult mono = oracle_output_layer(inst.batch, inst.W);
+                const OutputResult mono = cpu_oracle(inst.batch, inst.W);
                 total += 3;
                 bad += !close_results(run_naive(inst.batch, inst.W, p), mono);
                 bad += !close_results(run_alg1(inst.batch, inst.W, p), mono);
                 bad += !close_results(run_alg2(inst.batch, inst.W, p), mono);
               }
             }
-    check(bad == 0, "grid: naive/alg1/alg2 at p shards match the monolithic layer (" + std::to_string(total) +
+    check(bad == 0, "grid: naive/alg1/alg2 at p shards match the CPU oracle (" + std::to_string(total) +
                         " runs, " + std::to_string(bad) + " off)");
   }
   {  // test_vocab_math.cpp:108-114 — fault injection is detected
     const RandomInstance inst = random_instance(8, 4, 16, 3);
-    const OutputResult mono = oracle_output_layer(inst.batch, inst.W);
+    const OutputResult mono = cpu_oracle(inst.batch, inst.W);
     check(!close_results(run_alg1(inst.batch, inst.W, 4, 1.01), mono), "alg1 fault_scale 1.01 detected");
     check(!close_results(run_alg2(inst.batch, inst.W, 4, 1.01), mono), "alg2 fault_scale 1.01 detected");
   }

@@ -40,7 +40,7 @@ def test_verify_cli_contract():
     _build()
     r = _verify("--seed", "0")
     assert r.returncode == 0, r.stdout + r.stderr
-    assert r.stdout.count("PASS") == 4
+    assert r.stdout.count("PASS") == 5  # device oracle, naive, alg1, alg2 vs the CPU oracle + input layer
     r = _verify("--devices", "1")
     assert r.returncode == 0, r.stdout + r.stderr
     r = _verify("--fault-scale", "1.01")
@@ -50,3 +50,22 @@ def test_verify_cli_contract():
     assert r.returncode == 0, r.stdout + r.stderr
     r = _verify("--hidden", "4096", "--vocab", "128256", "--devices", "8", "--batch", "1", "--seq-len", "16")
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+@pytest.mark.gpu
+def test_verify_detects_a_corrupted_logits_kernel():
+    # a fault common to every p (K1 logits scaled by 1 + 2e-3) must fail
+    # against the independent CPU oracle
+    _build()
+    r = _verify("--inject-k1-fault", "2000", "--hidden", "64", "--vocab", "256")
+    assert r.returncode == 1, r.stdout + r.stderr
+    assert any(line.startswith("alg2") and line.endswith("FAIL") for line in r.stdout.splitlines())
+    assert any(line.startswith("device_oracle") and line.endswith("FAIL") for line in r.stdout.splitlines())
+
+
+@pytest.mark.gpu
+def test_verify_with_ranks_through_the_loopback_backend():
+    _build()
+    for p in ("2", "4"):
+        r = _verify("--placement", "loopback", "--devices", p, "--hidden", "64", "--vocab", "512")
+        assert r.returncode == 0, r.stdout + r.stderr

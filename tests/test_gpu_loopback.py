@@ -1,0 +1,252 @@
+"""GPU: the library's nranks > 1 code paths, run for real on one B200.
+
+p contexts on cuda:0 form one group through the loopback collective backend
+(vp_comm_init_all -> device mailboxes + host rendezvous), each rank driven from
+its own host thread and stream with ONE vocabulary shard — exactly what a
+torchrun rank does with NCCL: rank-offset shards, the [N x 2T] stats
+all-gather and fixed-order merge, owner-only loss + sum all-reduce, the dX
+all-reduce (forked onto the comm stream in alg2), alg1's C2, naive's max / sum
+all-reduces, the input layer's forward all-reduce, and the executor's C0
+broadcast / C1 / C2 with one program device per rank.  Results are checked
+against the CPU oracle at the north_star tolerances (input layer bit-exact),
+and every rank must hold bitwise the same loss / grad_x / stats.
+"""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from gpu_helpers import GRAD_REL_L2, LOSS_ABS, assert_parity, device_case, oracle, rel_l2
+from paper_2411_05288_b200 import dist as vpd
+from paper_2411_05288_b200 import vocab_math as vm
+
+pytestmark = pytest.mark.gpu
+
+os.environ.setdefault("VPIPE_LOOPBACK_TIMEOUT", "120")  # a failing rank must not hang the others forever
+
+
+def _shard(Wd, p, r):
+    rb, re = vpd.shard_rows(Wd.shape[0], p, r)
+    return vm.EmbeddingShard(Wd[rb:re], r, rb, re)
+
+
+def _close(ctxs):
+    for c in ctxs:
+        c.sync()
+    for c in ctxs:
+        c.close()
+
+
+def _same_on_every_rank(outs, key):
+    for o in outs[1:]:
+        assert torch.equal(getattr(o, key), getattr(outs[0], key)), key
+
+
+@pytest.mark.parametrize("p", [2, 4, 8])
+@pytest.mark.parametrize("alg", ["naive", "alg1", "alg2"])
+def test_drivers_with_p_ranks_match_the_oracle(alg, p):
+    T, h, V = 96, 64, 512 * p
+    X, W, g = oracle.random_instance(T, h, V, 10 + p)
+    Xb, Wb, batch, Wd = device_case(X, W, g)
+    ref = oracle.oracle_output_layer(Xb, g, Wb, want_softmax=False)
+    torch.cuda.synchronize()
+    ctxs = vpd.local_group(p)
+    assert all(c.comm_backend == "loopback" for c in ctxs)
+    assert [c.comm_info() for c in ctxs] == [(p, r) for r in range(p)]
+    fn = {"naive": vm.run_naive, "alg1": vm.run_alg1, "alg2": vm.run_alg2}[alg]
+
+    def rank(r, ctx):
+        out = fn(ctx, batch, [_shard(Wd, p, r)])
+        ctx.sync()
+        return out
+
+    outs = vpd.run_ranks(ctxs, rank)
+    for key in ("loss", "grad_x"):
+        _same_on_every_rank(outs, key)
+    for o in outs[1:]:
+        assert torch.equal(o.stats.m, outs[0].stats.m) and torch.equal(o.stats.sum, outs[0].stats.sum)
+    res = {"loss": outs[0].loss.double().cpu().numpy(), "grad_x": outs[0].grad_x[:, :h].double().cpu().numpy(),
+           "grad_w": torch.cat([o.grad_w[0] for o in outs])[:, :h].double().cpu().numpy()}
+    assert_parity(res, ref, f"loopback p={p} {alg}")
+    _close(ctxs)
+
+
+def test_loopback_equals_local_shards():
+    # the same 4 shards run as 4 ranks and as 4 local shards of one context
+    p, T, h, V = 4, 64, 128, 2048
+    X, W, g = oracle.random_instance(T, h, V, 3)
+    _, _, batch, Wd = device_case(X, W, g)
+    local_ctx = vm.Context(0)
+    local = vm.run_alg2(local_ctx, batch, vm.shard_weights(Wd, p))
+    local_ctx.sync()
+    torch.cuda.synchronize()
+    ctxs = vpd.local_group(p)
+    outs = vpd.run_ranks(ctxs, lambda r, c: vm.run_alg2(c, batch, [_shard(Wd, p, r)]))
+    for c in ctxs:
+        c.sync()
+    assert torch.equal(outs[0].loss, local.loss)
+    assert torch.equal(outs[0].stats.m, local.stats.m) and torch.equal(outs[0].stats.sum, local.stats.sum)
+    assert torch.allclose(outs[0].grad_x, local.grad_x, rtol=1e-5, atol=1e-6)
+    assert torch.allclose(torch.cat([o.grad_w[0] for o in outs]), local.grad_w_full(), rtol=1e-5, atol=1e-6)
+    _close(ctxs)
+    local_ctx.close()
+
+
+@pytest.mark.parametrize("p", [2, 8])
+def test_pass_functions_across_ranks(p):
+    # alg2: S -> C1 (all-gather merge + combine + dX all-reduce) -> T;
+    # alg1: S -> merge_max_sum (all-gather) -> T -> reduce_grad_x (C2 all-reduce)
+    T, h, V = 40, 32, 64 * p
+    X, W, g = oracle.random_instance(T, h, V, 5)
+    Xb, Wb, batch, Wd = device_case(X, W, g)
+    ref = oracle.oracle_output_layer(Xb, g, Wb, want_softmax=False)
+    torch.cuda.synchronize()
+    ctxs = vpd.local_group(p)
+
+    def rank(r, ctx):
+        sh = _shard(Wd, p, r)
+        st = vm.alg2_pass_S(ctx, batch, sh)
+        c1 = vm.alg2_barrier_C1(ctx, [st], [sh], batch)
+        gw2 = vm.alg2_pass_T(ctx, st, c1.stats, batch, sh)
+        loss = vm.output_loss(ctx, [st], [sh], c1.stats, batch)  # owner-only + sum all-reduce
+        st1 = vm.alg1_pass_S(ctx, batch, sh)
+        stats1 = vm.merge_max_sum(ctx, [st1])
+        gr = vm.alg1_pass_T(ctx, st1, stats1, batch, sh)
+        gx1 = vm.reduce_grad_x(ctx, [gr.grad_x_partial])
+        ctx.sync()
+        return c1, gw2, loss, stats1, gr, gx1
+
+    outs = vpd.run_ranks(ctxs, rank)
+    for o in outs[1:]:
+        assert torch.equal(o[0].grad_x, outs[0][0].grad_x)
+        assert torch.equal(o[2], outs[0][2])
+        assert torch.equal(o[3].m, outs[0][3].m) and torch.equal(o[3].sum, outs[0][3].sum)
+        assert torch.equal(o[5], outs[0][5])
+    assert np.abs(outs[0][2].double().cpu().numpy() - ref.loss).max() <= LOSS_ABS
+    assert rel_l2(outs[0][0].grad_x[:, :h].cpu().numpy(), ref.grad_x) <= GRAD_REL_L2
+    assert rel_l2(outs[0][5][:, :h].cpu().numpy(), ref.grad_x) <= GRAD_REL_L2
+    gw = lambda i: torch.cat([o[i] if i == 1 else o[i].grad_w for o in outs])[:, :h].cpu().numpy()  # noqa: E731
+    assert rel_l2(gw(1), ref.grad_w) <= GRAD_REL_L2
+    assert rel_l2(gw(4), ref.grad_w) <= GRAD_REL_L2
+    # the stats all-gather + merge equals the oracle's merge of the local stats
+    m_ref, s_ref = oracle.merge_max_sum(*zip(*[oracle.local_stats(Xb, Wb, p, k) for k in range(p)]))
+    assert np.abs(outs[0][3].m.cpu().numpy() - m_ref).max() < 1e-4
+    assert rel_l2(outs[0][3].sum.cpu().numpy(), s_ref) < 1e-3
+    _close(ctxs)
+
+
+@pytest.mark.parametrize("p", [2, 4, 8])
+def test_input_layer_across_ranks_is_bit_exact(p):
+    # forward: masked gather of each rank's shard + bf16 sum all-reduce
+    # (x + 0 = x: bit-exact); backward: each rank's shard gradient
+    V, h, T = 1024 * p, 256, 2000
+    rng = np.random.default_rng(p)
+    W = torch.from_numpy(rng.standard_normal((V, h)).astype(np.float32)).to(torch.bfloat16).cuda()
+    tok = torch.from_numpy(rng.integers(0, V, T)).cuda()
+    tok[:50] = 7  # a repeated row
+    grad = torch.from_numpy(rng.standard_normal((T, h)).astype(np.float32)).to(torch.bfloat16).cuda()
+    torch.cuda.synchronize()
+    ctxs = vpd.local_group(p)
+
+    def rank(r, ctx):
+        sh = _shard(W, p, r)
+        out = vm.input_forward(ctx, tok, sh)
+        vm.allreduce_sum(ctx, out)
+        dE = vm.input_backward(ctx, grad, tok, sh)
+        ctx.sync()
+        return out, dE
+
+    outs = vpd.run_ranks(ctxs, rank)
+    want = W[tok]
+    for out, _ in outs:
+        assert torch.equal(out, want)
+    g_np = grad.float().cpu().numpy()
+    t_np = tok.cpu().numpy()
+    for r, (_, dE) in enumerate(outs):
+        rb, re = vpd.shard_rows(V, p, r)
+        assert np.array_equal(dE.cpu().numpy(), oracle.input_backward_f32(g_np, t_np, re - rb, rb))
+    _close(ctxs)
+
+
+def test_label_out_of_range_raises_on_every_rank():
+    # VM.cpp:18: labels must lie in [0, V); V is the group's largest row_end
+    p, T, h, V = 2, 16, 32, 256
+    X, W, g = oracle.random_instance(T, h, V, 2)
+    g = g.copy()
+    g[3] = V  # owned by no shard
+    _, _, batch, Wd = device_case(X, W, g)
+    torch.cuda.synchronize()
+    ctxs = vpd.local_group(p)
+
+    def rank(r, ctx):
+        vm.run_alg2(ctx, batch, [_shard(Wd, p, r)])
+        with pytest.raises(ValueError, match="label out of range"):
+            ctx.sync()
+        return True
+
+    assert all(vpd.run_ranks(ctxs, rank))
+    _close(ctxs)
+
+
+@pytest.mark.parametrize("name", ["vocab2_p2_n4", "vocab2_p4_n8", "vocab1_p2_n4", "interlaced_p4_n8"])
+def test_executor_one_program_device_per_rank(name):
+    # vp_program_run in a group: rank k executes device k's pass list (C0
+    # broadcast of X_i from device p-1, C1 / C2 exchanges on the comm stream)
+    import json
+    golden = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "programs.json")))
+    prog = vm.Program(golden[name]["text"])
+    p, n = prog.p, prog.n
+    T, h, V = 48, 64, 96 * p
+    W = None
+    mbs = []
+    for i in range(n):
+        X, W_i, g = oracle.random_instance(T, h, V, 200 + i)
+        W = W_i if W is None else W
+        mbs.append(device_case(X, W, g))
+    Wd = mbs[0][3]
+    # local reference: every program device on one context
+    lctx = vm.Context(0)
+    local = vm.run_program(lctx, prog, [m[2] for m in mbs], vm.shard_weights(Wd, p))
+    lctx.sync()
+    torch.cuda.synchronize()
+    ctxs = vpd.local_group(p)
+
+    def rank(r, ctx):
+        # C0 broadcasts X_i from device p-1: the other ranks start from garbage
+        batches = [vm.TokenBatch(m[2].X.clone() if r == p - 1 else torch.zeros_like(m[2].X), m[2].labels)
+                   for m in mbs]
+        res = vm.run_program(ctx, prog, batches, [_shard(Wd, p, r)])
+        ctx.sync()
+        return res, batches
+
+    outs = vpd.run_ranks(ctxs, rank)
+    for r, (res, batches) in enumerate(outs):
+        for i in range(n):
+            assert torch.equal(batches[i].X, mbs[i][2].X)  # C0 delivered X_i
+            assert torch.equal(res.loss[i], outs[0][0].loss[i])
+            assert torch.equal(res.grad_x[i], outs[0][0].grad_x[i])
+            assert torch.allclose(res.loss[i], local.loss[i], rtol=1e-5, atol=1e-6)
+            assert torch.allclose(res.grad_x[i], local.grad_x[i], rtol=1e-4, atol=1e-6)
+        assert torch.allclose(res.grad_w[0], local.grad_w[r], rtol=1e-4, atol=1e-6)
+    gw_ref = 0
+    for i, (Xb, Wb, _, _) in enumerate(mbs):
+        ref = oracle.oracle_output_layer(Xb, mbs[i][2].labels.cpu().numpy(), Wb, want_softmax=False)
+        assert np.abs(outs[0][0].loss[i].double().cpu().numpy() - ref.loss).max() <= LOSS_ABS
+        gw_ref = gw_ref + ref.grad_w
+    got = torch.cat([o[0].grad_w[0] for o in outs])[:, :h].cpu().numpy()
+    assert rel_l2(got, gw_ref) <= GRAD_REL_L2
+    _close(ctxs)
+    lctx.close()
+
+
+def test_loopback_group_cannot_be_captured():
+    ctxs = vpd.local_group(2)
+
+    def rank(r, ctx):
+        with pytest.raises(ValueError, match="cannot be captured"):
+            vm.capture(ctx, lambda: None)
+        return True
+
+    assert all(vpd.run_ranks(ctxs, rank))
+    _close(ctxs)

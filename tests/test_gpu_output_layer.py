@@ -409,3 +409,48 @@ def test_tiny_and_ragged_token_counts(ctx, T):
         for p in (1, 2):
             res, _ = run_device(ctx, alg, batch, Wd, p, 64)
             assert_parity(res, ref, f"T={T} {alg} p={p}")
+
+
+def test_logit_shift_hook_is_invariant_and_matches_the_oracle(ctx):
+    # test_vocab_math.cpp:74-84 against the drop-in: the shift is added per row
+    # inside the K1 epilogue (vp_ctx_set_logit_shift)
+    X, W, g = oracle.random_instance(5, 3, 6, 7)
+    Xb, Wb, batch, Wd = device_case(X, W, g)
+    shift = np.array([3.0, -40.0, 0.5, 17.0, -2.25])
+    base = vm.oracle_output_layer(ctx, batch, Wd, with_softmax=True)
+    shifted = vm.oracle_output_layer(ctx, batch, Wd, torch.tensor(shift, dtype=torch.float32, device="cuda"),
+                                     with_softmax=True)
+    ctx.sync()
+    assert (shifted.softmax - base.softmax).abs().max().item() < 4e-3
+    assert (shifted.loss - base.loss).abs().max().item() < 1e-3
+    assert rel_l2(shifted.grad_x[:, :3].cpu().numpy(), base.grad_x[:, :3].cpu().numpy()) < 1e-2
+    ref = oracle.oracle_output_layer(Xb, g, Wb, logit_shift=shift)
+    res = {"loss": shifted.loss.double().cpu().numpy(), "grad_x": shifted.grad_x[:, :3].double().cpu().numpy(),
+           "grad_w": shifted.grad_w_full()[:, :3].double().cpu().numpy(),
+           "softmax": shifted.softmax.double().cpu().numpy()}
+    assert_parity(res, ref, "logit_shift")
+    # a large shift on the headline-style path (h = 512, V = 4096, 4 tiles / row)
+    X, W, g = oracle.random_instance(64, 512, 4096, 8)
+    Xb, Wb, batch, Wd = device_case(X, W, g)
+    shift = np.linspace(-60.0, 60.0, 64)
+    out = vm.oracle_output_layer(ctx, batch, Wd, torch.tensor(shift, dtype=torch.float32, device="cuda"))
+    ctx.sync()
+    ref = oracle.oracle_output_layer(Xb, g, Wb, logit_shift=shift, want_softmax=False)
+    assert_parity({"loss": out.loss.double().cpu().numpy(), "grad_x": out.grad_x.double().cpu().numpy(),
+                   "grad_w": out.grad_w_full().double().cpu().numpy()}, ref, "logit_shift h=512")
+
+
+def test_shard_state_Y_and_B_on_demand(ctx):
+    X, W, g = oracle.random_instance(33, 48, 300, 12)
+    Xb, Wb, batch, Wd = device_case(X, W, g)
+    shards = vm.shard_weights(Wd, 3)
+    for s in shards:
+        Y = vm.shard_logits(ctx, batch, s)
+        B = vm.shard_label_rows(ctx, batch, s)
+        ctx.sync()
+        Yref = Xb @ Wb[s.row_begin:s.row_end].T
+        assert np.abs(Y.double().cpu().numpy() - Yref).max() < 1e-4
+        Bref = np.zeros_like(Xb)
+        own = (g >= s.row_begin) & (g < s.row_end)
+        Bref[own] = Wb[g[own]]
+        assert np.array_equal(B.double().cpu().numpy(), Bref)

@@ -3,22 +3,35 @@
 //
 //   vpipe_verify [--batch B] [--seq-len S] [--hidden H] [--vocab V]
 //                [--devices P] [--seed N] [--fault-scale F]
+//                [--placement auto|local|spread|loopback] [--inject-k1-fault PPM]
 //
 // Same defaults (b=2, s=4, h=8, V=32, p=4; vpipe_main.cpp:285-287), same flow
-// (pad V to a multiple of 2p, random_instance, monolithic output layer, then
-// naive / alg1 / alg2 at p shards and the input layer), same exit codes
-// (0 pass, 1 verify failure, 2 usage / invalid argument).  The comparison is
-// at the north_star's bf16 tolerances instead of 1e-10: per-token loss
-// <= 1e-3 abs, softmax <= 4e-3 abs, grad_x / grad_w <= 1e-2 relative L2;
-// the input layer forward must be exact.
+// (pad V to a multiple of 2p, random_instance, naive / alg1 / alg2 at p shards
+// and the input layer), same exit codes (0 pass, 1 verify failure, 2 usage /
+// invalid argument).  The reference result comes from an INDEPENDENT checker:
+// the fp64 CPU oracle (oracle/liboracle.so, a restatement of VM.cpp — test
+// infrastructure, linked by this tool only) on the same bf16-rounded
+// operands the device sees; the device's own monolithic oracle_output_layer
+// is checked against it too.  Tolerances are the north_star's bf16 ones:
+// per-token loss <= 1e-3 abs, softmax <= 4e-3 abs, grad_x / grad_w <= 1e-2
+// relative L2; the input-layer forward must be exact.
+// --inject-k1-fault PPM scales every pass-S logit by 1 + PPM * 1e-6 inside the
+// K1 epilogue (a fault common to every p) — verify must then exit 1.
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "vpipe/vocab_math.hpp"
+
+// CPU oracle (oracle/vocab_oracle.cpp): the checker, never the product.
+extern "C" int or_oracle_output_layer(const double* X, const double* W, const int64_t* labels, int64_t n_tok,
+                                      int64_t h, int64_t V, const double* logit_shift, double* softmax,
+                                      double* loss, double* gx, double* gw);
+extern "C" const char* or_last_error(void);
 
 namespace {
 
@@ -34,9 +47,38 @@ double rel_l2(const vpipe::Matrix& a, const vpipe::Matrix& b) {
   return std::sqrt(num / (den > 0 ? den : 1e-300));
 }
 
+// The value the device computes with: double -> float -> bf16 (RNE), as the
+// drop-in's upload does.
+double bf16_round(double v) {
+  float f = float(v);
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  u += 0x7fffu + ((u >> 16) & 1u);
+  u &= 0xffff0000u;
+  std::memcpy(&f, &u, 4);
+  return f;
+}
+
+vpipe::OutputResult cpu_oracle(const vpipe::TokenBatch& batch, const vpipe::Matrix& W) {
+  const int64_t n = batch.X.rows(), h = batch.X.cols(), V = W.rows();
+  vpipe::Matrix Xb(n, h), Wb(V, h);
+  for (int64_t i = 0; i < Xb.size(); ++i) Xb.data()[i] = bf16_round(batch.X.data()[i]);
+  for (int64_t i = 0; i < Wb.size(); ++i) Wb.data()[i] = bf16_round(W.data()[i]);
+  vpipe::OutputResult r;
+  r.softmax.resize(n, V);
+  r.loss.resize(n);
+  r.grad_x.resize(n, h);
+  r.grad_w.resize(V, h);
+  if (or_oracle_output_layer(Xb.data(), Wb.data(), batch.labels.data(), n, h, V, nullptr, r.softmax.data(),
+                             r.loss.data(), r.grad_x.data(), r.grad_w.data()) != 0)
+    throw std::invalid_argument(or_last_error());
+  return r;
+}
+
 int usage(const char* msg) {
   std::fprintf(stderr, "vpipe_verify: %s\nusage: vpipe_verify [--batch B] [--seq-len S] [--hidden H] [--vocab V] "
-                       "[--devices P] [--seed N] [--fault-scale F]\n", msg);
+                       "[--devices P] [--seed N] [--fault-scale F] [--placement auto|local|spread|loopback] "
+                       "[--inject-k1-fault PPM]\n", msg);
   return kExitUsage;
 }
 
@@ -57,18 +99,27 @@ int main(int argc, char** argv) {
     else if (a == "--devices") p = std::atoll(v);
     else if (a == "--seed") seed = std::strtoull(v, nullptr, 10);
     else if (a == "--fault-scale") fault = std::atof(v);
-    else return usage(("unknown option " + a).c_str());
+    else if (a == "--inject-k1-fault") setenv("VPIPE_INJECT_K1_FAULT_PPM", v, 1);
+    else if (a == "--placement") {
+      const std::string pl = v;
+      if (pl == "auto") vpipe::set_placement(vpipe::Placement::Auto);
+      else if (pl == "local") vpipe::set_placement(vpipe::Placement::Local);
+      else if (pl == "spread") vpipe::set_placement(vpipe::Placement::Spread);
+      else if (pl == "loopback") vpipe::set_placement(vpipe::Placement::Loopback);
+      else return usage(("unknown placement " + pl).c_str());
+    } else return usage(("unknown option " + a).c_str());
   }
   try {
     const int64_t n_tok = b * s;
     const int64_t Vp = vpipe::pad_vocab_size(V, p);
     const vpipe::RandomInstance inst = vpipe::random_instance(n_tok, h, Vp, seed);
-    const vpipe::OutputResult oracle = vpipe::oracle_output_layer(inst.batch, inst.W);
+    const vpipe::OutputResult oracle = cpu_oracle(inst.batch, inst.W);
     struct Case {
       const char* name;
       vpipe::OutputResult r;
     };
     const Case cases[] = {
+        {"device_oracle", vpipe::oracle_output_layer(inst.batch, inst.W)},
         {"naive", vpipe::run_naive(inst.batch, inst.W, int(p))},
         {"alg1", vpipe::run_alg1(inst.batch, inst.W, int(p), fault)},
         {"alg2", vpipe::run_alg2(inst.batch, inst.W, int(p), fault)},
