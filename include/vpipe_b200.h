@@ -111,8 +111,6 @@ int vp_ctx_reserve(vp_ctx_t ctx, int64_t n_tok, int64_t h, int p);
  * "cooperative" (1 = persistent GEMMs launched cooperatively, so the whole grid
  * is co-resident, which their cross-CTA waits rely on when kernels of other
  * streams hold SMs; default 1; process-wide),
- * "scatter_threads" (64 / 128 / 256 threads per block of the sort-free
- * scatter-add; default 256; process-wide),
  * "tma_store" (1 = GEMM epilogues store through smem staging + TMA, the
  * default; 0 = per-thread st.global; process-wide),
  * "debug_logit_scale_ppm" (fault injection for verification tools: pass-S

@@ -17,6 +17,7 @@
 #include "comm.h"
 #include "common.h"
 #include "gemm_host.cuh"
+#include "scatter_kernels.cuh"
 #include "vocab_kernels.cuh"
 #include "vocab_program.h"
 
@@ -330,25 +331,56 @@ float* global_scale(vp_ctx_s* c, const vp_state_s* st, vp_stats_t g) {
   return sc;
 }
 
-int g_scatter_threads = 256;  // threads per block of k_scatter_rows (option "scatter_threads"; 64/128/256 measured equal)
-
 // dst[row] (+)= sign * src[i] over owned tokens, ascending i per row
-// (sort-free: row heads + multiplicities, then one warp per row head).
+// (scatter_kernels.cuh: counting sort into per-row segments, ordered
+// segments, then row / hot-chunk adds).
 template <typename Src>
 void segment_scatter(vp_ctx_s* c, const int64_t* tok, int64_t n, int64_t rb, int64_t re, const Src* src, int64_t lds,
                      int64_t h, float sign, float* dst, int64_t ldd, int accumulate, int err_bit = 0) {
   if (n == 0) return;
+  require(n < (int64_t(1) << 24), "scatter: at most 2^24 tokens per call");
   const int64_t rows = re - rb;
-  auto* head = c->buf<unsigned>(c->heads, size_t(rows));
-  auto* cnt = c->buf<int>(c->counts, size_t(rows));
-  VP_CUDA(cudaMemsetAsync(head, 0xFF, size_t(rows) * sizeof(unsigned), c->stream));
-  VP_CUDA(cudaMemsetAsync(cnt, 0, size_t(rows) * sizeof(int), c->stream));
-  vp::k_row_heads<<<c->grid_for(n, 256), 256, 0, c->stream>>>(tok, int(n), rb, re, head, cnt, c->d_err, err_bit);
+  const int nchunks = int(ceil_div(h, vp::kScChunk));
+  const int64_t hot_cap = ceil_div(n, vp::kScHot) * nchunks;
+  // zeroed: cnt, headr, fill, seg [rows each] + counters
+  int* z = c->buf<int>(c->heads, size_t(4 * rows + vp::kScCtrs));
+  // lists: list [n], uni int2 [n], small int4 [n], rep int4 [n], hot int4 [hot_cap]
+  int* L = c->buf<int>(c->counts, size_t(n + 2 * n + 4 * n + 4 * n + 4 * hot_cap) + 4);
+  vp::ScatterWs w;
+  w.cnt = z;
+  w.headr = z + rows;
+  w.fill = z + 2 * rows;
+  w.seg = z + 3 * rows;
+  w.ctr = z + 4 * rows;
+  w.list = L;
+  int* q = L + n;
+  q += (reinterpret_cast<uintptr_t>(q) & 15) ? (16 - (reinterpret_cast<uintptr_t>(q) & 15)) / 4 : 0;  // int4 alignment
+  w.small = reinterpret_cast<int4*>(q);
+  w.rep = w.small + n;
+  w.hot = w.rep + n;
+  w.uni = reinterpret_cast<int2*>(w.hot + hot_cap);
+  w.hot_cap = int(hot_cap);
+  VP_CUDA(cudaMemsetAsync(z, 0, size_t(4 * rows + vp::kScCtrs) * sizeof(int), c->stream));
+  const int g = c->grid_for(n, 256);
+  vp::k_sc_count<<<g, 256, 0, c->stream>>>(tok, int(n), rb, re, w, c->d_err, err_bit);
   VP_KCHECK();
-  vp::k_scatter_rows<Src><<<unsigned(n), g_scatter_threads, 0, c->stream>>>(
-      tok, int(n), rb, re, head, cnt, src, lds, int(h), sign, dst, ldd, accumulate);
+  vp::k_sc_plan<<<g, 256, 0, c->stream>>>(tok, int(n), rb, re, nchunks, w);
   VP_KCHECK();
-  c->launches += 2;
+  vp::k_sc_fill<<<g, 256, 0, c->stream>>>(tok, int(n), rb, re, w);
+  VP_KCHECK();
+  const size_t bits = size_t((n + 31) / 32) * sizeof(unsigned);
+  require(bits <= 200 * 1024, "scatter: token count too large for the segment sort");
+  static bool sort_attr = false;
+  if (!sort_attr && bits > 48 * 1024) {
+    VP_CUDA(cudaFuncSetAttribute(vp::k_sc_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    sort_attr = true;
+  }
+  vp::k_sc_sort<<<c->num_sms * 2, vp::kScThreads, bits, c->stream>>>(int(n), w);
+  VP_KCHECK();
+  vp::k_sc_apply<Src><<<unsigned(hot_cap + n), vp::kScThreads, vp::kScRingBytes, c->stream>>>(
+      w, src, lds, int(h), sign, dst, ldd, accumulate);
+  VP_KCHECK();
+  c->launches += 5;
 }
 
 // alg1_pass_S (VM.cpp:151-162): Y = X W_k^T with the fused stats epilogue
@@ -1041,9 +1073,6 @@ int vp_ctx_set_option(vp_ctx_t c, const char* key, int64_t value) {
     } else if (k == "lockstep_logits" || k == "lockstep_dx" || k == "lockstep_dw") {
       require(value >= 0 && value <= 4096, "vp_ctx_set_option: lockstep epoch must be in 0..4096 k-blocks");
       c->lock_epoch[k == "lockstep_logits" ? 0 : k == "lockstep_dx" ? 1 : 2] = int(value);
-    } else if (k == "scatter_threads") {
-      require(value == 64 || value == 128 || value == 256, "vp_ctx_set_option: scatter_threads must be 64, 128 or 256");
-      g_scatter_threads = int(value);
     } else if (k == "l2_promotion") {
       require(value >= 0 && value <= 3, "vp_ctx_set_option: l2_promotion must be 0..3");
       vp::g_l2_promotion = int(value);

@@ -504,143 +504,4 @@ __global__ void k_input_forward(const int64_t* __restrict__ tok, int n, const __
   }
 }
 
-// ---------------------------------------------------------------------------
-// Sort-free deterministic scatter-add (input_backward VM.cpp:238-251 and the
-// -G_k^T X correction of dW): dst[row,:] (+)= sign * src[i,:] over the owned
-// tokens i, accumulated per row in ascending i (the reference's order).
-//   k_row_heads: head[row] = min i with that row, cnt[row] = multiplicity
-//                (both arrays [rows], reset by the caller: 0xFF.. / 0).
-//   k_scatter_rows: one block per token; only a row's head works.  A unique
-//                row (the common case: 16384 ids over 256000 rows) is a plain
-//                vectorised row copy/add; a repeated row's head collects its
-//                later occurrences in ascending order (ballot scan over the
-//                ids) in batches of 32 and adds them in that order.
-// Replaces a bitonic sort of (row, i) keys (2 launches instead of ~12; about
-// the same time: the sorted scatter wrote rows in order, this one does not).
-// ---------------------------------------------------------------------------
-__global__ void k_row_heads(const int64_t* __restrict__ tok, int n, int64_t rb, int64_t re,
-                            unsigned* __restrict__ head, int* __restrict__ cnt, int* __restrict__ err, int err_bit) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const int64_t t = tok[i];
-    if (t < 0 && err_bit) atomicOr(err, err_bit);
-    if (t >= rb && t < re) {
-      atomicMin(head + (t - rb), unsigned(i));
-      atomicAdd(cnt + (t - rb), 1);
-    }
-  }
-}
-
-template <typename Src>
-__device__ __forceinline__ float4 load4(const Src* p) {
-  if constexpr (sizeof(Src) == 2) {
-    const __nv_bfloat162* q = reinterpret_cast<const __nv_bfloat162*>(p);
-    const float2 a = __bfloat1622float2(q[0]), b = __bfloat1622float2(q[1]);
-    return make_float4(a.x, a.y, b.x, b.y);
-  } else {
-    return *reinterpret_cast<const float4*>(p);
-  }
-}
-
-template <typename Src>
-__device__ __forceinline__ void scatter_row(const int64_t* __restrict__ tok, int n, int i, int64_t t, int c_tot,
-                                            int64_t rb, const Src* __restrict__ src, int64_t lds, int h, float sign,
-                                            float* __restrict__ dst, int64_t ldd, int accumulate, int* list, int& s_m,
-                                            int& s_j0) {
-  const int64_t r = t - rb;
-  float* d = dst + r * ldd;
-  if (c_tot == 1) {
-    const Src* sp = src + int64_t(i) * lds;
-    // four passes' loads in flight before any store (memory-level parallelism)
-    const int pass = int(blockDim.x) * 4;  // columns per pass
-    for (int c0 = threadIdx.x * 4; c0 < h; c0 += 4 * pass) {
-      float4 acc[4], v[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int c = c0 + u * pass;
-        if (c < h) {
-          acc[u] = accumulate ? *reinterpret_cast<const float4*>(d + c) : make_float4(0.f, 0.f, 0.f, 0.f);
-          v[u] = load4(sp + c);
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int c = c0 + u * pass;
-        if (c < h) {
-          acc[u].x += sign * v[u].x;
-          acc[u].y += sign * v[u].y;
-          acc[u].z += sign * v[u].z;
-          acc[u].w += sign * v[u].w;
-          *reinterpret_cast<float4*>(d + c) = acc[u];
-        }
-      }
-    }
-    return;
-  }
-  // repeated row: batches of up to 32 occurrences in ascending i, collected
-  // by warp 0 with a ballot scan over the ids
-  const int lane = threadIdx.x & 31;
-  __syncthreads();  // list / s_m / s_j0 are free (the previous row is done)
-  if (threadIdx.x == 0) s_j0 = i;
-  int done = 0;
-  bool first = true;
-  while (done < c_tot) {
-    __syncthreads();
-    if (threadIdx.x < 32) {
-      int m = 0, j0 = s_j0;
-      while (m < 32 && done + m < c_tot && j0 < n) {
-        const int j = j0 + lane;
-        unsigned bal = __ballot_sync(0xffffffffu, j < n && tok[j] == t);
-        const int hits = __popc(bal);
-        const int take = min(hits, min(32 - m, c_tot - done - m));
-        int last = j0;
-        for (int q = 0; q < take; ++q) {
-          last = j0 + __ffs(bal) - 1;
-          if (lane == 0) list[m + q] = last;
-          bal &= bal - 1;
-        }
-        m += take;
-        j0 = take < hits ? last + 1 : j0 + 32;
-      }
-      if (lane == 0) {
-        s_m = m;
-        s_j0 = j0;
-      }
-    }
-    __syncthreads();
-    const int m = s_m;
-    if (m == 0) break;  // (counts and ids disagree: cannot happen)
-    for (int c = threadIdx.x * 4; c < h; c += int(blockDim.x) * 4) {
-      float4 acc = (first && !accumulate) ? make_float4(0.f, 0.f, 0.f, 0.f) : *reinterpret_cast<const float4*>(d + c);
-      for (int q = 0; q < m; ++q) {
-        const float4 v = load4(src + int64_t(list[q]) * lds + c);
-        acc.x += sign * v.x;
-        acc.y += sign * v.y;
-        acc.z += sign * v.z;
-        acc.w += sign * v.w;
-      }
-      *reinterpret_cast<float4*>(d + c) = acc;
-    }
-    done += m;
-    first = false;
-  }
-  __syncthreads();
-}
-
-template <typename Src>
-__global__ void __launch_bounds__(256) k_scatter_rows(const int64_t* __restrict__ tok, int n, int64_t rb, int64_t re,
-                                                     const unsigned* __restrict__ head, const int* __restrict__ cnt,
-                                                     const Src* __restrict__ src, int64_t lds, int h, float sign,
-                                                     float* __restrict__ dst, int64_t ldd, int accumulate) {
-  // one block per token (only a row's head works), 256 threads x 4 columns
-  // per pass.  (Measured alternatives: 8 tokens per block, 164 -> 303 us;
-  // blocks over the rows in ascending order, -> 208 us.)
-  __shared__ int list[32];
-  __shared__ int s_m, s_j0;
-  const int i = blockIdx.x;
-  const int64_t t = tok[i];
-  if (t < rb || t >= re) return;
-  if (head[t - rb] != unsigned(i)) return;  // a later occurrence: its head adds it
-  scatter_row(tok, n, i, t, cnt[t - rb], rb, src, lds, h, sign, dst, ldd, accumulate, list, s_m, s_j0);
-}
-
 }  // namespace vp

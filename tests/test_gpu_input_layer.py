@@ -124,3 +124,54 @@ def test_input_backward_negative_token_raises(ctx):
         ctx.sync()
     with pytest.raises(ValueError, match="grad/token length mismatch"):
         vm.input_backward(ctx, torch.ones(3, 8, device="cuda"), torch.tensor([1, 2], device="cuda"), s)
+
+
+def _zipf_ids(T, V, s, seed):
+    gen = torch.Generator(device="cuda").manual_seed(seed)
+    k = torch.arange(1, V + 1, device="cuda", dtype=torch.float64)
+    ranks = torch.multinomial((1.0 / k.pow(s)).float(), T, replacement=True, generator=gen)
+    return torch.randperm(V, device="cuda", generator=gen)[ranks]
+
+
+@pytest.mark.parametrize("grad_dtype", [torch.bfloat16, torch.float32])
+def test_input_backward_zipf_ids_bit_exact(ctx, grad_dtype):
+    # Zipf(1.1) token ids at the config-4 shape: hot rows with thousands of
+    # occurrences (column-chunked, bulk-copy streamed) next to unique rows —
+    # still the ascending-i fp32 sum, bit for bit, accumulating into dE
+    V, h, T = 256000, 4096, 16384
+    tok = _zipf_ids(T, V, 1.1, 3)
+    counts = torch.bincount(tok, minlength=V)
+    assert counts.max().item() > 1000 and (counts == 1).sum().item() > 1000
+    grad = torch.randn(T, h, device="cuda", generator=torch.Generator(device="cuda").manual_seed(4)).to(grad_dtype)
+    p = 8  # the shard holding the hottest token (keeps the host-side reference at 0.5 GB)
+    shards = vm.shard_weights(torch.zeros(V, h, dtype=torch.bfloat16, device="cuda"), p)
+    s = shards[int(counts.argmax().item()) // (V // p)]
+    init = torch.randn(s.rows(), h, device="cuda", generator=torch.Generator(device="cuda").manual_seed(5))
+    dE = init.clone()
+    vm.input_backward(ctx, grad, tok, s, out=dE, accumulate=True)
+    ctx.sync()
+    ref = oracle.input_backward_f32(grad.float().cpu().numpy(), tok.cpu().numpy(), s.rows(), s.row_begin,
+                                    init=init.cpu().numpy())
+    assert np.array_equal(dE.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("T,h", [(5000, 520), (16384, 4096), (3000, 8)])
+def test_input_backward_every_multiplicity_class(ctx, T, h):
+    # rows occurring once, 2..15 times (whole-row path), 16..32 (hot chunks,
+    # warp-sorted segment), 33..T (hot chunks, bitmap-sorted segment) and one
+    # row holding most of the batch; ragged last hot chunk when h % 256 != 0
+    rng = np.random.default_rng(T + h)
+    V = 40000
+    tok = rng.integers(0, V, T)
+    pos = rng.permutation(T)
+    k = 0
+    for row, c in [(11, 2), (12, 7), (13, 15), (14, 16), (15, 31), (16, 32), (17, 33), (18, 300), (19, T // 3)]:
+        tok[pos[k:k + c]] = row
+        k += c
+    g = torch.from_numpy(rng.standard_normal((T, h)).astype(np.float32)).cuda().to(torch.bfloat16)
+    td = torch.from_numpy(tok.astype(np.int64)).cuda()
+    for s in vm.shard_weights(torch.zeros(V, h, dtype=torch.bfloat16, device="cuda"), 4):
+        dE = vm.input_backward(ctx, g, td, s)
+        ctx.sync()
+        ref = oracle.input_backward_f32(g.float().cpu().numpy(), tok, s.rows(), s.row_begin)
+        assert np.array_equal(dE.cpu().numpy(), ref), s.index
