@@ -106,8 +106,13 @@ int vp_ctx_reserve(vp_ctx_t ctx, int64_t n_tok, int64_t h, int p);
  * operand bands in L2; 0 = off; default 8 for all three),
  * "splits_dx" / "splits_dw" (split-K of the dX / A GEMM, whose K = V_k leaves
  * few tile waves, and of the dW GEMM for small shards: 0 = chosen from the wave
- * quantisation (default), 1 = off, 2..4 = forced; partial sums are added in
+ * quantisation (default), 1 = off, 2..32 = forced; partial sums are added in
  * split order, so results are deterministic),
+ * "split_workspace" (GEMMs whose tiles fill less than half a wave split K into
+ * concurrent units that store partials into a context workspace, summed in
+ * split order by a reduction kernel: 1 = auto (default), 0 = never (ordered
+ * in-place splits only), 2 = whenever split), "split_min_kb" (ordered splits
+ * keep at least this many 64-deep k-blocks per unit; default 64),
  * "cooperative" (1 = persistent GEMMs launched cooperatively, so the whole grid
  * is co-resident, which their cross-CTA waits rely on when kernels of other
  * streams hold SMs; default 1; process-wide),
@@ -124,6 +129,12 @@ int vp_ctx_set_option(vp_ctx_t ctx, const char* key, int64_t value);
  * Y[i, :] + shift[i] (device fp32 [n_tok], kept by pointer; NULL clears it).
  * Softmax, loss and gradients are shift-invariant (test_vocab_math.cpp:74-84). */
 int vp_ctx_set_logit_shift(vp_ctx_t ctx, const float* shift);
+/* Test hook: occupy `nsms` SMs (one block per SM, all of its shared memory)
+ * for `microseconds` on `stream` (NULL = legacy default stream), as NCCL's
+ * kernels do during the overlapped exchanges; used to show that the
+ * cooperative persistent GEMMs neither deadlock nor change results when other
+ * streams hold SMs. */
+int vp_debug_occupy_sms(vp_ctx_t ctx, void* stream, int nsms, int64_t microseconds);
 /* Number of kernels this context has launched (evidence counter). */
 int64_t vp_ctx_launch_count(vp_ctx_t ctx);
 /* Per-GEMM CUDA-event timing on the launching stream.  Returns (and resets)
@@ -224,6 +235,16 @@ int vp_run_alg1(vp_ctx_t ctx, const vp_batch_t* batch, const vp_shard_t* shards,
 int vp_run_alg2(vp_ctx_t ctx, const vp_batch_t* batch, const vp_shard_t* shards, const vp_state_t* states, int n,
                 double fault_scale, vp_stats_t out, float* loss, float* grad_x, int64_t ldgx, float* const* grad_w,
                 int64_t ldgw);
+/* Memory-bounded run_alg2 (the paper's future-work remark on
+ * avoiding the softmax round trip, R/PAPER.md:498): the batch is processed as
+ * consecutive chunks of at most chunk_tokens tokens (softmax rows are
+ * independent), each through S -> C1 -> T with the per-chunk exchanges, so P
+ * takes chunk_tokens x V_k instead of n_tok x V_k; dW accumulates over the
+ * chunks.  `states` are created for min(chunk_tokens, n_tok) tokens.  Results
+ * equal vp_run_alg2's to the parity tolerances (dW sums chunk partials). */
+int vp_run_alg2_chunked(vp_ctx_t ctx, const vp_batch_t* batch, const vp_shard_t* shards, const vp_state_t* states,
+                        int n, int64_t chunk_tokens, double fault_scale, vp_stats_t out, float* loss, float* grad_x,
+                        int64_t ldgx, float* const* grad_w, int64_t ldgw);
 
 /* ---- input layer -------------------------------------------------------- */
 /* input_forward (VM.cpp:227-236): out[i] = W_k[tok_i - row_begin] if owned,

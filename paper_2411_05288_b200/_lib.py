@@ -40,6 +40,7 @@ SIGNATURES = {
     "vp_ctx_reserve": (c_int, [c_void_p, c_int64, c_int64, c_int]),
     "vp_ctx_set_option": (c_int, [c_void_p, c_char_p, c_int64]),
     "vp_ctx_launch_count": (c_int64, [c_void_p]),
+    "vp_debug_occupy_sms": (c_int, [c_void_p, c_void_p, c_int, c_int64]),
     "vp_ctx_set_logit_shift": (c_int, [c_void_p, c_void_p]),
     "vp_shard_logits": (c_int, [c_void_p, POINTER(vp_batch_t), POINTER(vp_shard_t), c_void_p, c_int64]),
     "vp_shard_label_rows": (c_int, [c_void_p, POINTER(vp_batch_t), POINTER(vp_shard_t), c_void_p, c_int64]),
@@ -77,6 +78,9 @@ SIGNATURES = {
                             vp_stats_t, c_void_p, c_void_p, c_int64, POINTER(c_void_p), c_int64]),
     "vp_run_alg2": (c_int, [c_void_p, POINTER(vp_batch_t), POINTER(vp_shard_t), POINTER(c_void_p), c_int, c_double,
                             vp_stats_t, c_void_p, c_void_p, c_int64, POINTER(c_void_p), c_int64]),
+    "vp_run_alg2_chunked": (c_int, [c_void_p, POINTER(vp_batch_t), POINTER(vp_shard_t), POINTER(c_void_p), c_int,
+                                    c_int64, c_double, vp_stats_t, c_void_p, c_void_p, c_int64, POINTER(c_void_p),
+                                    c_int64]),
     "vp_input_forward": (c_int, [c_void_p, c_void_p, c_int64, c_int64, POINTER(vp_shard_t), c_void_p, c_int64,
                                  c_int]),
     "vp_input_backward": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_void_p, c_int64, c_int64,

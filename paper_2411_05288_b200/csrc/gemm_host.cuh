@@ -97,6 +97,12 @@ struct SplitCfg {
   int* flags = nullptr;
   int max_tiles = 0;
   int force = 0;  // > 0: use exactly this many splits (tests); 0: choose by wave quantisation
+  // parallel split-K workspace (fp32, >= clusters x 256 x 512 elements + slack):
+  // used when the tiles fill less than half a wave; null = ordered splits only
+  float* ws = nullptr;
+  size_t ws_elems = 0;
+  int ws_mode = 1;    // 0: never use the workspace; 2: force it whenever S > 1 (tests)
+  int min_kb = 64;    // ordered splits keep at least this many k-blocks per unit
 };
 
 // Wave-lockstep state owned by the caller (per stream, like SplitCfg):
@@ -110,9 +116,10 @@ struct LockCfg {
 // Splits for a persistent GEMM of `tiles` tiles on `clusters` clusters and
 // num_kb k-blocks: the smallest S in 1..4 whose wave efficiency
 // tiles*S / (clusters * ceil(tiles*S / clusters)) is within 1% of the best,
-// keeping >= 128 k-blocks per split (shorter units are epilogue-bound: dW of
-// an 8-way shard split 3 ways ran 20% slower); S = 1 unless that gains > 2%.
-inline int choose_splits(int tiles, int clusters, int num_kb) {
+// keeping >= min_kb k-blocks per split (round 1 used 128: dW of an 8-way shard
+// split 3 ways ran 20% slower before the epilogues released TMEM early; the
+// context default is now 64); S = 1 unless that gains > 2%.
+inline int choose_splits(int tiles, int clusters, int num_kb, int min_kb = 128) {
   auto eff = [&](int S) {
     const double w = double(tiles) * S / clusters;
     return w / std::ceil(w);
@@ -120,9 +127,36 @@ inline int choose_splits(int tiles, int clusters, int num_kb) {
   int best = 1;
   double be = eff(1);
   for (int S = 2; S <= 4; ++S)
-    if (num_kb / S >= 128 && eff(S) > be + 0.02) {
+    if (num_kb / S >= min_kb && eff(S) > be + 0.02) {
       best = S;
       be = eff(S);
+    }
+  return best;
+}
+
+// Parallel split-K for GEMMs whose tiles fill less than half a wave (small
+// token counts, narrow shards): S units per tile run concurrently and store
+// partials; a reduction kernel sums them.  Cost model in pair k-block cycles
+// (1024 per k-block of a 256 x 512 tile; ~6k fixed per unit for the pipeline
+// fill and the epilogue; the reduction streams (S + 1) * M * N * 4 bytes at
+// ~1.6 KB/cycle plus a launch): the S in 2..min(32, clusters / tiles) with at
+// least 8 k-blocks per unit that minimises it, if it beats S = 1.
+inline int choose_ws_splits(int tiles, int clusters, int num_kb, int64_t M, int64_t N) {
+  auto cost = [&](int S) {
+    const double units = double(tiles) * S;
+    const double waves = std::ceil(units / clusters);
+    const double kb = std::ceil(double(num_kb) / S);
+    double c = waves * (kb * 1024.0 + 6000.0);
+    if (S > 1) c += double(S + 1) * double(M) * double(N) * 4.0 / 1600.0 + 4000.0;
+    return c;
+  };
+  int best = 1;
+  double bc = cost(1);
+  const int smax = std::min(32, clusters / std::max(tiles, 1));
+  for (int S = 2; S <= smax && num_kb / S >= 8; ++S)
+    if (cost(S) < bc * 0.97) {
+      best = S;
+      bc = cost(S);
     }
   return best;
 }
@@ -130,6 +164,26 @@ inline int choose_splits(int tiles, int clusters, int num_kb) {
 template <class Params>
 inline bool splittable(const Params&) { return false; }
 inline bool splittable(const EpiStoreF32::Params& p) { return p.tile_max == nullptr; }
+template <class Params>
+inline bool uses_tma(const Params&) { return false; }
+inline bool uses_tma(const EpiStoreF32::Params& p) { return p.use_tma != 0; }
+template <class Params>
+inline void set_ws_map(Params&, float*, int, int64_t, int64_t) {}
+inline void set_ws_map(EpiStoreF32::Params& p, float* ws, int N, int64_t rows, int64_t ldws) {
+  p.ws_map = make_store_map(ws, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, uint64_t(N), uint64_t(rows), uint64_t(ldws),
+                            VP_F32_BOX128 ? 128 : 64);
+}
+template <class Params>
+inline void launch_split_reduce(const Params&, const GemmGeom&, int, int, int, cudaStream_t) {}
+inline void launch_split_reduce(const EpiStoreF32::Params& p, const GemmGeom& g, int M, int N, int num_sms,
+                                cudaStream_t st) {
+  const int64_t ldws = (int64_t(N) + 3) / 4 * 4;
+  const int64_t work = int64_t(M) * ((N + 3) / 4);
+  const int blocks = int(std::min<int64_t>((work + 255) / 256, int64_t(num_sms) * 8));
+  k_split_reduce<<<blocks, 256, 0, st>>>(g.split_ws, g.splits, g.ws_rows, ldws, p.out, p.ldo, M, N, p.accumulate);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw std::runtime_error(std::string("split reduce launch: ") + cudaGetErrorString(e));
+}
 
 // One GEMM operand: row-major storage `ptr` with leading dimension `ld`.
 //   K-major : storage [rows x K]  (A: rows = M, B: rows = N)
@@ -209,9 +263,25 @@ inline void launch_gemm_t(const Operand& A, const Operand& B, int M, int N, int 
   }
   int cap = num_sms / CL < max_active ? num_sms / CL : max_active;
   int clusters = tiles < cap ? tiles : cap;
+  typename Epi::Params epc = ep;
+  prepare_store(epc, M, N);
   if (MC == 1 && split != nullptr && split->flags != nullptr && splittable(ep) && tiles <= split->max_tiles) {
-    const int S = split->force > 0 ? split->force : choose_splits(tiles, cap, g.num_kb);
-    if (S > 1 && g.num_kb >= S) {
+    // workspace mode: less than half a wave of tiles, TMA-stored output, room
+    const int64_t ldws = (int64_t(N) + 3) / 4 * 4;
+    const bool ws_ok = split->ws != nullptr && split->ws_mode != 0 && uses_tma(epc) &&
+                       (split->ws_mode == 2 || tiles * 2 <= cap);
+    int S = split->force;
+    if (S <= 0)
+      S = ws_ok ? choose_ws_splits(tiles, cap, g.num_kb, M, N) : choose_splits(tiles, cap, g.num_kb, split->min_kb);
+    if (ws_ok && S > 1 && size_t(S) * size_t(g.tiles_m * C::BM) * size_t(ldws) > split->ws_elems)
+      S = 1;  // (forced S beyond the workspace: the tests stay within it)
+    if (ws_ok && S > 1 && g.num_kb >= S) {
+      g.splits = S;
+      g.split_ws = split->ws;
+      g.ws_rows = g.tiles_m * C::BM;
+      set_ws_map(epc, split->ws, N, int64_t(S) * g.ws_rows, ldws);
+      clusters = tiles * S < cap ? tiles * S : cap;
+    } else if (S > 1 && g.num_kb >= S) {
       g.splits = S;
       g.split_flags = split->flags;
       g.flag_base = 0;
@@ -252,10 +322,9 @@ inline void launch_gemm_t(const Operand& A, const Operand& B, int M, int N, int 
       if (me != cudaSuccess) throw std::runtime_error(std::string("lockstep memset: ") + cudaGetErrorString(me));
     }
   }
-  typename Epi::Params epc = ep;
-  prepare_store(epc, M, N);
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta, tb, g, epc);
   if (e != cudaSuccess) throw std::runtime_error(std::string("gemm launch: ") + cudaGetErrorString(e));
+  if (g.split_ws != nullptr) launch_split_reduce(epc, g, M, N, num_sms, st);
 }
 
 // Runtime dispatch over (cta_group, operand majors).

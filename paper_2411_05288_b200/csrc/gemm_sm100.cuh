@@ -42,6 +42,12 @@
 #ifndef VP_F32_BOX128
 #define VP_F32_BOX128 1  // fp32 epilogues store 32 x 128 B SWIZZLE_128B boxes (0: two 64 B boxes per chunk)
 #endif
+#ifndef VP_K1_EARLY
+#define VP_K1_EARLY 1  // K1 epilogue drains its accumulator half to registers and releases TMEM before the math
+#endif
+#ifndef VP_F32_EARLY
+#define VP_F32_EARLY 0  // the same for the fp32 (dX / dW) epilogues
+#endif
 #ifndef VP_K1_POLY
 #define VP_K1_POLY 0  // 1: half of the K1 epilogue's exponentials on the FMA pipe (ptx::ex2_poly)
 #endif
@@ -78,6 +84,11 @@ struct GemmGeom {
   int lock_epoch = 8;
   int lock_stride = 0;
   int store_evict_first = 0;  // epilogue TMA stores with an L2 evict-first hint
+  // Parallel split-K (less than a wave of tiles): unit (tile, s) stores its
+  // partial into rows [s * ws_rows, ...) of a workspace instead of waiting for
+  // split s-1; k_split_reduce then sums the S slices in fixed order.
+  float* split_ws = nullptr;
+  int ws_rows = 0;
 };
 
 __device__ __forceinline__ uint64_t make_policy(int p, bool dflt_first) {
@@ -225,6 +236,32 @@ __device__ __forceinline__ void tmem_chunks(uint32_t taddr, int nch, F&& f) {
     }
   }
 }
+
+// All 128 columns of this warp's accumulator rows into registers (one wait).
+__device__ __forceinline__ void tmem_load_all(uint32_t taddr, uint32_t (&acc)[kEpiCols]) {
+#pragma unroll
+  for (int c = 0; c < kEpiCols / 32; ++c)
+    ptx::tmem_ld32(taddr + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&acc[32 * c]));
+  ptx::tmem_ld_wait();
+#pragma unroll
+  for (int c = 0; c < kEpiCols / 32; ++c) ptx::tmem_pin(*reinterpret_cast<uint32_t(*)[32]>(&acc[32 * c]));
+}
+
+// Chunk sources for the epilogue walks: f(chunk regs, c) for c < nch.
+struct TmemSrc {
+  uint32_t taddr;
+  template <class F>
+  __device__ __forceinline__ void operator()(int nch, F&& f) const { tmem_chunks(taddr, nch, f); }
+};
+struct RegSrc {
+  uint32_t (&acc)[kEpiCols];
+  template <class F>
+  __device__ __forceinline__ void operator()(int nch, F&& f) const {
+#pragma unroll
+    for (int c = 0; c < kEpiCols / 32; ++c)
+      if (c < nch) f(*reinterpret_cast<uint32_t(*)[32]>(&acc[32 * c]), c);
+  }
+};
 
 // Split-K ordering (epilogue warps of one CTA).  split_wait: every lane
 // waits until the previous split of this tile/CTA has landed in global
@@ -537,7 +574,7 @@ __global__ void __launch_bounds__(384, 1)
       const int t = unit_tile(u), sp = unit_split(u);
       tile_coords(gc, t, mc, nb);
       const int mb = mc * MC + int(pair);
-      int* flag = g.splits > 1 ? g.split_flags + 2 * t + int(rank) : nullptr;
+      int* flag = (g.splits > 1 && g.split_ws == nullptr) ? g.split_flags + 2 * t + int(rank) : nullptr;
       const int row = mb * C::BM + int(rank) * C::BM_CTA + quad * 32 + lane;
       const typename Epi::Pre pre = Epi::prepare(ep, g, row, nb * C::BN_TILE);
       // one accumulator per N half (NH == 2, released separately: see the
@@ -552,7 +589,26 @@ __global__ void __launch_bounds__(384, 1)
         else ptx::mbar_wait(bar_tfull + 8 * slot, par);
         ptx::tc_fence_after();
         const unsigned long long c1 = probe ? clock64() : 0;
-        if (hw == 0 && sp > 0) split_wait(flag, g.flag_base + sp);
+        if constexpr (Epi::kEarly && NH == 2) {
+          // Early release: this warp's 128 accumulator columns of the half go
+          // to registers (4 x tcgen05.ld, one wait) and the half is handed back
+          // to the MMA issuer at once; the epilogue math and stores then run
+          // under the next tile's MMAs instead of inside the stagger window.
+          const int col0 = nb * C::BN_TILE + hw * C::BN + cgp * kEpiCols;
+          const uint32_t taddr = tmem_base + uint32_t(hw * C::BN + cgp * kEpiCols) + (uint32_t(quad * 32) << 16);
+          uint32_t acc[kEpiCols];
+          tmem_load_all(taddr, acc);
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive_remote(bar_tempty + 8 * slot, leader);
+          if (hw == 0 && flag && sp > 0) split_wait(flag, g.flag_base + sp);
+          if (col0 < g.N) Epi::apply_regs(ep, g, acc, row, col0, col0 / kEpiCols, sg, pre, sp);
+          if (probe && lane == 0) {
+            epi_wait_cyc += c1 - c0;
+            epi_work_cyc += clock64() - c1;
+          }
+        } else {
+        if (hw == 0 && flag && sp > 0) split_wait(flag, g.flag_base + sp);
 #pragma unroll 1
         for (int hh = (NH == 2 ? hw : 0); hh < (NH == 2 ? hw + 1 : NH); ++hh) {
           const int col0 = nb * C::BN_TILE + hh * C::BN + cgp * kEpiCols;
@@ -561,7 +617,7 @@ __global__ void __launch_bounds__(384, 1)
           // a ragged last tile's trailing column groups lie wholly past N:
           // no columns, no stats slot, nothing to store
 #if VP_EPI_MODE == 0 || VP_EPI_MODE >= 3
-          if (col0 < g.N) Epi::apply(ep, g, taddr, row, col0, col0 / kEpiCols, sg, pre, sp > 0);
+          if (col0 < g.N) Epi::apply(ep, g, taddr, row, col0, col0 / kEpiCols, sg, pre, sp);
 #elif VP_EPI_MODE == 1
           // probe: TMEM loads only (results discarded)
           tmem_chunks(taddr, 4, [&](uint32_t (&r)[32], int) {
@@ -581,6 +637,7 @@ __global__ void __launch_bounds__(384, 1)
         if (lane == 0) {
           if constexpr (CG == 1) ptx::mbar_arrive(bar_tempty + 8 * slot);
           else ptx::mbar_arrive_remote(bar_tempty + 8 * slot, leader);
+        }
         }
       }
       if (flag) split_done(flag, g.flag_base + sp + 1, sg);
@@ -626,6 +683,7 @@ __global__ void __launch_bounds__(384, 1)
 // the valid columns (naive F1: logits + local max).
 struct EpiStoreF32 {
   static constexpr bool kAStreams = true;
+  static constexpr bool kEarly = VP_F32_EARLY != 0;
   struct Params {
     float* out;
     int64_t ldo;
@@ -639,6 +697,7 @@ struct EpiStoreF32 {
     // 85% of MMA-ideal cycles.)
     int use_tma = 0;
     CUtensorMap map;
+    CUtensorMap ws_map;  // parallel split-K workspace (fp32 [S * ws_rows x N])
   };
   // per-row inputs loaded before the accumulator is waited for (hides their latency)
   struct Pre {
@@ -648,16 +707,30 @@ struct EpiStoreF32 {
     return Pre{(p.row_scale && row < g.M) ? p.row_scale[row] : 1.f};
   }
   __device__ static void apply(const Params& p, const GemmGeom& g, uint32_t taddr, int row, int col0, int nb,
-                               Stager& sg, const Pre& pre, bool split_add) {
+                               Stager& sg, const Pre& pre, int sp) {
+    run(p, g, TmemSrc{taddr}, row, col0, nb, sg, pre, sp);
+  }
+  __device__ static void apply_regs(const Params& p, const GemmGeom& g, uint32_t (&acc)[kEpiCols], int row, int col0,
+                                    int nb, Stager& sg, const Pre& pre, int sp) {
+    run(p, g, RegSrc{acc}, row, col0, nb, sg, pre, sp);
+  }
+  template <class Src>
+  __device__ static __forceinline__ void run(const Params& p, const GemmGeom& g, const Src& src, int row, int col0,
+                                             int nb, Stager& sg, const Pre& pre, int sp) {
     const bool row_ok = row < g.M;
     const int nvalid = min(kEpiCols, g.N - col0);
     const int nch = (nvalid + 31) / 32;
     const float rs = pre.rs;
-    const bool add = p.accumulate != 0 || split_add;
+    // parallel split-K: plain stores of this unit's partial into its workspace
+    // slice (use_tma is guaranteed by the host); else ordered accumulation
+    const bool to_ws = g.split_ws != nullptr;
+    const CUtensorMap* omap = to_ws ? &p.ws_map : &p.map;
+    const int rbase = to_ws ? sp * g.ws_rows : 0;
+    const bool add = !to_ws && (p.accumulate != 0 || sp > 0);
     float mx = -INFINITY;
     const int row0 = row - int(threadIdx.x & 31);
     if (p.use_tma) {
-      tmem_chunks(taddr, nch, [&](uint32_t (&r)[32], int c) {
+      src(nch, [&](uint32_t (&r)[32], int c) {
         if (p.row_scale) {
           const uint64_t rs2 = ptx::f2pack(rs, rs);
 #pragma unroll
@@ -690,7 +763,7 @@ struct EpiStoreF32 {
         ptx::fence_proxy_async_smem();
         __syncwarp();
         if ((threadIdx.x & 31) == 0) {
-          sg.put(&p.map, sg.base, col0 + c * 32, row0, add);
+          sg.put(omap, sg.base, col0 + c * 32, row0 + rbase, add);
           ptx::bulk_commit();
         }
 #else
@@ -702,13 +775,13 @@ struct EpiStoreF32 {
 #pragma unroll
         for (int q = 0; q < 4; ++q)
           ptx::st_shared_v4(Stager::chunk(b1, q), r[16 + 4 * q], r[16 + 4 * q + 1], r[16 + 4 * q + 2], r[16 + 4 * q + 3]);
-        sg.flush2(&p.map, b0, col0 + c * 32, row0, b1, col0 + c * 32 + 16, row0, add);
+        sg.flush2(omap, b0, col0 + c * 32, row0 + rbase, b1, col0 + c * 32 + 16, row0 + rbase, add);
 #endif
       });
     } else {
       float* dst = p.out + int64_t(row) * p.ldo + col0;
       const bool vec = ((p.ldo & 3) == 0) && ((reinterpret_cast<uintptr_t>(p.out) & 15) == 0);
-      tmem_chunks(taddr, nch, [&](uint32_t (&r)[32], int c) {
+      src(nch, [&](uint32_t (&r)[32], int c) {
         const int nv = nvalid - c * 32;
         if (p.row_scale) {
 #pragma unroll
@@ -763,6 +836,7 @@ struct EpiStoreF32 {
 // makes it unreachable.)  Full-vocab logits never touch HBM.
 struct EpiLogitStats {
   static constexpr bool kAStreams = false;  // A = X is reused by every vocab tile
+  static constexpr bool kEarly = VP_K1_EARLY != 0;
   static constexpr float kMaxRefGap = 64.f;  // e^{Y - q} <= e^64: P, its sums and P.W stay finite in fp32
   static constexpr float kRefLift = 16.f;    // r_i sits this far above the first vocab tile's max
   struct Params {
@@ -791,9 +865,10 @@ struct EpiLogitStats {
     float logit_scale = 1.f;
   };
   // max of the valid columns and the label logit (first pass of a two-pass tile)
-  __device__ static void scan(uint32_t taddr, int nvalid, int lb, float& mx, float& yt, bool& has_t) {
+  template <class Src>
+  __device__ static void scan(const Src& src, int nvalid, int lb, float& mx, float& yt, bool& has_t) {
     float mp[4] = {mx, mx, mx, mx};
-    tmem_chunks(taddr, (nvalid + 31) / 32, [&](uint32_t (&r)[32], int c) {
+    src((nvalid + 31) / 32, [&](uint32_t (&r)[32], int c) {
       const int nv = nvalid - c * 32;
       if (nv >= 32) {
 #pragma unroll
@@ -818,7 +893,8 @@ struct EpiLogitStats {
   // label logit (the single-pass path, where ref = r_i is known up front).
   // ref and shift are in logit space (y = acc * logit_scale + shift); mx / yt
   // are tracked in accumulator space.
-  __device__ static void emit(const Params& p, uint32_t taddr, int row, bool row_ok, int col0, int nvalid,
+  template <class Src>
+  __device__ static void emit(const Params& p, const Src& src, int row, bool row_ok, int col0, int nvalid,
                               float ref, float shift, int lb, bool track, float& mx, float& yt, bool& has_t,
                               float& sum, Stager& sg) {
     const float kLog2e = 1.4426950408889634f * p.logit_scale;
@@ -835,7 +911,7 @@ struct EpiLogitStats {
 #if !VP_P_BOX128
     uint32_t box0 = 0;  // first box of the pair being filled (TMA path)
 #endif
-    tmem_chunks(taddr, nch, [&](uint32_t (&r)[32], int c) {
+    src(nch, [&](uint32_t (&r)[32], int c) {
       const int nv = nvalid - c * 32;
       uint32_t pk[16];
       if (nv >= 32) {
@@ -974,7 +1050,16 @@ struct EpiLogitStats {
     return r;
   }
   __device__ static void apply(const Params& p, const GemmGeom& g, uint32_t taddr, int row, int col0, int nb,
-                               Stager& sg, const Pre& pre, bool /*split_add: never split*/) {
+                               Stager& sg, const Pre& pre, int /*sp: never split*/) {
+    run(p, g, TmemSrc{taddr}, row, col0, nb, sg, pre);
+  }
+  __device__ static void apply_regs(const Params& p, const GemmGeom& g, uint32_t (&acc)[kEpiCols], int row, int col0,
+                                    int nb, Stager& sg, const Pre& pre, int /*sp: never split*/) {
+    run(p, g, RegSrc{acc}, row, col0, nb, sg, pre);
+  }
+  template <class Src>
+  __device__ static __forceinline__ void run(const Params& p, const GemmGeom& g, const Src& src, int row, int col0,
+                                             int nb, Stager& sg, const Pre& pre) {
     const bool row_ok = row < g.M;
     const int lane = threadIdx.x & 31;
     const int nvalid = min(kEpiCols, g.N - col0);
@@ -1004,7 +1089,7 @@ struct EpiLogitStats {
     if (nb == 0 || !f) {
       // two passes: this tile is its own reference (the j = 0 tile defines r_i;
       // an early tile whose row reference is not published yet falls back)
-      scan(taddr, nvalid, lb, mx, yt, has_t);
+      scan(src, nvalid, lb, mx, yt, has_t);
       mx = mx * p.logit_scale + pre.shift;  // accumulator -> logit space
       yt = yt * p.logit_scale + pre.shift;
       ref = mx;
@@ -1024,11 +1109,11 @@ struct EpiLogitStats {
         own = true;
       }
       float m2 = -INFINITY, y2 = 0.f;
-      emit(p, taddr, row, row_ok, col0, nvalid, ref, pre.shift, lb, false, m2, y2, has_t, sum, sg);
+      emit(p, src, row, row_ok, col0, nvalid, ref, pre.shift, lb, false, m2, y2, has_t, sum, sg);
     } else {
       // single pass against the published row reference
       ref = row_ok ? pref : 0.f;
-      emit(p, taddr, row, row_ok, col0, nvalid, ref, pre.shift, lb, true, mx, yt, has_t, sum, sg);
+      emit(p, src, row, row_ok, col0, nvalid, ref, pre.shift, lb, true, mx, yt, has_t, sum, sg);
       mx = mx * p.logit_scale + pre.shift;  // accumulator -> logit space
       yt = yt * p.logit_scale + pre.shift;
       bad = row_ok && (mx - ref > kMaxRefGap);  // e^{Y - r} overflowed: redo against the tile max
@@ -1037,7 +1122,7 @@ struct EpiLogitStats {
         // the first pass's P boxes must land before they are overwritten
         if (p.use_tma) sg.drain();
         float m2 = -INFINITY, y2 = 0.f;
-        emit(p, taddr, row, row_ok, col0, nvalid, ref, pre.shift, lb, false, m2, y2, has_t, sum, sg);
+        emit(p, src, row, row_ok, col0, nvalid, ref, pre.shift, lb, false, m2, y2, has_t, sum, sg);
       }
     }
     if (row_ok) {
@@ -1052,5 +1137,39 @@ struct EpiLogitStats {
       p.fix_list[atomicAdd(p.fix_count, 1)] = make_int2(row >> 5, nb);
   }
 };
+
+// Parallel split-K reduction: out[r, :] (+)= sum_{s = 0..S-1} ws[s * ws_rows + r, :]
+// in ascending s (fixed order: bitwise deterministic).  4 columns per thread
+// (out and ws rows are 16-B aligned: the TMA-store precondition).
+__global__ void k_split_reduce(const float* __restrict__ ws, int S, int ws_rows, int64_t ldws, float* __restrict__ out,
+                               int64_t ldo, int M, int N, int accumulate) {
+  const int n4 = (N + 3) / 4;
+  const int64_t total = int64_t(M) * n4;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const int r = int(i / n4), c = int(i - int64_t(r) * n4) * 4;
+    float4 v = *reinterpret_cast<const float4*>(ws + int64_t(r) * ldws + c);
+    for (int sp = 1; sp < S; ++sp) {
+      const float4 w = __ldcs(reinterpret_cast<const float4*>(ws + (int64_t(sp) * ws_rows + r) * ldws + c));
+      v.x += w.x;
+      v.y += w.y;
+      v.z += w.z;
+      v.w += w.w;
+    }
+    float* o = out + int64_t(r) * ldo + c;
+    if (c + 4 <= N) {
+      if (accumulate) {
+        const float4 a = *reinterpret_cast<const float4*>(o);
+        v.x = a.x + v.x;
+        v.y = a.y + v.y;
+        v.z = a.z + v.z;
+        v.w = a.w + v.w;
+      }
+      *reinterpret_cast<float4*>(o) = v;
+    } else {
+      const float vv[4] = {v.x, v.y, v.z, v.w};
+      for (int j = 0; j < N - c; ++j) o[j] = (accumulate ? o[j] : 0.f) + vv[j];
+    }
+  }
+}
 
 }  // namespace vp

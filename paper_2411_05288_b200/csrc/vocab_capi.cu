@@ -3,6 +3,7 @@
 // naive / Algorithm-1 / Algorithm-2 output layer and the input layer.
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cstdlib>
@@ -85,6 +86,16 @@ inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 
 
 enum PForm { kRaw = 0, kLocal = 1, kGlobal = 2 };
 
+// NVTX range per vocabulary pass (S, C1, T, C2, the naive barriers, the input
+// layer): the reference's pass names on an Nsight timeline (header-only NVTX
+// v3: no cost unless a tool is attached).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 }  // namespace
 
 struct vp_ctx_s {
@@ -104,7 +115,8 @@ struct vp_ctx_s {
   int mc = 1;  // CTA pairs per cluster sharing B by TMA multicast (1 or 2)
   int nh[3] = {2, 2, 2};  // N halves per tile (2 = 256 x 512 pair tiles) for [logits, dX, dW]
   // split-K of the dX GEMM (K = V_k, few waves): ordered, deterministic;
-  // splits_dx option: 0 = by wave quantisation, 1 = off, 2..4 = forced
+  // splits_dx option: 0 = by wave quantisation (ordered splits) or, below half
+  // a wave of tiles, the parallel workspace split-K; 1 = off; 2..32 = forced
   vp::SplitCfg split;
   int splits_dx = 0, splits_dw = 0;
   // wave lockstep per GEMM [logits, dX, dW]: epoch length in k-blocks (0 = off)
@@ -390,6 +402,7 @@ void segment_scatter(vp_ctx_s* c, const int64_t* tok, int64_t n, int64_t rb, int
 // apply the Eq. 5 factor per row (dX epilogue / scaled X), so they never
 // rewrite P and remain pure.
 void pass_S_common(vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* s, vp_state_s* st) {
+  NvtxRange nr("vp:S");
   check_batch(b, false);
   check_shard(s, b->h);
   check_state(st, b, s);
@@ -418,6 +431,7 @@ void pass_S_common(vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* s, vp_sta
 
 void alg2_S(vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* s, vp_state_s* st) {
   pass_S_common(c, b, s, st);
+  NvtxRange nr("vp:S:A=softmax'W");
   gemm_dx(c, st, s, st->A, st->h, st->cfac);  // A = softmax' W_k = diag(cfac) P W_k (VM.cpp:183)
   st->has_grad_terms = true;
 }
@@ -454,6 +468,7 @@ int64_t global_vocab(vp_ctx_s* c, const vp_shard_t* shards, int n) {
 }
 
 void merge_stats(vp_ctx_s* c, const vp_state_t* states, int n, double fault_scale, vp_stats_t out) {
+  NvtxRange nr("vp:C1:stats");
   require(n >= 1 && states != nullptr, "merge_max_sum: empty input");
   require(out.m != nullptr && out.sum != nullptr, "merge_max_sum: null output");
   const int64_t T = states[0]->n_tok;
@@ -493,6 +508,7 @@ void merge_stats(vp_ctx_s* c, const vp_state_t* states, int n, double fault_scal
 //   dW_k = grad_y^T X = softmax'^T (c (.) X) - G_k^T X     (scaled X operand, ordered scatter)
 void alg1_T(vp_ctx_s* c, vp_state_s* st, vp_stats_t g, const vp_batch_t* b, const vp_shard_t* s, float* gx,
             int64_t ldgx, float* gw, int64_t ldgw) {
+  NvtxRange nr("vp:T(alg1)");
   check_batch(b);
   check_shard(s, b->h);
   check_state(st, b, s);
@@ -514,6 +530,7 @@ void alg1_T(vp_ctx_s* c, vp_state_s* st, vp_stats_t g, const vp_batch_t* b, cons
 // alg2_pass_T (VM.cpp:213-225): dW_k = softmax'^T (c (.) X) - G_k^T X
 void alg2_T(vp_ctx_s* c, vp_state_s* st, vp_stats_t g, const vp_batch_t* b, const vp_shard_t* s, float* gw,
             int64_t ldgw) {
+  NvtxRange nr("vp:T(alg2)");
   check_batch(b);
   check_shard(s, b->h);
   check_state(st, b, s);
@@ -528,6 +545,7 @@ void alg2_T(vp_ctx_s* c, vp_state_s* st, vp_stats_t g, const vp_batch_t* b, cons
 
 void alg2_C1(vp_ctx_s* c, const vp_state_t* states, const vp_shard_t* shards, int n, const vp_batch_t* b,
              double fault_scale, vp_stats_t out, float* gx, int64_t ldgx, bool reduce = true) {
+  NvtxRange nr("vp:C1");
   require(n >= 1 && states != nullptr, "alg2_barrier_C1: no states");
   check_batch(b);
   for (int k = 0; k < n; ++k) {
@@ -602,6 +620,7 @@ void reduce_partials(vp_ctx_s* c, float* const* partials, int n, int64_t T, int6
 // Fork the queued all-reduces (grad_x, loss) onto the comm stream after the
 // compute stream's current work; the compute stream continues with pass T.
 void fork_allreduces(vp_ctx_s* c, float* gx, int64_t n_gx, float* loss, int64_t n_loss) {
+  NvtxRange nr("vp:C1:allreduce(dX,loss)");
   VP_CUDA(cudaEventRecord(c->ev_ready, c->stream));
   VP_CUDA(cudaStreamWaitEvent(c->comm_stream, c->ev_ready, 0));
   c->cm().group_start();
@@ -655,6 +674,7 @@ void run_alg(int alg, vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* shards
       partials[size_t(k)] = c->distributed() ? gx : states[k]->A;
       alg1_T(c, states[k], out, b, &shards[k], partials[size_t(k)], c->distributed() ? ldgx : b->h, gw[k], ldgw);
     }
+    NvtxRange nr("vp:C2");
     if (c->distributed()) {
       require(ldgx == b->h, "run_alg1: grad_x must be dense for the all-reduce");
       c->cm().all_reduce(gx, gx, size_t(b->n_tok * b->h), vp::DType::F32, vp::RedOp::Sum, c->stream);
@@ -666,6 +686,7 @@ void run_alg(int alg, vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* shards
 
 void naive(vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* shards, const vp_state_t* states, int n,
            vp_stats_t out, float* loss, float* gx, int64_t ldgx, float* const* gw, int64_t ldgw) {
+  NvtxRange nr("vp:naive(F1,F2,B)");
   require(n >= 1 && shards != nullptr, "naive: no shards");
   require(n <= vp::kMaxLocalShards, "naive: too many local shards");
   require(!c->distributed() || n == 1, "naive: one shard per rank in an NCCL group");
@@ -968,6 +989,10 @@ int vp_ctx_create(int device, vp_ctx_t* out) {
       c->split.max_tiles = 1 << 14;
       VP_CUDA(cudaMalloc(&c->split.flags, size_t(2 * c->split.max_tiles) * sizeof(int)));
       VP_CUDA(cudaMemset(c->split.flags, 0, size_t(2 * c->split.max_tiles) * sizeof(int)));
+      // parallel split-K workspace: S * tiles <= one wave of CTA pairs, each
+      // tile <= 256 x 512 fp32 (+ row padding slack)
+      c->split.ws_elems = size_t(c->num_sms / 2 + 2) * 256 * 512 + (size_t(1) << 16);
+      VP_CUDA(cudaMalloc(&c->split.ws, c->split.ws_elems * sizeof(float)));
     } catch (...) {
       delete c;
       throw;
@@ -991,6 +1016,7 @@ int vp_ctx_destroy(vp_ctx_t c) {
       b->release();
     if (c->d_err) cudaFree(c->d_err);
     if (c->split.flags) cudaFree(c->split.flags);
+    if (c->split.ws) cudaFree(c->split.ws);
     if (c->lock.counters) cudaFree(c->lock.counters);
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
     delete c;
@@ -1083,8 +1109,14 @@ int vp_ctx_set_option(vp_ctx_t c, const char* key, int64_t value) {
       require(value == 0 || value == 1, "vp_ctx_set_option: store_evict_first must be 0 or 1");
       vp::g_store_evict_first = int(value);
     } else if (k == "splits_dx" || k == "splits_dw") {
-      require(value >= 0 && value <= 4, "vp_ctx_set_option: splits_dx / splits_dw must be in 0..4");
+      require(value >= 0 && value <= 32, "vp_ctx_set_option: splits_dx / splits_dw must be in 0..32");
       (k == "splits_dx" ? c->splits_dx : c->splits_dw) = int(value);
+    } else if (k == "split_workspace") {
+      require(value >= 0 && value <= 2, "vp_ctx_set_option: split_workspace must be 0, 1 or 2");
+      c->split.ws_mode = int(value);
+    } else if (k == "split_min_kb") {
+      require(value >= 1 && value <= 4096, "vp_ctx_set_option: split_min_kb must be in 1..4096");
+      c->split.min_kb = int(value);
     } else if (k == "tma_store") {
       require(value == 0 || value == 1, "vp_ctx_set_option: tma_store must be 0 or 1");
       vp::g_tma_store = int(value);
@@ -1510,6 +1542,81 @@ int vp_run_alg2(vp_ctx_t c, const vp_batch_t* b, const vp_shard_t* shards, const
   });
 }
 
+// Memory-bounded Algorithm 2 (SURVEY §8f-2, R/PAPER.md:498): softmax rows
+// are independent, so the batch runs as consecutive token chunks of at most
+// chunk_tokens rows through S -> C1 -> T, reusing states sized for one chunk
+// (P is chunk_tokens x V_k instead of n_tok x V_k); dW accumulates over the
+// chunks.  Per chunk the exchanges are the same as vp_run_alg2's.
+int vp_run_alg2_chunked(vp_ctx_t c, const vp_batch_t* b, const vp_shard_t* shards, const vp_state_t* states, int n,
+                        int64_t chunk_tokens, double fault_scale, vp_stats_t out, float* loss, float* gx, int64_t ldgx,
+                        float* const* gw, int64_t ldgw) {
+  return api([&] {
+    require(c != nullptr && gx != nullptr && gw != nullptr && loss != nullptr, "run_alg2: null argument");
+    require(out.m != nullptr && out.sum != nullptr, "run_alg2: null argument");
+    check_batch(b);
+    require(chunk_tokens >= 1, "run_alg2_chunked: chunk_tokens must be >= 1");
+    require(n >= 1 && n <= vp::kMaxLocalShards && states != nullptr, "run: bad shard count");
+    for (int k = 0; k < n; ++k)
+      require(states[k] != nullptr && states[k]->n_tok == std::min(chunk_tokens, b->n_tok),
+              "run_alg2_chunked: states must be created for min(chunk_tokens, n_tok) tokens");
+    c->activate();
+    const int64_t cap = states[0]->n_tok;
+    const bool acc0 = c->accumulate_dw;
+    struct Restore {
+      vp_ctx_s* c;
+      const vp_state_t* st;
+      int n;
+      int64_t cap;
+      bool acc0;
+      ~Restore() {
+        c->accumulate_dw = acc0;
+        for (int k = 0; k < n; ++k) st[k]->n_tok = cap;
+      }
+    } restore{c, states, n, cap, acc0};
+    for (int64_t t0 = 0; t0 < b->n_tok; t0 += cap) {
+      const int64_t rows = std::min(cap, b->n_tok - t0);
+      vp_batch_t bc = *b;
+      bc.X = static_cast<const __nv_bfloat16*>(b->X) + t0 * b->ldx;
+      bc.labels = b->labels + t0;
+      bc.n_tok = rows;
+      // a ragged last chunk: the state's kernels index with n_tok as the
+      // leading dimension of its tile stats, so a smaller n_tok stays consistent
+      for (int k = 0; k < n; ++k) states[k]->n_tok = rows;
+      c->accumulate_dw = acc0 || t0 > 0;
+      const vp_stats_t oc{out.m + t0, out.sum + t0};
+      run_alg(2, c, &bc, shards, states, n, fault_scale, oc, loss + t0, gx + t0 * ldgx, ldgx, gw, ldgw);
+    }
+  });
+}
+
+namespace {
+// One block per SM (the whole shared memory), spinning on the global timer:
+// stands in for NCCL's kernels holding SMs during the overlapped exchanges.
+__global__ void k_occupy(unsigned long long ns) {
+  extern __shared__ uint8_t pad[];
+  unsigned long long t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  do {
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (threadIdx.x == 0) pad[0] = uint8_t(t);
+  } while (t - t0 < ns);
+}
+}  // namespace
+
+int vp_debug_occupy_sms(vp_ctx_t c, void* stream, int nsms, int64_t microseconds) {
+  return api([&] {
+    require(c != nullptr && nsms >= 1 && nsms <= c->num_sms && microseconds >= 0,
+            "debug_occupy_sms: bad arguments");
+    c->activate();
+    int smem = 0;
+    VP_CUDA(cudaDeviceGetAttribute(&smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
+    VP_CUDA(cudaFuncSetAttribute(k_occupy, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    k_occupy<<<nsms, 32, size_t(smem), static_cast<cudaStream_t>(stream)>>>(
+        static_cast<unsigned long long>(microseconds) * 1000ull);
+    VP_KCHECK();
+  });
+}
+
 int vp_input_forward(vp_ctx_t c, const int64_t* tokens, int64_t n_tok, int64_t h, const vp_shard_t* s, void* out,
                      int64_t ldo, int accumulate) {
   return api([&] {
@@ -1519,6 +1626,7 @@ int vp_input_forward(vp_ctx_t c, const int64_t* tokens, int64_t n_tok, int64_t h
     require(h % 8 == 0 && ldo >= h && ldo % 8 == 0 && aligned16(out), "input_forward: h/ldo must be multiples of 8");
     if (n_tok == 0) return;
     c->activate();
+    NvtxRange nr("vp:input_forward");
     vp::k_input_forward<<<c->grid_for(n_tok, 8), 256, 0, c->stream>>>(
         tokens, int(n_tok), static_cast<const __nv_bfloat16*>(s->W), s->ldw, s->row_begin, s->row_end, int(h),
         static_cast<__nv_bfloat16*>(out), ldo, accumulate, c->d_err);
@@ -1536,6 +1644,7 @@ int vp_input_backward(vp_ctx_t c, const void* grad, int64_t ldg, int grad_is_f32
     require(h % 8 == 0 && ldg >= h && ldg % 8 == 0 && ldgw >= h && ldgw % 4 == 0 && aligned16(gw) && aligned16(grad),
             "input_backward: h/ld must be multiples of 8");
     c->activate();
+    NvtxRange nr("vp:input_backward");
     const int64_t rows = s->row_end - s->row_begin;
     if (!accumulate) {
       VP_CUDA(cudaMemset2DAsync(gw, size_t(ldgw) * sizeof(float), 0, size_t(h) * sizeof(float), size_t(rows),

@@ -403,19 +403,24 @@ def _alloc_outputs(ctx, batch, shards):
             [torch.empty(s.rows(), h, dtype=torch.float32, device=dev) for s in shards], GlobalStats.empty(n, dev))
 
 
-def _run(fn_name, ctx, batch, shards, fault_scale, states, outputs, with_softmax):
+def _run(fn_name, ctx, batch, shards, fault_scale, states, outputs, with_softmax, chunk_tokens=None):
     n, h = batch.X.shape
-    states = states or [ShardState(ctx, n, h, s.rows()) for s in shards]
+    rows_per_state = n if chunk_tokens is None else min(int(chunk_tokens), n)
+    states = states or [ShardState(ctx, rows_per_state, h, s.rows()) for s in shards]
     loss, gx, gw, stats = outputs or _alloc_outputs(ctx, batch, shards)
     b = batch.c()
     gw_arr = (ctypes.c_void_p * len(gw))(*[t.data_ptr() for t in gw])
     args = [ctx.handle, ctypes.byref(b), _shards_arr(shards), _states_arr(states), len(shards)]
+    if chunk_tokens is not None:
+        args.append(int(chunk_tokens))
     if fn_name != "vp_naive_partitioned_output":
         args.append(float(fault_scale))
     args += [stats.c(), _p(loss), _p(gx), gx.stride(0), gw_arr, gw[0].stride(0)]
     check(getattr(ctx.lib, fn_name)(*args))
     for st in states:
         st.has_grad_terms = fn_name == "vp_run_alg2"
+    if chunk_tokens is not None and with_softmax:
+        raise ValueError("run_alg2_chunked: states hold only the last chunk (no softmax assembly)")
     out = OutputResult(loss, gx, gw, stats, states)
     if with_softmax:
         out.softmax = torch.cat([st.softmax(stats) for st in states], dim=1)
@@ -440,6 +445,14 @@ def run_alg2(ctx: Context, batch: TokenBatch, shards: Sequence[EmbeddingShard], 
              states=None, outputs=None, with_softmax: bool = False) -> OutputResult:
     """VM.cpp:328-361."""
     return _run("vp_run_alg2", ctx, batch, shards, fault_scale, states, outputs, with_softmax)
+
+
+def run_alg2_chunked(ctx: Context, batch: TokenBatch, shards: Sequence[EmbeddingShard], chunk_tokens: int,
+                     fault_scale: float = 1.0, states=None, outputs=None) -> OutputResult:
+    """Memory-bounded run_alg2 (SURVEY §8f-2, R/PAPER.md:498): token chunks of
+    at most chunk_tokens rows through S -> C1 -> T with states (P) sized for
+    one chunk; dW accumulates over the chunks (vp_run_alg2_chunked)."""
+    return _run("vp_run_alg2_chunked", ctx, batch, shards, fault_scale, states, outputs, False, chunk_tokens)
 
 
 def oracle_output_layer(ctx: Context, batch: TokenBatch, W: torch.Tensor, logit_shift: Optional[torch.Tensor] = None,

@@ -73,3 +73,52 @@ def assert_parity(res, ref, what=""):
 
 __all__ = ["oracle", "bf16_round", "pad8", "to_dev_bf16", "rel_l2", "device_case", "run_device", "assert_parity",
            "LOSS_ABS", "GRAD_REL_L2", "SOFTMAX_ABS"]
+
+
+def fp64_full_check(out, X, W, labels, chunk=16000):
+    """Full-size parity without the CPU oracle: an fp64 torch restatement of
+    oracle_output_layer (VM.cpp:31-63) streamed over vocabulary chunks on the
+    GPU (cuBLAS DGEMM; none of this library's kernels), compared with EVERY
+    loss, grad_x and grad_w entry of `out`.  Returns (loss max abs err,
+    grad_x rel-L2, grad_w rel-L2)."""
+    T, h = X.shape
+    V = W.shape[0]
+    X64 = X.double()
+    lab = labels.long()
+    m = torch.full((T,), -float("inf"), dtype=torch.float64, device=X.device)
+    s = torch.zeros(T, dtype=torch.float64, device=X.device)
+    ylab = torch.zeros(T, dtype=torch.float64, device=X.device)
+    for v0 in range(0, V, chunk):
+        v1 = min(V, v0 + chunk)
+        Y = X64 @ W[v0:v1].double().T
+        cm = Y.max(dim=1).values
+        nm = torch.maximum(m, cm)
+        s = s * torch.exp(m - nm) + torch.exp(Y - nm[:, None]).sum(dim=1)
+        m = nm
+        own = (lab >= v0) & (lab < v1)
+        idx = torch.nonzero(own)[:, 0]
+        ylab[idx] = Y[idx, lab[idx] - v0]
+        del Y
+    lse = m + torch.log(s)
+    loss_err = (out.loss.double() - (lse - ylab)).abs().max().item()
+    gx = torch.zeros(T, h, dtype=torch.float64, device=X.device)
+    gw_num = 0.0
+    gw_den = 0.0
+    gw_dev = out.grad_w_full() if len(out.grad_w) > 1 else out.grad_w[0]
+    for v0 in range(0, V, chunk):
+        v1 = min(V, v0 + chunk)
+        Wc = W[v0:v1].double()
+        G = torch.exp(X64 @ Wc.T - lse[:, None])
+        own = (lab >= v0) & (lab < v1)
+        idx = torch.nonzero(own)[:, 0]
+        G[idx, lab[idx] - v0] -= 1.0
+        gx += G @ Wc
+        gw_ref = G.T @ X64
+        gw_num += (gw_dev[v0:v1, :h].double() - gw_ref).square().sum().item()
+        gw_den += gw_ref.square().sum().item()
+        del G, gw_ref, Wc
+    gx_err = ((out.grad_x[:, :h].double() - gx).norm() / gx.norm()).item()
+    return loss_err, gx_err, (gw_num / max(gw_den, 1e-300)) ** 0.5
+
+
+__all__.append("fp64_full_check")

@@ -46,9 +46,13 @@ int main(int argc, char** argv) {
   const std::string kind = argv[1];
   const int raster = atoi(argv[2]), pa = atoi(argv[3]), pb = atoi(argv[4]);
   const int iters = argc > 5 ? atoi(argv[5]) : 10;
-  const int64_t T = 8192, h = 4096, V = argc > 6 ? atoll(argv[6]) : 256000;
+  // VP_T / VP_H: token count and hidden size (default: the headline shape)
+  const int64_t T = getenv("VP_T") ? atoll(getenv("VP_T")) : 8192, h = getenv("VP_H") ? atoll(getenv("VP_H")) : 4096,
+                V = argc > 6 ? atoll(argv[6]) : 256000;
   int nsm = 0;
   if (getenv("VP_TMA_STORE")) vp::g_tma_store = atoi(getenv("VP_TMA_STORE"));
+  // ncu's kernel replay cannot relaunch cooperative grids (as in the library)
+  if (getenv("NV_NSIGHT_INJECTION_TRANSPORT_TYPE") || getenv("CUDA_INJECTION64_PATH")) vp::g_cooperative = 0;
   CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0));
   __nv_bfloat16 *X, *W, *P;
   float* out;
@@ -82,6 +86,11 @@ int main(int argc, char** argv) {
   CK(cudaMemset(scfg.flags, 0, 2 * 16384 * sizeof(int)));
   scfg.max_tiles = 16384;
   scfg.force = split_dx > 0 ? split_dx : 0;
+  // VP_WS: parallel split-K workspace mode (0 never, 1 auto, 2 force); VP_MINKB: ordered-split floor
+  scfg.ws_mode = getenv("VP_WS") ? atoi(getenv("VP_WS")) : 1;
+  scfg.min_kb = getenv("VP_MINKB") ? atoi(getenv("VP_MINKB")) : 64;
+  scfg.ws_elems = size_t(nsm / 2 + 2) * 256 * 512 + (size_t(1) << 16);
+  CK(cudaMalloc(&scfg.ws, scfg.ws_elems * sizeof(float)));
   // VP_LOCKSTEP: wave-lockstep epoch (k-blocks, 0 = off)
   vp::LockCfg lcfg;
   lcfg.epoch = getenv("VP_LOCKSTEP") ? atoi(getenv("VP_LOCKSTEP")) : 0;
@@ -103,7 +112,7 @@ int main(int argc, char** argv) {
     } else if (kind == "dw") {
       vp::EpiStoreF32::Params ep{out, h, nullptr, 0, nullptr};
       vp::launch_gemm<vp::EpiStoreF32>(2, {P, V, true}, {X, h, true}, int(V), int(h), int(T), raster, ep, nsm, 0, pa,
-                                       pb, mc, nh, nullptr, &lcfg);
+                                       pb, mc, nh, split_dx ? &scfg : nullptr, &lcfg);
     } else {  // sq8192: plain 8192^3 K-major GEMM (W as an 8192 x 8192 slice), fp32 out
       vp::EpiStoreF32::Params ep{out, 8192, nullptr, 0, nullptr};
       vp::launch_gemm<vp::EpiStoreF32>(2, {W, 8192, false}, {W + int64_t(8192) * 8192, 8192, false}, 8192, 8192,
