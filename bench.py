@@ -60,6 +60,8 @@ def parse():
                     help="N>1 without N GPUs: ranks share the visible GPU(s) (round-robin) and exchange through the "
                          "library's loopback backend (CUDA IPC mailboxes) instead of NCCL; torch.distributed runs on "
                          "gloo.  Exercises the whole multi-rank path; the timing is not a scaling number.")
+    ap.add_argument("--chunk-tokens", type=int, default=0,
+                    help="alg2 in token chunks of this size with P held for one chunk (vp_run_alg2_chunked)")
     ap.add_argument("--ids", choices=["uniform", "zipf"], default="uniform",
                     help="input workload: token-id distribution (zipf: s=1.1 over the vocabulary)")
     return ap.parse_args()
@@ -232,7 +234,7 @@ class Step:
     """Pre-marshalled call of vp_run_alg{1,2} / vp_naive_partitioned_output for
     one rank's shard (no per-step Python allocation or argument building)."""
 
-    def __init__(self, ctx, alg, batch, shard, state, outs):
+    def __init__(self, ctx, alg, batch, shard, state, outs, chunk_tokens=0):
         from paper_2411_05288_b200._lib import vp_shard_t
         self.ctx = ctx
         loss, gx, gw, stats = outs
@@ -249,6 +251,8 @@ class Step:
         else:
             fn = lib.vp_run_alg2 if alg == "alg2" else lib.vp_run_alg1
             self.fn, self.args = fn, head + [1.0] + common_tail
+            if chunk_tokens:  # memory-bounded alg2 (vp_run_alg2_chunked)
+                self.fn, self.args = lib.vp_run_alg2_chunked, head + [int(chunk_tokens), 1.0] + common_tail
 
     def __call__(self):
         rc = self.fn(*self.args)
@@ -306,10 +310,12 @@ def run_ours(args):
     W_k = (torch.randn(rows, h, device="cuda", generator=gen) * 0.02).to(torch.bfloat16)
     shard = vm.EmbeddingShard(W_k, rank, row_begin, row_end)
     batch = vm.TokenBatch(X, labels)
-    state = vm.ShardState(ctx, T, h, rows)
+    if args.chunk_tokens and args.alg != "alg2":
+        raise SystemExit("--chunk-tokens needs --alg alg2")
+    state = vm.ShardState(ctx, min(args.chunk_tokens, T) if args.chunk_tokens else T, h, rows)
     outs = (torch.empty(T, dtype=torch.float32, device="cuda"), torch.empty(T, h, dtype=torch.float32, device="cuda"),
             torch.empty(rows, h, dtype=torch.float32, device="cuda"), vm.GlobalStats.empty(T, "cuda"))
-    step = Step(ctx, args.alg, batch, shard, state, outs)
+    step = Step(ctx, args.alg, batch, shard, state, outs, args.chunk_tokens)
     stream = torch.cuda.current_stream()
 
     def barrier():
@@ -373,7 +379,8 @@ def run_ours(args):
         # every step's copy and its loss read-back stay inside the timed region.
         copy_stream = torch.cuda.Stream()
         bufs = [(torch.empty_like(X), torch.empty_like(labels)) for _ in range(2)]
-        steps_e2e = [Step(ctx, args.alg, vm.TokenBatch(xd, ld), shard, state, outs) for xd, ld in bufs]
+        steps_e2e = [Step(ctx, args.alg, vm.TokenBatch(xd, ld), shard, state, outs, args.chunk_tokens)
+                     for xd, ld in bufs]
         ready = [torch.cuda.Event() for _ in range(2)]
         consumed = [torch.cuda.Event() for _ in range(2)]
 
@@ -424,7 +431,9 @@ def run_ours(args):
     peak = peaks.get("bf16_tflops_sustained") if peaks else 1400.0
     peak_src = "MEASURED_PEAKS.json bf16_tflops_sustained (kernel timed inside a long step)" if peaks else \
         "fallback (B200_PROFILING.md)"
-    flops_launch = 2.0 * T * h * rows  # each of K1 (logits), K3 (dX / A), K4 (dW)
+    # each of K1 (logits), K3 (dX / A), K4 (dW); chunked alg2 launches each once per chunk
+    chunks = -(-T // args.chunk_tokens) if args.chunk_tokens else 1
+    flops_launch = 2.0 * T * h * rows / chunks
     kern = {}
     for name, (kms, n) in gemm.items():
         if n:
@@ -447,11 +456,14 @@ def run_ours(args):
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         T_s, V_s, p_s = cpu_sample_shape(args, V)  # the --impl reference arm's sample
-        times, cores = cpu_reference_sample(T_s, h, V_s, p_s, reps=3)
-        t_s = statistics.mean(times[1:])
+        # the same schedule as the --impl reference arm (W warm-up + K timed
+        # samples), so the two CPU legs agree (sustained host clocks included)
+        times, cores = cpu_reference_sample(T_s, h, V_s, p_s, reps=args.warmup + args.steps)
+        t_s = statistics.mean(times[args.warmup:])
         cpu = {"value": T_s / (t_s * V / V_s), "unit": "tokens/s", "cores": cores, "kind": "port",
                "sample": (f"CPU oracle run_alg2 (fp64, restates VM.cpp:328-361) on {T_s} tokens x {V_s} of {V} "
-                          f"vocab rows, h={h}, p={p_s}, mean of 2 after 1 warm-up: {t_s:.1f} s; tokens/s scaled by {V_s}/{V} "
+                          f"vocab rows, h={h}, p={p_s}, mean of {args.steps} after {args.warmup} warm-up: {t_s:.2f} s; "
+                          f"tokens/s scaled by {V_s}/{V} "
                           f"(the --impl reference arm's sample); host {host_info()}")}
 
     line = {
@@ -462,6 +474,8 @@ def run_ours(args):
             "alg2": "Algorithm 2 (reduced barrier)", "alg1": "Algorithm 1 (2 barriers)",
             "naive": "naive 3-barrier"}[args.alg]),
             "alg": args.alg, "tokens": T, "hidden": h, "vocab": V, "vocab_rows_per_gpu": rows,
+            **({"chunk_tokens": args.chunk_tokens,
+                "P_bytes": 2 * min(args.chunk_tokens, T) * (rows + 63) // 64 * 64} if args.chunk_tokens else {}),
             "parallelism": f"vocab{world}", "operands": "bf16", "accum_and_stats": "fp32",
             "cta_group": args.cta_group, "options": args.opt,
             "l2": "inputs larger than L2 every step (W_k %.0f MB, P %.0f MB per GPU)" % (

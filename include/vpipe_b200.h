@@ -257,6 +257,21 @@ int vp_input_forward(vp_ctx_t ctx, const int64_t* tokens, int64_t n_tok, int64_t
 int vp_input_backward(vp_ctx_t ctx, const void* grad_out, int64_t ldg, int grad_is_f32, const int64_t* tokens,
                       int64_t n_tok, int64_t h, const vp_shard_t* shard, float* grad_w, int64_t ldgw,
                       int accumulate);
+/* The input layer's forward over the whole group without the zero-padded
+ * all-reduce: every rank gets out[i] = W[tok_i] (a zero row when no shard owns
+ * tok_i), i.e. input_forward summed over the shards (VM.cpp:227-236 +
+ * R/PAPER.md:582), by an owner gather: ranks pack the rows they own and
+ * exchange only those in one grouped broadcast per rank (about half the bytes
+ * of the sum all-reduce; pure copies, bit-exact).  Synchronises the context
+ * stream once (block sizes to the host); not capturable.  One rank: equals
+ * vp_input_forward. */
+int vp_input_forward_gathered(vp_ctx_t ctx, const int64_t* tokens, int64_t n_tok, int64_t h,
+                              const vp_shard_t* shard, void* out, int64_t ldo);
+/* The input layer's pre-backward broadcast (R/PAPER.md:582): grad_out of the
+ * embedding output [n_tok x h] (row stride ldg; fp32 or bf16), in place from
+ * rank `root` to every rank of the group.  No-op without a group. */
+int vp_input_grad_broadcast(vp_ctx_t ctx, void* grad_out, int64_t ldg, int grad_is_f32, int64_t n_tok, int64_t h,
+                            int root);
 /* In-place sum all-reduce over the context's NCCL group (the input layer's
  * post-forward all-reduce, R/PAPER.md:582).  dtype 0 = fp32, 1 = bf16. */
 int vp_allreduce_sum(vp_ctx_t ctx, void* buf, int64_t count, int dtype);

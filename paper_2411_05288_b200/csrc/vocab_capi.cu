@@ -133,6 +133,8 @@ struct vp_ctx_s {
   int nranks = 1, rank = 0;
   bool gemm_sms_set = false;  // "gemm_sms" given explicitly (else a colocated share)
   int64_t vocab_cache_key = -1, vocab_cache = -1;  // global V of the group (label checks)
+  vp::RankBounds bounds{};  // every rank's shard rows (owner-gather input forward), cached
+  int64_t bounds_key_rb = -1, bounds_key_re = -1;
   int* d_err = nullptr;
   int64_t launches = 0;
   // optional per-GEMM event timing (bench instrumentation): kind -> events
@@ -932,6 +934,8 @@ void attach_comm(vp_ctx_s* c, std::unique_ptr<vp::Comm> comm) {
   c->rank = comm->rank;
   const int share = comm->colocated();
   c->comm = std::move(comm);
+  c->vocab_cache_key = -1;  // group-derived caches belong to the previous group
+  c->bounds_key_rb = c->bounds_key_re = -1;
   if (share > 1 && !c->gemm_sms_set) c->gemm_sms = std::max(2, c->num_sms / share / 2 * 2);
   int lo = 0, hi = 0;
   VP_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
@@ -1657,6 +1661,97 @@ int vp_input_backward(vp_ctx_t c, const void* grad, int64_t ldg, int grad_is_f32
     else
       segment_scatter(c, tokens, n_tok, s->row_begin, s->row_end, static_cast<const __nv_bfloat16*>(grad), ldg, h, 1.f,
                       gw, ldgw, 1, kErrInputBwd);
+  });
+}
+
+// Row ranges of every rank's shard (all-gathered once per layout, cached).
+const vp::RankBounds& rank_bounds(vp_ctx_s* c, const vp_shard_t* s) {
+  if (c->bounds_key_rb == s->row_begin && c->bounds_key_re == s->row_end && c->bounds.n == c->nranks)
+    return c->bounds;
+  require(c->nranks <= vp::kMaxRanks, "input_forward_gathered: too many ranks");
+  require(s->row_end < (int64_t(1) << 24), "input_forward_gathered: vocab size must be < 2^24");
+  float* d = c->buf<float>(c->vtmp, size_t(2 + 2 * c->nranks));
+  const float mine[2] = {float(s->row_begin), float(s->row_end)};
+  VP_CUDA(cudaMemcpyAsync(d, mine, sizeof(mine), cudaMemcpyHostToDevice, c->stream));
+  c->cm().all_gather(d, d + 2, 2, vp::DType::F32, c->stream);
+  std::vector<float> all(size_t(2 * c->nranks));
+  VP_CUDA(cudaMemcpyAsync(all.data(), d + 2, all.size() * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+  VP_CUDA(cudaStreamSynchronize(c->stream));
+  c->bounds.n = c->nranks;
+  for (int k = 0; k < c->nranks; ++k) {
+    c->bounds.rb[k] = int64_t(all[size_t(2 * k)]);
+    c->bounds.re[k] = int64_t(all[size_t(2 * k + 1)]);
+  }
+  c->bounds_key_rb = s->row_begin;
+  c->bounds_key_re = s->row_end;
+  return c->bounds;
+}
+
+int vp_input_forward_gathered(vp_ctx_t c, const int64_t* tokens, int64_t n_tok, int64_t h, const vp_shard_t* s,
+                              void* out, int64_t ldo) {
+  return api([&] {
+    require(c != nullptr && out != nullptr && tokens != nullptr, "input_forward: null argument");
+    require(n_tok >= 0, "input_forward: negative token count");
+    check_shard(s, h);
+    require(h % 8 == 0 && ldo >= h && ldo % 8 == 0 && aligned16(out), "input_forward: h/ldo must be multiples of 8");
+    if (n_tok == 0) return;
+    c->activate();
+    if (!c->distributed()) {  // one rank: the plain masked gather is the whole layer
+      NvtxRange nr("vp:input_forward");
+      vp::k_input_forward<<<c->grid_for(n_tok, 8), 256, 0, c->stream>>>(
+          tokens, int(n_tok), static_cast<const __nv_bfloat16*>(s->W), s->ldw, s->row_begin, s->row_end, int(h),
+          static_cast<__nv_bfloat16*>(out), ldo, 0, c->d_err);
+      VP_KCHECK();
+      ++c->launches;
+      return;
+    }
+    require(n_tok < (int64_t(1) << 31), "input_forward_gathered: too many tokens");
+    NvtxRange nr("vp:input_forward(owner gather)");
+    const vp::RankBounds& B = rank_bounds(c, s);
+    int* pos = c->buf<int>(c->heads, size_t(n_tok) + size_t(vp::kMaxRanks));
+    int* counts = pos + n_tok;
+    vp::k_owner_positions<<<1, 1024, 0, c->stream>>>(tokens, int(n_tok), B, pos, counts, c->d_err);
+    VP_KCHECK();
+    std::vector<int> cnt(size_t(B.n));
+    VP_CUDA(cudaMemcpyAsync(cnt.data(), counts, cnt.size() * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    VP_CUDA(cudaStreamSynchronize(c->stream));  // the block sizes of the broadcasts (host side)
+    vp::RankOffsets O{};
+    int64_t total = 0;
+    for (int k = 0; k < B.n; ++k) {
+      O.off[k] = total;
+      total += cnt[size_t(k)];
+    }
+    auto* buf = c->buf<__nv_bfloat16>(c->xs, size_t(std::max<int64_t>(total, 1) * h));
+    vp::k_owner_pack<<<c->grid_for(n_tok, 8), 256, 0, c->stream>>>(
+        tokens, int(n_tok), B, pos, O, c->rank, static_cast<const __nv_bfloat16*>(s->W), s->ldw, int(h), buf);
+    VP_KCHECK();
+    c->cm().group_start();
+    for (int k = 0; k < B.n; ++k)
+      if (cnt[size_t(k)] > 0)
+        c->cm().broadcast(buf + O.off[k] * h, buf + O.off[k] * h, size_t(cnt[size_t(k)]) * size_t(h),
+                          vp::DType::BF16, k, c->stream);
+    c->cm().group_end();
+    vp::k_owner_unpack<<<c->grid_for(n_tok, 8), 256, 0, c->stream>>>(tokens, int(n_tok), B, pos, O, buf, int(h),
+                                                                     static_cast<__nv_bfloat16*>(out), ldo);
+    VP_KCHECK();
+    c->launches += 3;
+  });
+}
+
+// The input layer's pre-backward broadcast (R/PAPER.md:582): grad_out of the
+// embedding output, produced on one rank, to every vocabulary shard.
+int vp_input_grad_broadcast(vp_ctx_t c, void* grad, int64_t ldg, int grad_is_f32, int64_t n_tok, int64_t h,
+                            int root) {
+  return api([&] {
+    require(c != nullptr && grad != nullptr, "input_grad_broadcast: null argument");
+    require(n_tok >= 0 && h >= 1 && ldg >= h, "input_grad_broadcast: bad shape");
+    if (!c->distributed() || n_tok == 0) return;
+    require(root >= 0 && root < c->nranks, "input_grad_broadcast: root out of range");
+    c->activate();
+    NvtxRange nr("vp:input_grad_broadcast");
+    // the logical extent (ldg may pad rows; the pad is carried along)
+    const size_t count = size_t((n_tok - 1) * ldg + h);
+    c->cm().broadcast(grad, grad, count, grad_is_f32 ? vp::DType::F32 : vp::DType::BF16, root, c->stream);
   });
 }
 

