@@ -77,6 +77,23 @@ def test_gemma_shape_8_shards_reduced_tokens(ctx):
     assert_parity(res, ref, "gemma p=8 alg2")
 
 
+@pytest.mark.parametrize("V", [32000, 128256, 262144, 524288])
+def test_vocab_sweep_8_shards_naive_and_alg2(ctx, V):
+    # BASELINE configs[4] (vocabulary sweep 32k-512k at h=4096, 8 shards),
+    # naive 3-barrier vs reduced-barrier, T reduced for the oracle
+    rng = np.random.default_rng(V % 1000)
+    T, h = 8, 4096
+    X = rng.standard_normal((T, h))
+    W = rng.standard_normal((V, h)) * 0.02
+    g = rng.integers(0, V, T)
+    g[0] = V - 1  # the last row of the last shard
+    Xb, Wb, batch, Wd = device_case(X, W, g)
+    ref = oracle.oracle_output_layer(Xb, g, Wb, want_softmax=False)
+    for alg in ("naive", "alg2"):
+        res, _ = run_device(ctx, alg, batch, Wd, 8, h, with_softmax=False)
+        assert_parity(res, ref, f"sweep V={V} {alg}")
+
+
 def test_large_logits_uniform_inputs(ctx):
     # reference-style U[-1,1] operands at h=2048: logit std ~26, so the
     # per-tile max subtraction is exercised hard

@@ -7,3 +7,5 @@ for sef in 0 1; do export VP_SEF=$sef; echo "#### store_evict_first=$sef"
   run dw -4 2 2; run dw -8 2 2; run dw -8 1 2; run dw -4 1 2
   run dx 16 2 2; run dx 32 2 1; run dx 8 2 2
 done
+timeout 2400 python -m pytest tests/test_gpu_robustness.py -q > gpurun_out/r02n_pytest.log 2>&1; echo pytest_rc=$?
+tail -20 gpurun_out/r02n_pytest.log
