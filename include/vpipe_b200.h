@@ -91,7 +91,8 @@ int vp_ctx_reserve(vp_ctx_t ctx, int64_t n_tok, int64_t h, int p);
 /* Options: "cta_group" (1 or 2, default 2), "gemm_sms" (SMs used by GEMMs),
  * "raster_{logits,dx,dw}" (tile order, see GemmGeom::raster),
  * "policy_{logits,dx,dw}" (TMA L2 policy of both operands: -1 per-epilogue default,
- * 0 normal, 1 first, 2 last = the default), "policyb_{logits,dx,dw}" (B operand only),
+ * 0 normal, 1 first, 2 last = the default), "policyb_{logits,dx,dw}" (B operand only;
+ * logits default 1: W evict-first so X stays L2-resident),
  * "multicast" (1 = CTA-pair clusters, 2 = 4-CTA clusters sharing B by TMA multicast),
  * "nh_logits" / "nh_dx" / "nh_dw" (1 = 256x256 pair tiles, 2 = 256x512 pair tiles),
  * "force_collectives" (1 = use the NCCL group even with one rank; tests),
@@ -100,7 +101,9 @@ int vp_ctx_reserve(vp_ctx_t ctx, int64_t n_tok, int64_t h, int p);
  * during the overlap and NCCL's maxCTAs; set before vp_ctx_comm_init),
  * "epi_wait" (GEMM epilogue wait: 0 try_wait loop, 1 nanosleep backoff;
  * process-wide), "store_evict_first" (1 = epilogue TMA stores with an L2
- * evict-first hint; default 0; process-wide),
+ * evict-first hint; default 0; process-wide), "store_hint_{logits,dx,dw}"
+ * (per GEMM of this context: 1 evict-first, 0 normal, -1 the process-wide
+ * option; default logits 1 (P), dx / dw -1),
  * "lockstep_logits" / "lockstep_dx" / "lockstep_dw" (wave lockstep of the
  * persistent GEMM's clusters every N k-blocks so co-scheduled tiles share
  * operand bands in L2; 0 = off; default 8 for all three),

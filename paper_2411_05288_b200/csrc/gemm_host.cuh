@@ -202,7 +202,8 @@ inline int g_cooperative = 1;        // cooperative (co-resident) launches of th
 template <int CG, bool A_MN, bool B_MN, class Epi, int MC = 1, int NH = 1>
 inline void launch_gemm_t(const Operand& A, const Operand& B, int M, int N, int K, int raster,
                           const typename Epi::Params& ep, int num_sms, cudaStream_t st, int pol_a = -1,
-                          int pol_b = -1, SplitCfg* split = nullptr, const LockCfg* lock = nullptr) {
+                          int pol_b = -1, SplitCfg* split = nullptr, const LockCfg* lock = nullptr,
+                          int store_hint = -1) {
   using C = GemmCfg<CG, NH>;
   const CUtensorMap ta = A_MN ? make_tmap_bf16(A.ptr, uint64_t(M), uint64_t(K), uint64_t(A.ld), 64, 64)
                               : make_tmap_bf16(A.ptr, uint64_t(K), uint64_t(M), uint64_t(A.ld), 64, C::BM_CTA);
@@ -221,7 +222,7 @@ inline void launch_gemm_t(const Operand& A, const Operand& B, int M, int N, int 
   g.pol_a = pol_a;
   g.pol_b = pol_b;
   g.prof = g_gemm_prof;
-  g.store_evict_first = g_store_evict_first;
+  g.store_evict_first = store_hint >= 0 ? store_hint : g_store_evict_first;
   g.epi_wait = g_epi_wait;
   auto kern = gemm_sm100_kernel<CG, A_MN, B_MN, Epi, MC, NH>;
   // per device: the smem attribute and the occupancy query (contexts of one
@@ -332,10 +333,11 @@ template <class Epi>
 inline void launch_gemm(int cg, const Operand& A, const Operand& B, int M, int N, int K, int raster,
                         const typename Epi::Params& ep, int num_sms, cudaStream_t st, int pol_a = -1,
                         int pol_b = -1, int mc = 1, int nh = 1, SplitCfg* split = nullptr,
-                        const LockCfg* lock = nullptr) {
+                        const LockCfg* lock = nullptr, int store_hint = -1) {
 #define VP_GEMM_CASE(CGV, AM, BM_, MCV, NHV)                                                                        \
   if (cg == CGV && A.mn_major == AM && B.mn_major == BM_ && mc == MCV && nh == NHV) {                               \
-    launch_gemm_t<CGV, AM, BM_, Epi, MCV, NHV>(A, B, M, N, K, raster, ep, num_sms, st, pol_a, pol_b, split, lock);  \
+    launch_gemm_t<CGV, AM, BM_, Epi, MCV, NHV>(A, B, M, N, K, raster, ep, num_sms, st, pol_a, pol_b, split, lock,    \
+                                               store_hint);                                                        \
     return;                                                                                                         \
   }
   VP_GEMM_CASE(2, false, false, 1, 1)

@@ -110,7 +110,12 @@ struct vp_ctx_s {
   // GEMMs, +2.7% tokens/s over evict_normal, tools/experiments/combo_ab.sh)
   int raster[3] = {16, 16, -4};  // logits: M-fastest in groups of 16 m-tiles (+1.3% with lockstep)
   int pol[3] = {2, 2, 2};
-  int polb[3] = {-9, -9, -9};  // B-operand policy when set ("policyb_*"); -9 = same as pol
+  // B-operand policy when set ("policyb_*"); -9 = same as pol.  Logits: W
+  // evict-first, with P stored evict-first (store_hint), so X stays in L2:
+  // K1 DRAM 13.3 -> 9.8 GB per launch at the headline (ncu, r02n), step
+  // throughput unchanged (r02o)
+  int polb[3] = {1, -9, -9};
+  int store_hint[3] = {1, -1, -1};  // epilogue store L2 hint per GEMM: 1 evict-first, 0 normal, -1 process-wide option
   int pb(int i) const { return polb[i] == -9 ? pol[i] : polb[i]; }
   int mc = 1;  // CTA pairs per cluster sharing B by TMA multicast (1 or 2)
   int nh[3] = {2, 2, 2};  // N halves per tile (2 = 256 x 512 pair tiles) for [logits, dX, dW]
@@ -274,7 +279,8 @@ void gemm_logits(vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* s, vp_state
   timed_gemm(c, 0, [&] {
     vp::launch_gemm<vp::EpiLogitStats>(c->cg, {b->X, b->ldx, false}, {s->W, s->ldw, false}, int(b->n_tok),
                                        int(st->rows), int(b->h), c->raster[0], ep, c->gemm_sms, c->stream,
-                                       c->pol[0], c->pb(0), c->eff_mc(0), c->eff_nh(0), nullptr, c->lock_for(0));
+                                       c->pol[0], c->pb(0), c->eff_mc(0), c->eff_nh(0), nullptr, c->lock_for(0),
+                                       c->store_hint[0]);
   });
   ++c->launches;
 }
@@ -298,7 +304,7 @@ void gemm_dx(vp_ctx_s* c, vp_state_s* st, const vp_shard_t* s, float* out, int64
     vp::launch_gemm<vp::EpiStoreF32>(c->cg, {st->P, st->ldp, false}, {s->W, s->ldw, true}, int(st->n_tok),
                                      int(st->h), int(st->rows), c->raster[1], ep, c->gemm_sms, c->stream, c->pol[1],
                                      c->pb(1), c->eff_mc(1), c->eff_nh(1), c->splits_dx == 1 ? nullptr : &c->split,
-                                     c->lock_for(1));
+                                     c->lock_for(1), c->store_hint[1]);
   });
   ++c->launches;
 }
@@ -312,7 +318,7 @@ void gemm_dw(vp_ctx_s* c, vp_state_s* st, const void* Xop, int64_t ldx, float* o
     vp::launch_gemm<vp::EpiStoreF32>(c->cg, {st->P, st->ldp, true}, {Xop, ldx, true}, int(st->rows), int(st->h),
                                      int(st->n_tok), raster, ep, c->gemm_sms, c->stream, c->pol[2], c->pb(2),
                                      c->eff_mc(2), c->eff_nh(2), c->splits_dw == 1 ? nullptr : &c->split,
-                                     c->lock_for(2));
+                                     c->lock_for(2), c->store_hint[2]);
   });
   ++c->launches;
 }
@@ -1112,6 +1118,9 @@ int vp_ctx_set_option(vp_ctx_t c, const char* key, int64_t value) {
     } else if (k == "store_evict_first") {
       require(value == 0 || value == 1, "vp_ctx_set_option: store_evict_first must be 0 or 1");
       vp::g_store_evict_first = int(value);
+    } else if (k == "store_hint_logits" || k == "store_hint_dx" || k == "store_hint_dw") {
+      require(value >= -1 && value <= 1, "vp_ctx_set_option: store_hint_* must be -1, 0 or 1");
+      c->store_hint[k == "store_hint_logits" ? 0 : k == "store_hint_dx" ? 1 : 2] = int(value);
     } else if (k == "splits_dx" || k == "splits_dw") {
       require(value >= 0 && value <= 32, "vp_ctx_set_option: splits_dx / splits_dw must be in 0..32");
       (k == "splits_dx" ? c->splits_dx : c->splits_dw) = int(value);
