@@ -450,6 +450,16 @@ def test_gemm_schedule_options_do_not_change_results(ctx):
             assert np.array_equal(res[key], base[key]), (opts, key)
         octx.close()
     vm.Context(0).set_option("store_evict_first", 0)  # process-wide option: restore
+    # other tile shapes: 256 x 256 pair tiles, with and without 4-CTA clusters
+    # sharing B by TMA multicast (different split-K choices: tolerance, not bits)
+    for opts in ({"nh_logits": 1, "nh_dx": 1, "nh_dw": 1}, {"nh_logits": 1, "nh_dx": 1, "nh_dw": 1, "multicast": 2}):
+        octx = vm.Context(0)
+        for k, v in opts.items():
+            octx.set_option(k, v)
+        _, out = run_device(octx, "alg2", batch, Wd, 1, 1024, with_softmax=False)
+        dl, gx, gw = fp64_full_check(out, batch.X, Wd, batch.labels)
+        assert dl <= LOSS_ABS and gx <= GRAD_REL_L2 and gw <= GRAD_REL_L2, (opts, dl, gx, gw)
+        octx.close()
 
 
 @pytest.mark.parametrize("T", [1, 3, 129])
