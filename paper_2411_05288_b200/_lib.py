@@ -11,7 +11,9 @@ import os
 from ctypes import POINTER, c_char_p, c_double, c_int, c_int32, c_int64, c_void_p
 
 LIB_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib")
-LIB_PATH = os.path.join(LIB_DIR, "libvpipe_b200.so")
+# VPIPE_LIB: an alternative build of the same library (developer A/B of
+# compile-time kernel variants, tools/build_variant.sh)
+LIB_PATH = os.environ.get("VPIPE_LIB") or os.path.join(LIB_DIR, "libvpipe_b200.so")
 
 VP_OK, VP_EINVAL, VP_ECUDA, VP_ENCCL, VP_EINTERNAL = 0, 1, 2, 3, 4
 

@@ -57,6 +57,25 @@ def test_chunked_alg2_long_context_shape(ctx):
     assert dl <= LOSS_ABS and gx <= GRAD_REL_L2 and gw <= GRAD_REL_L2, (dl, gx, gw)
 
 
+@pytest.mark.parametrize("chunk", [0, 16384])
+def test_long_context_past_2_to_the_31_logits(ctx, chunk):
+    # T = 65536 tokens x V = 33000 rows: P has 2.16e9 entries (> 2^31), so
+    # every P / tile-stats offset must be 64-bit; unchunked and in 16384-token
+    # chunks, every output entry against fp64
+    T, h, V = 65536, 512, 33000
+    gen = torch.Generator(device="cuda").manual_seed(9)
+    X = torch.randn(T, h, device="cuda", generator=gen).to(torch.bfloat16)
+    W = (torch.randn(V, h, device="cuda", generator=gen) * 0.05).to(torch.bfloat16)
+    labels = torch.randint(0, V, (T,), device="cuda", generator=gen)
+    labels[-1] = V - 1
+    batch = vm.TokenBatch(X, labels)
+    shards = vm.shard_weights(W, 1)
+    out = vm.run_alg2(ctx, batch, shards) if chunk == 0 else vm.run_alg2_chunked(ctx, batch, shards, chunk)
+    ctx.sync()
+    dl, gx, gw = fp64_full_check(out, X, W, labels, chunk=11000)
+    assert dl <= LOSS_ABS and gx <= GRAD_REL_L2 and gw <= GRAD_REL_L2, (dl, gx, gw)
+
+
 def test_chunked_alg2_argument_errors(ctx):
     X, W, g = oracle.random_instance(64, 32, 256, 2)
     _, _, batch, Wd = device_case(X, W, g)

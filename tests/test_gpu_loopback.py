@@ -72,6 +72,31 @@ def test_drivers_with_p_ranks_match_the_oracle(alg, p):
     _close(ctxs)
 
 
+@pytest.mark.parametrize("p", [2, 4])
+def test_chunked_alg2_across_ranks(p):
+    # the memory-bounded driver with a group: every chunk's stats all-gather,
+    # combine and dX / loss all-reduce (overlapped with the chunk's pass T)
+    T, h, V = 300, 64, 400 * p
+    X, W, g = oracle.random_instance(T, h, V, 30 + p)
+    Xb, Wb, batch, Wd = device_case(X, W, g)
+    ref = oracle.oracle_output_layer(Xb, g, Wb, want_softmax=False)
+    torch.cuda.synchronize()
+    ctxs = vpd.local_group(p)
+
+    def rank(r, ctx):
+        out = vm.run_alg2_chunked(ctx, batch, [_shard(Wd, p, r)], 128)
+        ctx.sync()
+        return out
+
+    outs = vpd.run_ranks(ctxs, rank)
+    for key in ("loss", "grad_x"):
+        _same_on_every_rank(outs, key)
+    res = {"loss": outs[0].loss.double().cpu().numpy(), "grad_x": outs[0].grad_x[:, :h].double().cpu().numpy(),
+           "grad_w": torch.cat([o.grad_w[0] for o in outs])[:, :h].double().cpu().numpy()}
+    assert_parity(res, ref, f"loopback chunked p={p}")
+    _close(ctxs)
+
+
 def test_loopback_equals_local_shards():
     # the same 4 shards run as 4 ranks and as 4 local shards of one context
     p, T, h, V = 4, 64, 128, 2048
