@@ -107,7 +107,7 @@ struct vp_ctx_s {
   int cg = 2;
   // GEMM tile rasterisation and TMA L2 policy per GEMM [logits, dX, dW]
   // (measured with lockstep on: evict_last on both operands of all three
-  // GEMMs, +2.7% tokens/s over evict_normal, tools/experiments/combo_ab.sh)
+  // GEMMs, +2.7% tokens/s over evict_normal, tools/experiments/round1/combo_ab.sh)
   int raster[3] = {16, 16, -4};  // logits: M-fastest in groups of 16 m-tiles (+1.3% with lockstep)
   int pol[3] = {2, 2, 2};
   // B-operand policy when set ("policyb_*"); -9 = same as pol.  Logits: W
