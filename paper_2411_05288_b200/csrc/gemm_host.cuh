@@ -103,6 +103,7 @@ struct SplitCfg {
   size_t ws_elems = 0;
   int ws_mode = 1;    // 0: never use the workspace; 2: force it whenever S > 1 (tests)
   int min_kb = 64;    // ordered splits keep at least this many k-blocks per unit
+  int64_t reduce_launches = 0;  // k_split_reduce launches so far (evidence counters)
 };
 
 // Wave-lockstep state owned by the caller (per stream, like SplitCfg):
@@ -325,7 +326,10 @@ inline void launch_gemm_t(const Operand& A, const Operand& B, int M, int N, int 
   }
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta, tb, g, epc);
   if (e != cudaSuccess) throw std::runtime_error(std::string("gemm launch: ") + cudaGetErrorString(e));
-  if (g.split_ws != nullptr) launch_split_reduce(epc, g, M, N, num_sms, st);
+  if (g.split_ws != nullptr) {
+    launch_split_reduce(epc, g, M, N, num_sms, st);
+    ++split->reduce_launches;
+  }
 }
 
 // Runtime dispatch over (cta_group, operand majors).

@@ -306,7 +306,8 @@ void gemm_dx(vp_ctx_s* c, vp_state_s* st, const vp_shard_t* s, float* out, int64
                                      c->pb(1), c->eff_mc(1), c->eff_nh(1), c->splits_dx == 1 ? nullptr : &c->split,
                                      c->lock_for(1), c->store_hint[1]);
   });
-  ++c->launches;
+  c->launches += 1 + c->split.reduce_launches;
+  c->split.reduce_launches = 0;
 }
 
 // out[rows x h] = P^T . Xop   (Xop [T x h] bf16)
@@ -320,7 +321,8 @@ void gemm_dw(vp_ctx_s* c, vp_state_s* st, const void* Xop, int64_t ldx, float* o
                                      c->eff_mc(2), c->eff_nh(2), c->splits_dw == 1 ? nullptr : &c->split,
                                      c->lock_for(2), c->store_hint[2]);
   });
-  ++c->launches;
+  c->launches += 1 + c->split.reduce_launches;
+  c->split.reduce_launches = 0;
 }
 
 // ---- small kernel wrappers ---------------------------------------------------
@@ -1715,6 +1717,10 @@ int vp_input_forward_gathered(vp_ctx_t c, const int64_t* tokens, int64_t n_tok, 
       return;
     }
     require(n_tok < (int64_t(1) << 31), "input_forward_gathered: too many tokens");
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    VP_CUDA(cudaStreamIsCapturing(c->stream, &cap));
+    require(cap == cudaStreamCaptureStatusNone,
+            "input_forward_gathered: not capturable (the broadcast sizes go through the host)");
     NvtxRange nr("vp:input_forward(owner gather)");
     const vp::RankBounds& B = rank_bounds(c, s);
     int* pos = c->buf<int>(c->heads, size_t(n_tok) + size_t(vp::kMaxRanks));
