@@ -483,6 +483,11 @@ def run_ours(args):
         "e2e": e2e, "graph": graph, "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu,
         "clocks": clk.summary(), "comm": ctx.comm_backend,
     }
+    if world > 1:
+        # C1 of the output layer: the fused reduce-scatter (dX epilogue -> the
+        # token rows' owners over peer memory) or the dX all-reduce
+        line["c1_exchange"] = ("fused: dX GEMM epilogue stores into the owners' peer buffers, owner combine, "
+                               "grad_x all-gather" if ctx.fused_c1_count > 0 else "dX all-reduce")
     if args.dry_run:
         line["dry_run"] = ("N ranks shared %d visible GPU(s) through the loopback backend: a functional run of the "
                            "multi-rank path, not a scaling measurement" % torch.cuda.device_count())

@@ -125,7 +125,16 @@ int vp_ctx_reserve(vp_ctx_t ctx, int64_t n_tok, int64_t h, int p);
  * logits scaled by 1 + ppm * 1e-6; 0 = off),
  * "accumulate_grad_w" (1 = the T passes add dW_k into grad_w: gradient
  * accumulation, or tied input/output embeddings sharing the shard's buffer
- * with vp_input_backward(accumulate=1); R/PAPER.md:333). */
+ * with vp_input_backward(accumulate=1); R/PAPER.md:333),
+ * "fused_c1" (vp_run_alg2 / vp_run_alg2_chunked in a group of nranks > 1:
+ * 1 = the dX GEMM of pass S stores each A_k tile straight into the buffer of
+ * the rank that owns those token rows, over peer memory (NVLink P2P or CUDA
+ * IPC), the label rows follow, and at C1 each owner combines its rows from
+ * local memory and the group all-gathers grad_x — a reduce-scatter fused into
+ * the GEMM epilogue instead of an all-reduce of [n_tok x h] fp32 partials;
+ * grad_x has the bits of a one-GPU run over the same shards.  Default 1; the
+ * group falls back to the all-reduce when a rank cannot map its peers.
+ * 0 = always the all-reduce). */
 int vp_ctx_set_option(vp_ctx_t ctx, const char* key, int64_t value);
 /* The reference's per-row logit_shift test hook (VM.cpp:41-43,
  * oracle_output_layer's `logit_shift`): subsequent pass-S logits are
@@ -140,6 +149,9 @@ int vp_ctx_set_logit_shift(vp_ctx_t ctx, const float* shift);
 int vp_debug_occupy_sms(vp_ctx_t ctx, void* stream, int nsms, int64_t microseconds);
 /* Number of kernels this context has launched (evidence counter). */
 int64_t vp_ctx_launch_count(vp_ctx_t ctx);
+/* Number of fused C1 exchanges (option "fused_c1") this context has run;
+ * -1 for a null context (evidence counter). */
+int64_t vp_ctx_fused_c1_count(vp_ctx_t ctx);
 /* Per-GEMM CUDA-event timing on the launching stream.  Returns (and resets)
  * the accumulated milliseconds / launch counts per GEMM kind since the last
  * call — [0] logits+stats (K1), [1] fp32 logits (naive F1), [2] dX (K3),

@@ -359,6 +359,113 @@ class LoopbackComm final : public Comm {
 
 }  // namespace
 
+// ============================================================================
+// Peer memory (both backends): one all-gather of a 128-byte record per rank.
+// ============================================================================
+namespace {
+struct PeerRecord {
+  int32_t pid;
+  int32_t device;
+  uint64_t ptr;
+  uint64_t host;  // hash of the host name: IPC only maps buffers of this node
+  int32_t ipc_ok;
+  int32_t pad;
+  cudaIpcMemHandle_t h;  // 64 bytes
+  char fill[128 - 32 - sizeof(cudaIpcMemHandle_t)];
+};
+static_assert(sizeof(PeerRecord) == 128, "peer record is 128 bytes");
+
+uint64_t host_hash() {
+  char name[256] = {};
+  gethostname(name, sizeof(name) - 1);
+  uint64_t x = 1469598103934665603ull;
+  for (const char* c = name; *c; ++c) x = (x ^ uint64_t(uint8_t(*c))) * 1099511628211ull;
+  return x;
+}
+}  // namespace
+
+std::vector<void*> Comm::open_peers(void* local, cudaStream_t st) {
+  int dev = 0;
+  VP_CUDA(cudaGetDevice(&dev));
+  PeerRecord mine{};
+  mine.pid = int32_t(getpid());
+  mine.device = dev;
+  mine.ptr = reinterpret_cast<uint64_t>(local);
+  mine.host = host_hash();
+  mine.ipc_ok = cudaIpcGetMemHandle(&mine.h, local) == cudaSuccess ? 1 : 0;
+  (void)cudaGetLastError();
+  void* d = nullptr;
+  VP_CUDA(cudaMalloc(&d, sizeof(PeerRecord) * size_t(nranks + 1) + 16));
+  std::vector<PeerRecord> all(static_cast<size_t>(nranks));
+  std::vector<void*> out(static_cast<size_t>(nranks), nullptr);
+  std::vector<void*> opened;
+  float fail = 0.f;
+  try {
+    VP_CUDA(cudaMemcpyAsync(d, &mine, sizeof(mine), cudaMemcpyHostToDevice, st));
+    char* recv = static_cast<char*>(d) + sizeof(PeerRecord);
+    all_gather(d, recv, sizeof(PeerRecord) / 2, DType::BF16, st);
+    VP_CUDA(cudaMemcpyAsync(all.data(), recv, sizeof(PeerRecord) * size_t(nranks), cudaMemcpyDeviceToHost, st));
+    VP_CUDA(cudaStreamSynchronize(st));
+    for (int k = 0; k < nranks && fail == 0.f; ++k) {
+      const PeerRecord& o = all[size_t(k)];
+      if (k == rank) {
+        out[size_t(k)] = local;
+      } else if (o.host != mine.host) {
+        fail = 1.f;
+      } else if (o.pid == mine.pid) {
+        if (o.device != dev) {
+          int can = 0;
+          if (cudaDeviceCanAccessPeer(&can, dev, o.device) != cudaSuccess || !can) {
+            fail = 1.f;
+            break;
+          }
+          const cudaError_t e = cudaDeviceEnablePeerAccess(o.device, 0);
+          if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) fail = 1.f;
+        }
+        out[size_t(k)] = reinterpret_cast<void*>(o.ptr);
+      } else if (!o.ipc_ok) {
+        fail = 1.f;
+      } else {
+        void* p = nullptr;
+        if (cudaIpcOpenMemHandle(&p, o.h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+          fail = 1.f;
+        } else {
+          opened.push_back(p);
+          out[size_t(k)] = p;
+        }
+      }
+    }
+    (void)cudaGetLastError();
+    // every rank learns whether all of them mapped all of their peers
+    VP_CUDA(cudaMemcpyAsync(d, &fail, sizeof(float), cudaMemcpyHostToDevice, st));
+    all_reduce(d, d, 1, DType::F32, RedOp::Max, st);
+    VP_CUDA(cudaMemcpyAsync(&fail, d, sizeof(float), cudaMemcpyDeviceToHost, st));
+    VP_CUDA(cudaStreamSynchronize(st));
+  } catch (...) {
+    for (void* p : opened) cudaIpcCloseMemHandle(p);
+    cudaFree(d);
+    throw;
+  }
+  cudaFree(d);
+  if (fail != 0.f) {
+    for (void* p : opened) cudaIpcCloseMemHandle(p);
+    (void)cudaGetLastError();
+    return {};
+  }
+  ipc_opened_.insert(ipc_opened_.end(), opened.begin(), opened.end());
+  return out;
+}
+
+void Comm::close_peers(const std::vector<void*>& peers) {
+  for (void* p : peers) {
+    auto it = std::find(ipc_opened_.begin(), ipc_opened_.end(), p);
+    if (it == ipc_opened_.end()) continue;
+    cudaIpcCloseMemHandle(p);
+    ipc_opened_.erase(it);
+  }
+  (void)cudaGetLastError();
+}
+
 double loopback_timeout_s() {
   const char* e = std::getenv("VPIPE_LOOPBACK_TIMEOUT");
   const double v = e ? std::atof(e) : 0.0;

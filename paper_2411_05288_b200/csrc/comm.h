@@ -22,6 +22,7 @@
 #include <cstddef>
 #include <cstdint>
 #include <memory>
+#include <vector>
 
 namespace vp {
 
@@ -46,7 +47,22 @@ class Comm {
   // ranks of this group on this rank's physical GPU (itself included): they
   // share its SMs, so the persistent GEMMs of each get a 1/colocated share
   virtual int colocated() const { return 1; }
+
+  // Peer memory for the fused exchanges (the dX GEMM that stores its tiles
+  // straight into the owning rank's buffer over NVLink).  Collective and
+  // host-blocking: every rank passes one device buffer it allocated with
+  // cudaMalloc (base pointer); returns every rank's buffer as addressable
+  // from this rank (own pointer, a peer-enabled pointer of a GPU this process
+  // drives, or a CUDA IPC mapping of another process's buffer).  Returns an
+  // empty vector on every rank when any rank cannot map some peer (other
+  // node, no P2P path): the caller then keeps the collective path.
+  std::vector<void*> open_peers(void* local, cudaStream_t st);
+  // Unmaps what open_peers mapped (IPC mappings; no-op for the rest).
+  void close_peers(const std::vector<void*>& peers);
   int nranks = 1, rank = 0;
+
+ private:
+  std::vector<void*> ipc_opened_;
 };
 
 // NCCL from a 128-byte ncclUniqueId; max_ctas bounds NCCL's SM use.

@@ -78,6 +78,10 @@ inline bool tma_store_ok(const void* p, int64_t ld, int esize) {
   return g_tma_store && (reinterpret_cast<uintptr_t>(p) & 15) == 0 && (ld * esize) % 16 == 0;
 }
 inline void prepare_store(EpiStoreF32::Params& ep, int M, int N) {
+  if (ep.route_n > 0) {  // routed: the caller built route_map[] (make_store_map per owner)
+    ep.use_tma = 1;
+    return;
+  }
   ep.use_tma = tma_store_ok(ep.out, ep.ldo, 4);
   if (ep.use_tma)
     ep.map = make_store_map(ep.out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, uint64_t(N), uint64_t(M), uint64_t(ep.ldo),
@@ -166,6 +170,9 @@ template <class Params>
 inline bool splittable(const Params&) { return false; }
 inline bool splittable(const EpiStoreF32::Params& p) { return p.tile_max == nullptr; }
 template <class Params>
+inline bool routed(const Params&) { return false; }
+inline bool routed(const EpiStoreF32::Params& p) { return p.route_n > 0; }
+template <class Params>
 inline bool uses_tma(const Params&) { return false; }
 inline bool uses_tma(const EpiStoreF32::Params& p) { return p.use_tma != 0; }
 template <class Params>
@@ -225,6 +232,7 @@ inline void launch_gemm_t(const Operand& A, const Operand& B, int M, int N, int 
   g.prof = g_gemm_prof;
   g.store_evict_first = store_hint >= 0 ? store_hint : g_store_evict_first;
   g.epi_wait = g_epi_wait;
+  g.sys_fence = routed(ep) ? 1 : 0;
   auto kern = gemm_sm100_kernel<CG, A_MN, B_MN, Epi, MC, NH>;
   // per device: the smem attribute and the occupancy query (contexts of one
   // process may drive several GPUs)
@@ -270,7 +278,7 @@ inline void launch_gemm_t(const Operand& A, const Operand& B, int M, int N, int 
   if (MC == 1 && split != nullptr && split->flags != nullptr && splittable(ep) && tiles <= split->max_tiles) {
     // workspace mode: less than half a wave of tiles, TMA-stored output, room
     const int64_t ldws = (int64_t(N) + 3) / 4 * 4;
-    const bool ws_ok = split->ws != nullptr && split->ws_mode != 0 && uses_tma(epc) &&
+    const bool ws_ok = split->ws != nullptr && split->ws_mode != 0 && uses_tma(epc) && !routed(epc) &&
                        (split->ws_mode == 2 || tiles * 2 <= cap);
     int S = split->force;
     if (S <= 0)

@@ -171,6 +171,19 @@ struct vp_ctx_s {
   // dW passes add into grad_w instead of overwriting it (gradient accumulation
   // across microbatches; tied input/output embeddings sharing one dE/dW buffer)
   bool accumulate_dw = false;
+  // fused C1 (alg2 in a group, option "fused_c1"): one peer-mapped buffer per
+  // rank — slots [nranks][R][h] fp32 (A_k of my token rows, written by rank
+  // k's dX epilogue) then B [R][h] bf16 (label rows) — and its mapping on
+  // every peer.  Grow-only; a grown buffer and its mappings stay alive until
+  // the context is destroyed (graphs keep the old pointers).
+  bool fused_c1 = true;
+  int64_t fused_count = 0;
+  void* sym = nullptr;
+  size_t sym_bytes = 0;
+  std::vector<void*> sym_peers;
+  std::vector<std::pair<void*, std::vector<void*>>> sym_retired;
+  bool sym_failed = false;    // some rank could not map its peers: the all-reduce path
+  DevBuf gfull;               // grad_x all-gather target when n_tok != nranks * R
   bool distributed() const { return comm != nullptr && (nranks > 1 || force_collectives); }
   // the NCCL / loopback group; callers check distributed() first
   vp::Comm& cm() const { return *comm; }
@@ -296,9 +309,13 @@ void gemm_logits_f32(vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* s, vp_s
 }
 
 // out[T x h] = diag(row_scale) . P[T x rows] . W_k[rows x h]
+void gemm_dx_ep(vp_ctx_s* c, vp_state_s* st, const vp_shard_t* s, const vp::EpiStoreF32::Params& ep);
 void gemm_dx(vp_ctx_s* c, vp_state_s* st, const vp_shard_t* s, float* out, int64_t ldo,
              const float* row_scale = nullptr) {
   vp::EpiStoreF32::Params ep{out, ldo, nullptr, 0, row_scale};
+  gemm_dx_ep(c, st, s, ep);
+}
+void gemm_dx_ep(vp_ctx_s* c, vp_state_s* st, const vp_shard_t* s, const vp::EpiStoreF32::Params& ep) {
   c->split.force = c->splits_dx;
   timed_gemm(c, 2, [&] {
     vp::launch_gemm<vp::EpiStoreF32>(c->cg, {st->P, st->ldp, false}, {s->W, s->ldw, true}, int(st->n_tok),
@@ -647,11 +664,203 @@ void join_allreduces(vp_ctx_s* c) {
   c->reduce_pending = false;
 }
 
+// Row ranges of every rank's shard (all-gathered once per layout, cached).
+const vp::RankBounds& rank_bounds(vp_ctx_s* c, const vp_shard_t* s) {
+  if (c->bounds_key_rb == s->row_begin && c->bounds_key_re == s->row_end && c->bounds.n == c->nranks)
+    return c->bounds;
+  require(c->nranks <= vp::kMaxRanks, "input_forward_gathered: too many ranks");
+  require(s->row_end < (int64_t(1) << 24), "input_forward_gathered: vocab size must be < 2^24");
+  float* d = c->buf<float>(c->vtmp, size_t(2 + 2 * c->nranks));
+  const float mine[2] = {float(s->row_begin), float(s->row_end)};
+  VP_CUDA(cudaMemcpyAsync(d, mine, sizeof(mine), cudaMemcpyHostToDevice, c->stream));
+  c->cm().all_gather(d, d + 2, 2, vp::DType::F32, c->stream);
+  std::vector<float> all(size_t(2 * c->nranks));
+  VP_CUDA(cudaMemcpyAsync(all.data(), d + 2, all.size() * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+  VP_CUDA(cudaStreamSynchronize(c->stream));
+  c->bounds.n = c->nranks;
+  for (int k = 0; k < c->nranks; ++k) {
+    c->bounds.rb[k] = int64_t(all[size_t(2 * k)]);
+    c->bounds.re[k] = int64_t(all[size_t(2 * k + 1)]);
+  }
+  c->bounds_key_rb = s->row_begin;
+  c->bounds_key_re = s->row_end;
+  return c->bounds;
+}
+
+// ---- fused C1 over peer memory (alg2 in a group; option "fused_c1") ---------
+// Rank o owns token rows [o R, min(T, (o + 1) R)), R a multiple of 32 so one
+// epilogue store box (32 rows) never straddles two owners.  See
+// k_alg2_combine_owned for the data flow.
+struct FusedLayout {
+  int64_t R = 0;
+  int n_own = 0;          // ranks that own at least one row
+  size_t slot_bytes = 0;  // [nranks][R][h] fp32
+  size_t need = 0;        // + B [R][h] bf16
+};
+
+FusedLayout fused_layout(const vp_ctx_s* c, int64_t T, int64_t h) {
+  FusedLayout L;
+  L.R = round_up(ceil_div(T, c->nranks), 32);
+  L.n_own = int(ceil_div(T, L.R));
+  L.slot_bytes = size_t(c->nranks) * size_t(L.R) * size_t(h) * sizeof(float);
+  L.need = L.slot_bytes + size_t(L.R) * size_t(h) * sizeof(__nv_bfloat16);
+  return L;
+}
+
+// Collective: every rank's peer buffer holds >= need bytes and is mapped on
+// every peer.  false (on every rank) when some rank cannot map its peers.
+bool ensure_sym(vp_ctx_s* c, size_t need) {
+  if (c->sym_failed) return false;
+  if (need <= c->sym_bytes) return true;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  VP_CUDA(cudaStreamIsCapturing(c->stream, &cs));
+  require(cs == cudaStreamCaptureStatusNone,
+          "fused_c1: the peer buffers must be sized outside graph capture (run the step once eagerly first)");
+  const size_t bytes = size_t(round_up(int64_t(need), int64_t(2) << 20));
+  void* p = nullptr;
+  VP_CUDA(cudaMalloc(&p, bytes));
+  std::vector<void*> peers;
+  try {
+    peers = c->cm().open_peers(p, c->stream);
+  } catch (...) {
+    cudaFree(p);
+    throw;
+  }
+  if (peers.empty()) {
+    cudaFree(p);
+    c->sym_failed = true;
+    return false;
+  }
+  if (c->sym) c->sym_retired.emplace_back(c->sym, c->sym_peers);
+  c->sym = p;
+  c->sym_bytes = bytes;
+  c->sym_peers = std::move(peers);
+  return true;
+}
+
+// The fused path is decided from the group-wide shape (every rank takes the
+// same branch); per-rank buffer requirements are checked, not negotiated.
+bool use_fused_c1(vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* s, int n, FusedLayout& L) {
+  if (!(c->fused_c1 && c->distributed() && c->nranks > 1 && n == 1 && c->nranks <= vp::kMaxRoute &&
+        b->h % 8 == 0 && !c->sym_failed))
+    return false;
+  require(s->ldw % 8 == 0 && aligned16(s->W),
+          "fused_c1: the shard needs ldw % 8 == 0 and a 16-byte aligned W (or set fused_c1 = 0 on every rank)");
+  L = fused_layout(c, b->n_tok, b->h);
+  return ensure_sym(c, L.need);
+}
+
+// alg2_pass_S with the dX epilogue routed to the token rows' owners and the
+// label rows B_k pushed after it.
+void alg2_S_fused(vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* s, vp_state_s* st, const FusedLayout& L) {
+  pass_S_common(c, b, s, st);
+  NvtxRange nr("vp:S:A=softmax'W->owners");
+  const int64_t T = b->n_tok, h = b->h;
+  vp::EpiStoreF32::Params ep{nullptr, h, nullptr, 0, st->cfac};
+  ep.route_n = L.n_own;
+  ep.route_rows = int(L.R);
+  vp::PeerRows pr{};
+  for (int o = 0; o < L.n_own; ++o) {
+    float* base = static_cast<float*>(c->sym_peers[size_t(o)]) + size_t(c->rank) * size_t(L.R) * size_t(h);
+    const int64_t rows = std::min(L.R, T - o * L.R);
+    ep.route_map[o] = vp::make_store_map(base, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, uint64_t(h), uint64_t(rows),
+                                         uint64_t(h), VP_F32_BOX128 ? 128 : 64);
+    pr.p[o] = static_cast<char*>(c->sym_peers[size_t(o)]) + L.slot_bytes;
+  }
+  gemm_dx_ep(c, st, s, ep);  // A_k = diag(cfac) P W_k (VM.cpp:183), tile by tile into the owners
+  vp::k_push_label_rows<<<c->grid_for(T * h / 8, 256), 256, 0, c->stream>>>(
+      static_cast<const __nv_bfloat16*>(s->W), s->ldw, s->row_begin, s->row_end, b->labels, int(T), int(h),
+      int(L.R), pr);  // B_k (VM.cpp:185-188) into the owners' B rows
+  VP_KCHECK();
+  ++c->launches;
+  st->has_grad_terms = false;  // A_k is in the owners' buffers, not in the state
+}
+
+// alg2_barrier_C1 (VM.cpp:193-211) for the fused layout: stats all-gather and
+// merge, the owner's combine of its rows from local memory, the loss at the
+// label owner, then (on the comm stream when overlapped with pass T) the
+// grad_x all-gather and the loss all-reduce.
+void alg2_C1_fused(vp_ctx_s* c, const vp_state_t st, const vp_shard_t* s, const vp_batch_t* b, double fault_scale,
+                   vp_stats_t out, float* loss, float* gx, int64_t ldgx, const FusedLayout& L, bool overlap) {
+  NvtxRange nr("vp:C1(fused)");
+  require(gx != nullptr && ldgx >= b->h && ldgx % 4 == 0 && aligned16(gx), "alg2_barrier_C1: bad grad_x buffer");
+  const int64_t T = b->n_tok, h = b->h, R = L.R;
+  merge_stats(c, &st, 1, fault_scale, out);
+  const vp::RankBounds& RB = rank_bounds(c, s);
+  vp::OwnedCombine S{};
+  S.slots = static_cast<const float*>(c->sym);
+  S.B = reinterpret_cast<const __nv_bfloat16*>(static_cast<const char*>(c->sym) + L.slot_bytes);
+  S.gathered = static_cast<const float*>(c->gathered.p);
+  for (int k = 0; k < c->nranks; ++k) {
+    S.rb[k] = RB.rb[k];
+    S.re[k] = RB.re[k];
+  }
+  S.nranks = c->nranks;
+  S.R = int(R);
+  S.row0 = int(c->rank * R);
+  S.rows = int(std::max<int64_t>(0, std::min(R, T - c->rank * R)));
+  const bool exact = R * c->nranks == T && ldgx == h;
+  float* full = exact ? gx : c->buf<float>(c->gfull, size_t(c->nranks * R * h));
+  float* mine = full + c->rank * R * h;
+  const int64_t V = global_vocab(c, s, 1);
+  if (S.rows > 0) {
+    vp::k_alg2_combine_owned<<<c->grid_for(int64_t(S.rows) * h / 4, 256), 256, 0, c->stream>>>(
+        S, out.m, out.sum, b->labels, int(T), int(h), mine, h, V, c->d_err, kErrLabel);
+    VP_KCHECK();
+    ++c->launches;
+  }
+  loss_of(c, &st, s, 1, out, b, loss, /*reduce=*/false);
+  NvtxRange nx("vp:C1:allgather(dX)+allreduce(loss)");
+  cudaStream_t xs = c->stream;
+  if (overlap) {
+    VP_CUDA(cudaEventRecord(c->ev_ready, c->stream));
+    VP_CUDA(cudaStreamWaitEvent(c->comm_stream, c->ev_ready, 0));
+    xs = c->comm_stream;
+  }
+  c->cm().group_start();
+  c->cm().all_gather(mine, full, size_t(R * h), vp::DType::F32, xs);
+  c->cm().all_reduce(loss, loss, size_t(T), vp::DType::F32, vp::RedOp::Sum, xs);
+  c->cm().group_end();
+  if (!exact)
+    VP_CUDA(cudaMemcpy2DAsync(gx, size_t(ldgx) * sizeof(float), full, size_t(h) * sizeof(float),
+                              size_t(h) * sizeof(float), size_t(T), cudaMemcpyDeviceToDevice, xs));
+  if (overlap) {
+    VP_CUDA(cudaEventRecord(c->ev_done, c->comm_stream));
+    c->reduce_pending = true;
+  }
+  ++c->fused_count;
+}
+
+void run_alg2_fused(vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* s, vp_state_t st, double fault_scale,
+                    vp_stats_t out, float* loss, float* gx, int64_t ldgx, float* gw, int64_t ldgw,
+                    const FusedLayout& L) {
+  alg2_S_fused(c, b, s, st, L);
+  const bool overlap = c->overlap_c1 && c->comm_stream != nullptr;
+  alg2_C1_fused(c, st, s, b, fault_scale, out, loss, gx, ldgx, L, overlap);
+  const int sms = c->gemm_sms;
+  if (overlap) c->gemm_sms = std::max(2, (c->gemm_sms - c->comm_sms) / 2 * 2);
+  try {
+    alg2_T(c, st, out, b, s, gw, ldgw);
+  } catch (...) {
+    c->gemm_sms = sms;
+    join_allreduces(c);
+    throw;
+  }
+  c->gemm_sms = sms;
+  join_allreduces(c);
+}
+
 void run_alg(int alg, vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* shards, const vp_state_t* states, int n,
              double fault_scale, vp_stats_t out, float* loss, float* gx, int64_t ldgx, float* const* gw,
              int64_t ldgw) {
   require(n >= 1 && n <= vp::kMaxLocalShards, "run: bad shard count");
   require(!c->distributed() || n == 1, "run: one shard per rank in an NCCL group");
+  FusedLayout L;
+  if (alg == 2 && use_fused_c1(c, b, shards, n, L)) {
+    check_batch(b);
+    run_alg2_fused(c, b, &shards[0], states[0], fault_scale, out, loss, gx, ldgx, gw[0], ldgw, L);
+    return;
+  }
   if (alg == 2) {
     for (int k = 0; k < n; ++k) alg2_S(c, b, &shards[k], states[k]);
     const bool overlap = c->distributed() && c->overlap_c1 && c->comm_stream != nullptr;
@@ -1018,6 +1227,13 @@ int vp_ctx_destroy(vp_ctx_t c) {
     if (!c) return;
     c->activate();
     cudaStreamSynchronize(c->stream);
+    if (c->comm) {
+      c->comm->close_peers(c->sym_peers);
+      for (auto& r : c->sym_retired) c->comm->close_peers(r.second);
+    }
+    if (c->sym) cudaFree(c->sym);
+    for (auto& r : c->sym_retired) cudaFree(r.first);
+    c->gfull.release();
     c->comm.reset();
     if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
     if (c->ev_ready) cudaEventDestroy(c->ev_ready);
@@ -1102,6 +1318,9 @@ int vp_ctx_set_option(vp_ctx_t c, const char* key, int64_t value) {
       c->nh[k == "nh_logits" ? 0 : k == "nh_dx" ? 1 : 2] = int(value);
     } else if (k == "accumulate_grad_w") {
       c->accumulate_dw = value != 0;
+    } else if (k == "fused_c1") {
+      require(value == 0 || value == 1, "vp_ctx_set_option: fused_c1 must be 0 or 1");
+      c->fused_c1 = value != 0;
     } else if (k == "overlap_c1") {
       c->overlap_c1 = value != 0;
     } else if (k == "comm_sms") {
@@ -1159,6 +1378,7 @@ int vp_ctx_set_option(vp_ctx_t c, const char* key, int64_t value) {
 }
 
 int64_t vp_ctx_launch_count(vp_ctx_t c) { return c ? c->launches : -1; }
+int64_t vp_ctx_fused_c1_count(vp_ctx_t c) { return c ? c->fused_count : -1; }
 
 int vp_ctx_set_logit_shift(vp_ctx_t c, const float* shift) {
   return api([&] {
@@ -1675,28 +1895,6 @@ int vp_input_backward(vp_ctx_t c, const void* grad, int64_t ldg, int grad_is_f32
   });
 }
 
-// Row ranges of every rank's shard (all-gathered once per layout, cached).
-const vp::RankBounds& rank_bounds(vp_ctx_s* c, const vp_shard_t* s) {
-  if (c->bounds_key_rb == s->row_begin && c->bounds_key_re == s->row_end && c->bounds.n == c->nranks)
-    return c->bounds;
-  require(c->nranks <= vp::kMaxRanks, "input_forward_gathered: too many ranks");
-  require(s->row_end < (int64_t(1) << 24), "input_forward_gathered: vocab size must be < 2^24");
-  float* d = c->buf<float>(c->vtmp, size_t(2 + 2 * c->nranks));
-  const float mine[2] = {float(s->row_begin), float(s->row_end)};
-  VP_CUDA(cudaMemcpyAsync(d, mine, sizeof(mine), cudaMemcpyHostToDevice, c->stream));
-  c->cm().all_gather(d, d + 2, 2, vp::DType::F32, c->stream);
-  std::vector<float> all(size_t(2 * c->nranks));
-  VP_CUDA(cudaMemcpyAsync(all.data(), d + 2, all.size() * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
-  VP_CUDA(cudaStreamSynchronize(c->stream));
-  c->bounds.n = c->nranks;
-  for (int k = 0; k < c->nranks; ++k) {
-    c->bounds.rb[k] = int64_t(all[size_t(2 * k)]);
-    c->bounds.re[k] = int64_t(all[size_t(2 * k + 1)]);
-  }
-  c->bounds_key_rb = s->row_begin;
-  c->bounds_key_re = s->row_end;
-  return c->bounds;
-}
 
 int vp_input_forward_gathered(vp_ctx_t c, const int64_t* tokens, int64_t n_tok, int64_t h, const vp_shard_t* s,
                               void* out, int64_t ldo) {

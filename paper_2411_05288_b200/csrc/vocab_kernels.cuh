@@ -300,6 +300,74 @@ __global__ void k_alg2_combine(CombineShards S, const float* __restrict__ mg, co
   }
 }
 
+// ---------------------------------------------------------------------------
+// Fused C1 over peer memory (alg2, nranks > 1).  Token rows are owned in
+// blocks of R rows: rank o owns rows [o R, min(T, (o + 1) R)).  In pass S the
+// dX GEMM of rank k stores its A_k tiles straight into slot k of the owner's
+// buffer (routed epilogue, over NVLink), and k_push_label_rows sends the
+// label rows B_k (W_k rows of the labels rank k owns) into the owner's B
+// buffer; every token row gets exactly one B row, from its label's owner.
+// At C1 the owner combines its rows from local memory only, in rank order:
+//   grad_x[i,:] = sum_k ( c_k[i] A_k[i,:] - [k owns g_i] B[i,:] )
+// — the expression and order of k_alg2_combine over p local shards, so the
+// group's grad_x has the same bits as a one-GPU p-shard run.
+// ---------------------------------------------------------------------------
+struct PeerRows {
+  void* p[kMaxLocalShards];  // owner o's B buffer [R x h] bf16, as mapped here
+};
+__global__ void k_push_label_rows(const __nv_bfloat16* __restrict__ W, int64_t ldw, int64_t rb, int64_t re,
+                                  const int64_t* __restrict__ labels, int n, int h, int R, PeerRows dst) {
+  const int hv = h / 8;  // 16-byte vectors
+  const int64_t total = int64_t(n) * hv;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < total; t += int64_t(gridDim.x) * blockDim.x) {
+    const int i = int(t / hv), c = int(t - int64_t(i) * hv) * 8;
+    const int64_t g = labels[i];
+    if (g < rb || g >= re) continue;
+    const int o = i / R;
+    const uint4 v = *reinterpret_cast<const uint4*>(W + (g - rb) * ldw + c);
+    *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(dst.p[o]) + int64_t(i - o * R) * h + c) = v;
+  }
+  __threadfence_system();  // peer stores performed before the kernel's completion is observed
+}
+
+struct OwnedCombine {
+  const float* slots;            // [nranks][R][h] fp32, slot k = A_k of my rows
+  const __nv_bfloat16* B;        // [R][h] bf16
+  const float* gathered;         // [nranks][2T]: rank k's local m at k*2T, sum at k*2T + T
+  int64_t rb[kMaxLocalShards], re[kMaxLocalShards];
+  int nranks, R, row0, rows;     // my rows: [row0, row0 + rows)
+};
+__global__ void k_alg2_combine_owned(OwnedCombine S, const float* __restrict__ mg, const float* __restrict__ sg,
+                                     const int64_t* __restrict__ labels, int T, int h, float* __restrict__ out,
+                                     int64_t ldo, int64_t V, int* __restrict__ err, int err_bit) {
+  const int hv = h / 4;
+  const int64_t total = int64_t(S.rows) * hv;
+  const int64_t slot = int64_t(S.R) * h;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < total; t += int64_t(gridDim.x) * blockDim.x) {
+    const int li = int(t / hv), c = int(t - int64_t(li) * hv) * 4;
+    const int i = S.row0 + li;
+    const int64_t g = labels[i];
+    if (c == 0 && (g < 0 || (V >= 0 && g >= V))) atomicOr(err, err_bit);  // VM.cpp:18
+    const float* a_row = S.slots + int64_t(li) * h + c;
+    const __nv_bfloat16* w = S.B + int64_t(li) * h + c;
+    const float2 w0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(w));
+    const float2 w1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(w + 2));
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int k = 0; k < S.nranks; ++k) {
+      const float ml = S.gathered[int64_t(k) * 2 * T + i], sl = S.gathered[int64_t(k) * 2 * T + T + i];
+      const float sc = sl * expf(ml - mg[i]) / sg[i];
+      const float4 a = *reinterpret_cast<const float4*>(a_row + k * slot);
+      float4 b = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (g >= S.rb[k] && g < S.re[k]) b = make_float4(w0.x, w0.y, w1.x, w1.y);
+      acc.x += a.x * sc - b.x;
+      acc.y += a.y * sc - b.y;
+      acc.z += a.z * sc - b.z;
+      acc.w += a.w * sc - b.w;
+    }
+    *reinterpret_cast<float4*>(out + int64_t(li) * ldo + c) = acc;
+  }
+}
+
 // Sum of p partials in k order (alg1/naive C2 on one device).
 struct PartialPtrs {
   const float* P[kMaxLocalShards];

@@ -74,6 +74,11 @@ class Context:
     def launches(self) -> int:
         return int(self.lib.vp_ctx_launch_count(self.handle))
 
+    @property
+    def fused_c1_count(self) -> int:
+        """Fused C1 exchanges run so far (dX GEMM -> owner over peer memory)."""
+        return int(self.lib.vp_ctx_fused_c1_count(self.handle))
+
     def gemm_timing(self, enable: bool):
         """Accumulated (ms, launches) per GEMM kind since the last call
         (logits, logits_f32, dx, dw), then switches event timing on/off."""

@@ -318,3 +318,130 @@ def test_loopback_group_cannot_be_captured():
 
     assert all(vpd.run_ranks(ctxs, rank))
     _close(ctxs)
+
+
+# ---------------------------------------------------------------------------
+# Fused C1 (option "fused_c1", the default in a group): pass S's dX GEMM
+# stores every A_k tile straight into the buffer of the rank owning those
+# token rows (peer memory; on one GPU the peers' buffers are plain device
+# pointers, across processes CUDA IPC mappings), the label rows follow, the
+# owner combines its rows in rank order and the group all-gathers grad_x.
+# The combine's expression and order are those of the one-GPU p-shard
+# combine, so the group's loss / grad_x / grad_w carry the one-GPU bits.
+# ---------------------------------------------------------------------------
+def _local_and_group(p, T, h, V, seed, opts=()):
+    X, W, g = oracle.random_instance(T, h, V, seed)
+    Xb, Wb, batch, Wd = device_case(X, W, g)
+    local_ctx = vm.Context(0)
+    for k, v in opts:
+        local_ctx.set_option(k, v)
+    local = vm.run_alg2(local_ctx, batch, vm.shard_weights(Wd, p))
+    local_ctx.sync()
+    torch.cuda.synchronize()
+    ctxs = vpd.local_group(p)
+    for c in ctxs:
+        for k, v in opts:
+            c.set_option(k, v)
+    outs = vpd.run_ranks(ctxs, lambda r, c: vm.run_alg2(c, batch, [_shard(Wd, p, r)]))
+    for c in ctxs:
+        c.sync()
+    return Xb, Wb, g, local, local_ctx, ctxs, outs
+
+
+@pytest.mark.parametrize("p,T", [(2, 256), (4, 256), (8, 512), (2, 96), (8, 96), (4, 1000)])
+def test_fused_c1_has_the_one_gpu_bits(p, T):
+    # T = p * R exactly (grad_x gathered in place) and ragged T (owners of
+    # 32-row multiples, some ranks owning nothing at T=96, p=8)
+    # (split-K pinned: ranks sharing one GPU get a share of its SMs, so the
+    # automatic split choice could differ from the one-context run's)
+    h, V = 128, 1024 * p
+    opts = (("splits_dx", 1), ("splits_dw", 1))
+    Xb, Wb, g, local, local_ctx, ctxs, outs = _local_and_group(p, T, h, V, 40 + p, opts)
+    assert [c.fused_c1_count for c in ctxs] == [1] * p
+    for o in outs:
+        assert torch.equal(o.loss, local.loss)
+        assert torch.equal(o.grad_x, local.grad_x)
+        assert torch.equal(o.stats.m, local.stats.m) and torch.equal(o.stats.sum, local.stats.sum)
+    assert torch.equal(torch.cat([o.grad_w[0] for o in outs]), local.grad_w_full())
+    ref = oracle.oracle_output_layer(Xb, g, Wb, want_softmax=False)
+    res = {"loss": outs[-1].loss.double().cpu().numpy(), "grad_x": outs[-1].grad_x[:, :h].double().cpu().numpy(),
+           "grad_w": torch.cat([o.grad_w[0] for o in outs])[:, :h].double().cpu().numpy()}
+    assert_parity(res, ref, f"fused C1 p={p} T={T}")
+    _close(ctxs)
+    local_ctx.close()
+
+
+def test_fused_c1_routed_ordered_split_k():
+    # the routed epilogue with ordered split-K units (split 1 reduce-adds into
+    # the owner's slot after split 0's stores landed, system-scope hand-off)
+    p, T, h, V = 4, 512, 256, 4 * 8192
+    opts = (("splits_dx", 3), ("split_workspace", 0), ("splits_dw", 1))
+    Xb, Wb, g, local, local_ctx, ctxs, outs = _local_and_group(p, T, h, V, 7, opts)
+    assert [c.fused_c1_count for c in ctxs] == [1] * p
+    for o in outs:
+        assert torch.equal(o.grad_x, local.grad_x) and torch.equal(o.loss, local.loss)
+    ref = oracle.oracle_output_layer(Xb, g, Wb, want_softmax=False)
+    res = {"loss": outs[0].loss.double().cpu().numpy(), "grad_x": outs[0].grad_x[:, :h].double().cpu().numpy(),
+           "grad_w": torch.cat([o.grad_w[0] for o in outs])[:, :h].double().cpu().numpy()}
+    assert_parity(res, ref, "fused C1 split-K 3")
+    _close(ctxs)
+    local_ctx.close()
+
+
+def test_fused_c1_off_keeps_the_all_reduce():
+    p, T, h, V = 4, 256, 128, 4096
+    X, W, g = oracle.random_instance(T, h, V, 5)
+    _, _, batch, Wd = device_case(X, W, g)
+    res = {}
+    for fused in (0, 1):
+        ctxs = vpd.local_group(p)
+        for c in ctxs:
+            c.set_option("fused_c1", fused)
+        outs = vpd.run_ranks(ctxs, lambda r, c: vm.run_alg2(c, batch, [_shard(Wd, p, r)]))
+        for c in ctxs:
+            c.sync()
+        assert [c.fused_c1_count for c in ctxs] == [fused] * p
+        res[fused] = outs[0]
+        _close(ctxs)
+    assert torch.allclose(res[0].grad_x, res[1].grad_x, rtol=1e-5, atol=1e-6)
+    assert torch.allclose(res[0].loss, res[1].loss, rtol=1e-6, atol=1e-6)
+
+
+def test_fused_c1_repeated_steps_and_growth():
+    # back-to-back steps reuse the peer buffers (write-after-read across
+    # steps is ordered by the grad_x all-gather); a larger batch grows them
+    p, h, V = 4, 128, 4096
+    ctxs = vpd.local_group(p)
+    for T in (128, 128, 640, 128):
+        X, W, g = oracle.random_instance(T, h, V, T)
+        Xb, Wb, batch, Wd = device_case(X, W, g)
+        ref = oracle.oracle_output_layer(Xb, g, Wb, want_softmax=False)
+        outs = vpd.run_ranks(ctxs, lambda r, c: vm.run_alg2(c, batch, [_shard(Wd, p, r)]))
+        for c in ctxs:
+            c.sync()
+        res = {"loss": outs[1].loss.double().cpu().numpy(), "grad_x": outs[1].grad_x[:, :h].double().cpu().numpy(),
+               "grad_w": torch.cat([o.grad_w[0] for o in outs])[:, :h].double().cpu().numpy()}
+        assert_parity(res, ref, f"fused C1 step T={T}")
+    assert [c.fused_c1_count for c in ctxs] == [4] * p
+    _close(ctxs)
+
+
+def test_fused_c1_across_processes(tmp_path):
+    # two processes on one GPU (torchrun): the peer buffers are CUDA IPC
+    # mappings, the path a one-process-per-GPU NCCL group takes
+    import socket
+    import subprocess
+    import sys
+    import json
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    here = os.path.dirname(os.path.abspath(__file__))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(here, "mp_fused_worker.py"),
+           str(tmp_path)]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    reps = [json.load(open(tmp_path / f"rank{k}.json")) for k in range(2)]
+    for rep in reps:
+        assert rep["ok"], rep
