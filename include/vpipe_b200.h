@@ -126,7 +126,8 @@ int vp_ctx_reserve(vp_ctx_t ctx, int64_t n_tok, int64_t h, int p);
  * "accumulate_grad_w" (1 = the T passes add dW_k into grad_w: gradient
  * accumulation, or tied input/output embeddings sharing the shard's buffer
  * with vp_input_backward(accumulate=1); R/PAPER.md:333),
- * "fused_c1" (vp_run_alg2 / vp_run_alg2_chunked in a group of nranks > 1:
+ * "fused_c1" (vp_run_alg2 / vp_run_alg2_chunked / vp_run_alg1 in a group of
+ * nranks > 1 (alg1: the dX of pass T, then C2):
  * 1 = the dX GEMM of pass S stores each A_k tile straight into the buffer of
  * the rank that owns those token rows, over peer memory (NVLink P2P or CUDA
  * IPC), the label rows follow, and at C1 each owner combines its rows from

@@ -184,6 +184,7 @@ struct vp_ctx_s {
   std::vector<std::pair<void*, std::vector<void*>>> sym_retired;
   bool sym_failed = false;    // some rank could not map its peers: the all-reduce path
   DevBuf gfull;               // grad_x all-gather target when n_tok != nranks * R
+  DevBuf bar;                 // one float: the alg1 C2 barrier
   bool distributed() const { return comm != nullptr && (nranks > 1 || force_collectives); }
   // the NCCL / loopback group; callers check distributed() first
   vp::Comm& cm() const { return *comm; }
@@ -752,11 +753,84 @@ bool use_fused_c1(vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* s, int n, 
 
 // alg2_pass_S with the dX epilogue routed to the token rows' owners and the
 // label rows B_k pushed after it.
+void gemm_dx_routed(vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* s, vp_state_s* st, const float* row_scale,
+                    const FusedLayout& L);
 void alg2_S_fused(vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* s, vp_state_s* st, const FusedLayout& L) {
   pass_S_common(c, b, s, st);
   NvtxRange nr("vp:S:A=softmax'W->owners");
+  gemm_dx_routed(c, b, s, st, st->cfac, L);  // A_k = diag(cfac) P W_k (VM.cpp:183), tile by tile into the owners
+  st->has_grad_terms = false;  // A_k is in the owners' buffers, not in the state
+}
+
+// The owner's combine of its token rows (from local memory) and the group's
+// grad_x all-gather (+ the loss all-reduce when `loss`), on the comm stream
+// when `overlap`.  alg2 C1: slots hold A_k, scaled here by c_k from the
+// gathered stats; alg1 C2 (`prescaled`): slots hold c_k A_k.
+void owner_combine_gather(vp_ctx_s* c, const vp_shard_t* s, const vp_batch_t* b, vp_stats_t g, bool prescaled,
+                          float* loss, float* gx, int64_t ldgx, const FusedLayout& L, bool overlap) {
+  const int64_t T = b->n_tok, h = b->h, R = L.R;
+  const vp::RankBounds& RB = rank_bounds(c, s);
+  vp::OwnedCombine S{};
+  S.slots = static_cast<const float*>(c->sym);
+  S.B = reinterpret_cast<const __nv_bfloat16*>(static_cast<const char*>(c->sym) + L.slot_bytes);
+  S.gathered = prescaled ? nullptr : static_cast<const float*>(c->gathered.p);
+  for (int k = 0; k < c->nranks; ++k) {
+    S.rb[k] = RB.rb[k];
+    S.re[k] = RB.re[k];
+  }
+  S.nranks = c->nranks;
+  S.R = int(R);
+  S.row0 = int(c->rank * R);
+  S.rows = int(std::max<int64_t>(0, std::min(R, T - c->rank * R)));
+  S.prescaled = prescaled ? 1 : 0;
+  const bool exact = R * c->nranks == T && ldgx == h;
+  float* full = exact ? gx : c->buf<float>(c->gfull, size_t(c->nranks * R * h));
+  float* mine = full + c->rank * R * h;
+  const int64_t V = global_vocab(c, s, 1);
+  if (S.rows > 0) {
+    vp::k_alg2_combine_owned<<<c->grid_for(int64_t(S.rows) * h / 4, 256), 256, 0, c->stream>>>(
+        S, g.m, g.sum, b->labels, int(T), int(h), mine, h, V, c->d_err, kErrLabel);
+    VP_KCHECK();
+    ++c->launches;
+  }
+  NvtxRange nx("vp:allgather(dX)");
+  cudaStream_t xs = c->stream;
+  if (overlap) {
+    VP_CUDA(cudaEventRecord(c->ev_ready, c->stream));
+    VP_CUDA(cudaStreamWaitEvent(c->comm_stream, c->ev_ready, 0));
+    xs = c->comm_stream;
+  }
+  c->cm().group_start();
+  c->cm().all_gather(mine, full, size_t(R * h), vp::DType::F32, xs);
+  if (loss) c->cm().all_reduce(loss, loss, size_t(T), vp::DType::F32, vp::RedOp::Sum, xs);
+  c->cm().group_end();
+  if (!exact)
+    VP_CUDA(cudaMemcpy2DAsync(gx, size_t(ldgx) * sizeof(float), full, size_t(h) * sizeof(float),
+                              size_t(h) * sizeof(float), size_t(T), cudaMemcpyDeviceToDevice, xs));
+  if (overlap) {
+    VP_CUDA(cudaEventRecord(c->ev_done, c->comm_stream));
+    c->reduce_pending = true;
+  }
+  ++c->fused_count;
+}
+
+// alg2_barrier_C1 (VM.cpp:193-211) for the fused layout: stats all-gather and
+// merge, the loss at the label owner, then the owners' combine + gather.
+void alg2_C1_fused(vp_ctx_s* c, const vp_state_t st, const vp_shard_t* s, const vp_batch_t* b, double fault_scale,
+                   vp_stats_t out, float* loss, float* gx, int64_t ldgx, const FusedLayout& L, bool overlap) {
+  NvtxRange nr("vp:C1(fused)");
+  require(gx != nullptr && ldgx >= b->h && ldgx % 4 == 0 && aligned16(gx), "alg2_barrier_C1: bad grad_x buffer");
+  merge_stats(c, &st, 1, fault_scale, out);
+  loss_of(c, &st, s, 1, out, b, loss, /*reduce=*/false);
+  owner_combine_gather(c, s, b, out, false, loss, gx, ldgx, L, overlap);
+}
+
+// Routed dX of a T pass / pass S: out rows go to their owners' slot `rank`,
+// then the label rows B_k (VM.cpp:185-188, :176) into the owners' B rows.
+void gemm_dx_routed(vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* s, vp_state_s* st, const float* row_scale,
+                    const FusedLayout& L) {
   const int64_t T = b->n_tok, h = b->h;
-  vp::EpiStoreF32::Params ep{nullptr, h, nullptr, 0, st->cfac};
+  vp::EpiStoreF32::Params ep{nullptr, h, nullptr, 0, row_scale};
   ep.route_n = L.n_own;
   ep.route_rows = int(L.R);
   vp::PeerRows pr{};
@@ -767,68 +841,37 @@ void alg2_S_fused(vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* s, vp_stat
                                          uint64_t(h), VP_F32_BOX128 ? 128 : 64);
     pr.p[o] = static_cast<char*>(c->sym_peers[size_t(o)]) + L.slot_bytes;
   }
-  gemm_dx_ep(c, st, s, ep);  // A_k = diag(cfac) P W_k (VM.cpp:183), tile by tile into the owners
+  gemm_dx_ep(c, st, s, ep);
   vp::k_push_label_rows<<<c->grid_for(T * h / 8, 256), 256, 0, c->stream>>>(
       static_cast<const __nv_bfloat16*>(s->W), s->ldw, s->row_begin, s->row_end, b->labels, int(T), int(h),
-      int(L.R), pr);  // B_k (VM.cpp:185-188) into the owners' B rows
+      int(L.R), pr);
   VP_KCHECK();
   ++c->launches;
-  st->has_grad_terms = false;  // A_k is in the owners' buffers, not in the state
 }
 
-// alg2_barrier_C1 (VM.cpp:193-211) for the fused layout: stats all-gather and
-// merge, the owner's combine of its rows from local memory, the loss at the
-// label owner, then (on the comm stream when overlapped with pass T) the
-// grad_x all-gather and the loss all-reduce.
-void alg2_C1_fused(vp_ctx_s* c, const vp_state_t st, const vp_shard_t* s, const vp_batch_t* b, double fault_scale,
-                   vp_stats_t out, float* loss, float* gx, int64_t ldgx, const FusedLayout& L, bool overlap) {
-  NvtxRange nr("vp:C1(fused)");
-  require(gx != nullptr && ldgx >= b->h && ldgx % 4 == 0 && aligned16(gx), "alg2_barrier_C1: bad grad_x buffer");
-  const int64_t T = b->n_tok, h = b->h, R = L.R;
+// alg1 with the fused C2: pass T's dX (c (.) softmax' W_k, VM.cpp:176) goes
+// to the owners; after T a barrier, the owners' combine, the gather.
+void run_alg1_fused(vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* s, vp_state_t st, double fault_scale,
+                    vp_stats_t out, float* loss, float* gx, int64_t ldgx, float* gw, int64_t ldgw,
+                    const FusedLayout& L) {
+  pass_S_common(c, b, s, st);
   merge_stats(c, &st, 1, fault_scale, out);
-  const vp::RankBounds& RB = rank_bounds(c, s);
-  vp::OwnedCombine S{};
-  S.slots = static_cast<const float*>(c->sym);
-  S.B = reinterpret_cast<const __nv_bfloat16*>(static_cast<const char*>(c->sym) + L.slot_bytes);
-  S.gathered = static_cast<const float*>(c->gathered.p);
-  for (int k = 0; k < c->nranks; ++k) {
-    S.rb[k] = RB.rb[k];
-    S.re[k] = RB.re[k];
+  loss_of(c, &st, s, 1, out, b, loss);
+  {
+    NvtxRange nr("vp:T(alg1, dX->owners)");
+    require(gx != nullptr && ldgx >= b->h && ldgx % 4 == 0 && aligned16(gx), "run_alg1: bad grad_x buffer");
+    check_grad_w(gw, ldgw, b->h, "alg1_pass_T: grad_w needs ldgw >= h, ldgw % 4 == 0 and a 16-byte aligned base");
+    const float* sc = global_scale(c, st, out);
+    gemm_dx_routed(c, b, s, st, sc, L);
+    gemm_dw(c, st, scaled_x(c, b, sc), b->h, gw, ldgw);
+    segment_scatter(c, b->labels, b->n_tok, s->row_begin, s->row_end, static_cast<const __nv_bfloat16*>(b->X),
+                    b->ldx, b->h, -1.f, gw, ldgw, 1, kErrLabel);
   }
-  S.nranks = c->nranks;
-  S.R = int(R);
-  S.row0 = int(c->rank * R);
-  S.rows = int(std::max<int64_t>(0, std::min(R, T - c->rank * R)));
-  const bool exact = R * c->nranks == T && ldgx == h;
-  float* full = exact ? gx : c->buf<float>(c->gfull, size_t(c->nranks * R * h));
-  float* mine = full + c->rank * R * h;
-  const int64_t V = global_vocab(c, s, 1);
-  if (S.rows > 0) {
-    vp::k_alg2_combine_owned<<<c->grid_for(int64_t(S.rows) * h / 4, 256), 256, 0, c->stream>>>(
-        S, out.m, out.sum, b->labels, int(T), int(h), mine, h, V, c->d_err, kErrLabel);
-    VP_KCHECK();
-    ++c->launches;
-  }
-  loss_of(c, &st, s, 1, out, b, loss, /*reduce=*/false);
-  NvtxRange nx("vp:C1:allgather(dX)+allreduce(loss)");
-  cudaStream_t xs = c->stream;
-  if (overlap) {
-    VP_CUDA(cudaEventRecord(c->ev_ready, c->stream));
-    VP_CUDA(cudaStreamWaitEvent(c->comm_stream, c->ev_ready, 0));
-    xs = c->comm_stream;
-  }
-  c->cm().group_start();
-  c->cm().all_gather(mine, full, size_t(R * h), vp::DType::F32, xs);
-  c->cm().all_reduce(loss, loss, size_t(T), vp::DType::F32, vp::RedOp::Sum, xs);
-  c->cm().group_end();
-  if (!exact)
-    VP_CUDA(cudaMemcpy2DAsync(gx, size_t(ldgx) * sizeof(float), full, size_t(h) * sizeof(float),
-                              size_t(h) * sizeof(float), size_t(T), cudaMemcpyDeviceToDevice, xs));
-  if (overlap) {
-    VP_CUDA(cudaEventRecord(c->ev_done, c->comm_stream));
-    c->reduce_pending = true;
-  }
-  ++c->fused_count;
+  NvtxRange nr("vp:C2(fused)");
+  // every rank's routed stores are complete (stream order + the collective)
+  float* bar = c->buf<float>(c->bar, 1);
+  c->cm().all_reduce(bar, bar, 1, vp::DType::F32, vp::RedOp::Max, c->stream);
+  owner_combine_gather(c, s, b, out, true, nullptr, gx, ldgx, L, false);
 }
 
 void run_alg2_fused(vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* s, vp_state_t st, double fault_scale,
@@ -856,9 +899,10 @@ void run_alg(int alg, vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* shards
   require(n >= 1 && n <= vp::kMaxLocalShards, "run: bad shard count");
   require(!c->distributed() || n == 1, "run: one shard per rank in an NCCL group");
   FusedLayout L;
-  if (alg == 2 && use_fused_c1(c, b, shards, n, L)) {
+  if (alg != 0 && use_fused_c1(c, b, shards, n, L)) {
     check_batch(b);
-    run_alg2_fused(c, b, &shards[0], states[0], fault_scale, out, loss, gx, ldgx, gw[0], ldgw, L);
+    if (alg == 2) run_alg2_fused(c, b, &shards[0], states[0], fault_scale, out, loss, gx, ldgx, gw[0], ldgw, L);
+    else run_alg1_fused(c, b, &shards[0], states[0], fault_scale, out, loss, gx, ldgx, gw[0], ldgw, L);
     return;
   }
   if (alg == 2) {
@@ -1234,6 +1278,7 @@ int vp_ctx_destroy(vp_ctx_t c) {
     if (c->sym) cudaFree(c->sym);
     for (auto& r : c->sym_retired) cudaFree(r.first);
     c->gfull.release();
+    c->bar.release();
     c->comm.reset();
     if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
     if (c->ev_ready) cudaEventDestroy(c->ev_ready);

@@ -336,6 +336,7 @@ struct OwnedCombine {
   const float* gathered;         // [nranks][2T]: rank k's local m at k*2T, sum at k*2T + T
   int64_t rb[kMaxLocalShards], re[kMaxLocalShards];
   int nranks, R, row0, rows;     // my rows: [row0, row0 + rows)
+  int prescaled;                 // alg1 C2: the slots already hold c_k A_k (c_k = 1 here)
 };
 __global__ void k_alg2_combine_owned(OwnedCombine S, const float* __restrict__ mg, const float* __restrict__ sg,
                                      const int64_t* __restrict__ labels, int T, int h, float* __restrict__ out,
@@ -354,11 +355,20 @@ __global__ void k_alg2_combine_owned(OwnedCombine S, const float* __restrict__ m
     const float2 w1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(w + 2));
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int k = 0; k < S.nranks; ++k) {
-      const float ml = S.gathered[int64_t(k) * 2 * T + i], sl = S.gathered[int64_t(k) * 2 * T + T + i];
-      const float sc = sl * expf(ml - mg[i]) / sg[i];
       const float4 a = *reinterpret_cast<const float4*>(a_row + k * slot);
       float4 b = make_float4(0.f, 0.f, 0.f, 0.f);
       if (g >= S.rb[k] && g < S.re[k]) b = make_float4(w0.x, w0.y, w1.x, w1.y);
+      if (S.prescaled) {
+        // alg1 / C2: partial_k = c_k A_k - G_k W_k, summed in k order (the
+        // one-GPU path's k_sub_label_rows + k_sum_partials)
+        acc.x += a.x - b.x;
+        acc.y += a.y - b.y;
+        acc.z += a.z - b.z;
+        acc.w += a.w - b.w;
+        continue;
+      }
+      const float ml = S.gathered[int64_t(k) * 2 * T + i], sl = S.gathered[int64_t(k) * 2 * T + T + i];
+      const float sc = sl * expf(ml - mg[i]) / sg[i];
       acc.x += a.x * sc - b.x;
       acc.y += a.y * sc - b.y;
       acc.z += a.z * sc - b.z;

@@ -329,34 +329,36 @@ def test_loopback_group_cannot_be_captured():
 # The combine's expression and order are those of the one-GPU p-shard
 # combine, so the group's loss / grad_x / grad_w carry the one-GPU bits.
 # ---------------------------------------------------------------------------
-def _local_and_group(p, T, h, V, seed, opts=()):
+def _local_and_group(p, T, h, V, seed, opts=(), alg="alg2"):
+    fn = {"alg1": vm.run_alg1, "alg2": vm.run_alg2}[alg]
     X, W, g = oracle.random_instance(T, h, V, seed)
     Xb, Wb, batch, Wd = device_case(X, W, g)
     local_ctx = vm.Context(0)
     for k, v in opts:
         local_ctx.set_option(k, v)
-    local = vm.run_alg2(local_ctx, batch, vm.shard_weights(Wd, p))
+    local = fn(local_ctx, batch, vm.shard_weights(Wd, p))
     local_ctx.sync()
     torch.cuda.synchronize()
     ctxs = vpd.local_group(p)
     for c in ctxs:
         for k, v in opts:
             c.set_option(k, v)
-    outs = vpd.run_ranks(ctxs, lambda r, c: vm.run_alg2(c, batch, [_shard(Wd, p, r)]))
+    outs = vpd.run_ranks(ctxs, lambda r, c: fn(c, batch, [_shard(Wd, p, r)]))
     for c in ctxs:
         c.sync()
     return Xb, Wb, g, local, local_ctx, ctxs, outs
 
 
+@pytest.mark.parametrize("alg", ["alg2", "alg1"])
 @pytest.mark.parametrize("p,T", [(2, 256), (4, 256), (8, 512), (2, 96), (8, 96), (4, 1000)])
-def test_fused_c1_has_the_one_gpu_bits(p, T):
+def test_fused_c1_has_the_one_gpu_bits(p, T, alg):
     # T = p * R exactly (grad_x gathered in place) and ragged T (owners of
     # 32-row multiples, some ranks owning nothing at T=96, p=8)
     # (split-K pinned: ranks sharing one GPU get a share of its SMs, so the
     # automatic split choice could differ from the one-context run's)
     h, V = 128, 1024 * p
     opts = (("splits_dx", 1), ("splits_dw", 1))
-    Xb, Wb, g, local, local_ctx, ctxs, outs = _local_and_group(p, T, h, V, 40 + p, opts)
+    Xb, Wb, g, local, local_ctx, ctxs, outs = _local_and_group(p, T, h, V, 40 + p, opts, alg)
     assert [c.fused_c1_count for c in ctxs] == [1] * p
     for o in outs:
         assert torch.equal(o.loss, local.loss)
@@ -366,7 +368,7 @@ def test_fused_c1_has_the_one_gpu_bits(p, T):
     ref = oracle.oracle_output_layer(Xb, g, Wb, want_softmax=False)
     res = {"loss": outs[-1].loss.double().cpu().numpy(), "grad_x": outs[-1].grad_x[:, :h].double().cpu().numpy(),
            "grad_w": torch.cat([o.grad_w[0] for o in outs])[:, :h].double().cpu().numpy()}
-    assert_parity(res, ref, f"fused C1 p={p} T={T}")
+    assert_parity(res, ref, f"fused C1 p={p} T={T} {alg}")
     _close(ctxs)
     local_ctx.close()
 
