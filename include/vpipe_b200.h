@@ -126,6 +126,12 @@ int vp_ctx_reserve(vp_ctx_t ctx, int64_t n_tok, int64_t h, int p);
  * "accumulate_grad_w" (1 = the T passes add dW_k into grad_w: gradient
  * accumulation, or tied input/output embeddings sharing the shard's buffer
  * with vp_input_backward(accumulate=1); R/PAPER.md:333),
+ * "persist_logits" / "persist_dw" (1 = the logits / dW GEMM launch carries a
+ * persisting L2 access-policy window over its X operand, with the device's
+ * persisting L2 set-aside sized on first use: with raster_logits=32, or with
+ * raster_dw=-8 policy_dw=0 policyb_dw=2, DRAM bytes per launch fall to about
+ * the algorithmic bytes, but in-step throughput measured 0.5-1.5% lower
+ * (profiles/r02y_*, r02z_*); default 0),
  * "fused_c1" (vp_run_alg2 / vp_run_alg2_chunked / vp_run_alg1 in a group of
  * nranks > 1 (alg1: the dX of pass T, then C2):
  * 1 = the dX GEMM of pass S stores each A_k tile straight into the buffer of

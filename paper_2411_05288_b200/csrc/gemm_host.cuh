@@ -110,6 +110,15 @@ struct SplitCfg {
   int64_t reduce_launches = 0;  // k_split_reduce launches so far (evidence counters)
 };
 
+// Optional L2 access-policy window of one launch (cudaLaunchAttributeAccessPolicyWindow):
+// accesses to [ptr, ptr + bytes) are marked persisting (hit_ratio of them),
+// the rest streaming.  Needs a persisting L2 set-aside (cudaLimitPersistingL2CacheSize).
+struct L2Window {
+  const void* ptr = nullptr;
+  size_t bytes = 0;
+  float hit_ratio = 1.f;
+};
+
 // Wave-lockstep state owned by the caller (per stream, like SplitCfg):
 // counters for up to `capacity` (wave, epoch) pairs, reset by each launch.
 struct LockCfg {
@@ -211,7 +220,7 @@ template <int CG, bool A_MN, bool B_MN, class Epi, int MC = 1, int NH = 1>
 inline void launch_gemm_t(const Operand& A, const Operand& B, int M, int N, int K, int raster,
                           const typename Epi::Params& ep, int num_sms, cudaStream_t st, int pol_a = -1,
                           int pol_b = -1, SplitCfg* split = nullptr, const LockCfg* lock = nullptr,
-                          int store_hint = -1) {
+                          int store_hint = -1, const L2Window* win = nullptr) {
   using C = GemmCfg<CG, NH>;
   const CUtensorMap ta = A_MN ? make_tmap_bf16(A.ptr, uint64_t(M), uint64_t(K), uint64_t(A.ld), 64, 64)
                               : make_tmap_bf16(A.ptr, uint64_t(K), uint64_t(M), uint64_t(A.ld), 64, C::BM_CTA);
@@ -306,7 +315,7 @@ inline void launch_gemm_t(const Operand& A, const Operand& B, int M, int N, int 
   cfg.blockDim = dim3(C::THREADS, 1, 1);
   cfg.dynamicSmemBytes = C::SMEM_BYTES;
   cfg.stream = st;
-  cudaLaunchAttribute at[2];
+  cudaLaunchAttribute at[3];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = CL;
   at[0].val.clusterDim.y = 1;
@@ -319,6 +328,15 @@ inline void launch_gemm_t(const Operand& A, const Operand& B, int M, int N, int 
   at[1].val.cooperative = g_cooperative;
   cfg.attrs = at;
   cfg.numAttrs = 2;
+  if (win != nullptr && win->ptr != nullptr && win->bytes > 0) {
+    at[2].id = cudaLaunchAttributeAccessPolicyWindow;
+    at[2].val.accessPolicyWindow.base_ptr = const_cast<void*>(win->ptr);
+    at[2].val.accessPolicyWindow.num_bytes = win->bytes;
+    at[2].val.accessPolicyWindow.hitRatio = win->hit_ratio;
+    at[2].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    at[2].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    cfg.numAttrs = 3;
+  }
   if (lock != nullptr && lock->counters != nullptr && lock->epoch > 0) {
     const int units = tiles * g.splits;
     const int waves = (units + clusters - 1) / clusters;
@@ -345,11 +363,11 @@ template <class Epi>
 inline void launch_gemm(int cg, const Operand& A, const Operand& B, int M, int N, int K, int raster,
                         const typename Epi::Params& ep, int num_sms, cudaStream_t st, int pol_a = -1,
                         int pol_b = -1, int mc = 1, int nh = 1, SplitCfg* split = nullptr,
-                        const LockCfg* lock = nullptr, int store_hint = -1) {
+                        const LockCfg* lock = nullptr, int store_hint = -1, const L2Window* win = nullptr) {
 #define VP_GEMM_CASE(CGV, AM, BM_, MCV, NHV)                                                                        \
   if (cg == CGV && A.mn_major == AM && B.mn_major == BM_ && mc == MCV && nh == NHV) {                               \
     launch_gemm_t<CGV, AM, BM_, Epi, MCV, NHV>(A, B, M, N, K, raster, ep, num_sms, st, pol_a, pol_b, split, lock,    \
-                                               store_hint);                                                        \
+                                               store_hint, win);                                                   \
     return;                                                                                                         \
   }
   VP_GEMM_CASE(2, false, false, 1, 1)

@@ -118,6 +118,24 @@ struct vp_ctx_s {
   int store_hint[3] = {1, -1, -1};  // epilogue store L2 hint per GEMM: 1 evict-first, 0 normal, -1 process-wide option
   int pb(int i) const { return polb[i] == -9 ? pol[i] : polb[i]; }
   int mc = 1;  // CTA pairs per cluster sharing B by TMA multicast (1 or 2)
+  // Persisting L2 window per GEMM [logits, dX, dW] on the operand re-read
+  // across waves (logits: X, dW: c (.) X); needs the device's persisting L2
+  // set-aside (sized on first use, up to persist_max bytes)
+  int persist[3] = {0, 0, 0};
+  size_t persist_max = 0, persist_set = 0;
+  vp::L2Window persist_win(int i, const void* p, size_t bytes) {
+    vp::L2Window w;
+    if (!persist[i] || persist_max == 0) return w;
+    const size_t want = std::min(bytes, persist_max);
+    if (want > persist_set) {
+      VP_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want));
+      persist_set = want;
+    }
+    w.ptr = p;
+    w.bytes = bytes;
+    w.hit_ratio = std::min(1.f, float(double(persist_set) / double(bytes)));
+    return w;
+  }
   int nh[3] = {2, 2, 2};  // N halves per tile (2 = 256 x 512 pair tiles) for [logits, dX, dW]
   // split-K of the dX GEMM (K = V_k, few waves): ordered, deterministic;
   // splits_dx option: 0 = by wave quantisation (ordered splits) or, below half
@@ -290,11 +308,12 @@ void gemm_logits(vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* s, vp_state
                                st->counters + 1, st->fix_list};
   ep.logit_shift = c->logit_shift;
   ep.logit_scale = c->logit_scale;
+  const vp::L2Window win = c->persist_win(0, b->X, size_t((b->n_tok - 1) * b->ldx + b->h) * 2);
   timed_gemm(c, 0, [&] {
     vp::launch_gemm<vp::EpiLogitStats>(c->cg, {b->X, b->ldx, false}, {s->W, s->ldw, false}, int(b->n_tok),
                                        int(st->rows), int(b->h), c->raster[0], ep, c->gemm_sms, c->stream,
                                        c->pol[0], c->pb(0), c->eff_mc(0), c->eff_nh(0), nullptr, c->lock_for(0),
-                                       c->store_hint[0]);
+                                       c->store_hint[0], &win);
   });
   ++c->launches;
 }
@@ -332,12 +351,13 @@ void gemm_dx_ep(vp_ctx_s* c, vp_state_s* st, const vp_shard_t* s, const vp::EpiS
 void gemm_dw(vp_ctx_s* c, vp_state_s* st, const void* Xop, int64_t ldx, float* out, int64_t ldo) {
   vp::EpiStoreF32::Params ep{out, ldo, nullptr, 0, nullptr, c->accumulate_dw ? 1 : 0};
   const int raster = c->raster[2];
+  const vp::L2Window win = c->persist_win(2, Xop, size_t((st->n_tok - 1) * ldx + st->h) * 2);
   c->split.force = c->splits_dw;  // (few-wave shards, e.g. V/8 rows: 13.5 waves -> 3 splits)
   timed_gemm(c, 3, [&] {
     vp::launch_gemm<vp::EpiStoreF32>(c->cg, {st->P, st->ldp, true}, {Xop, ldx, true}, int(st->rows), int(st->h),
                                      int(st->n_tok), raster, ep, c->gemm_sms, c->stream, c->pol[2], c->pb(2),
                                      c->eff_mc(2), c->eff_nh(2), c->splits_dw == 1 ? nullptr : &c->split,
-                                     c->lock_for(2), c->store_hint[2]);
+                                     c->lock_for(2), c->store_hint[2], &win);
   });
   c->launches += 1 + c->split.reduce_launches;
   c->split.reduce_launches = 0;
@@ -1237,6 +1257,7 @@ int vp_ctx_create(int device, vp_ctx_t* out) {
       if (prop.major != 10) throw std::invalid_argument("vp_ctx_create: this library targets sm_100a (B200)");
       c->num_sms = prop.multiProcessorCount;
       c->gemm_sms = c->num_sms;
+      c->persist_max = std::min<size_t>(size_t(prop.persistingL2CacheMaxSize), size_t(prop.accessPolicyMaxWindowSize));
       VP_CUDA(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
       c->stream = c->own_stream;
       VP_CUDA(cudaMalloc(&c->d_err, sizeof(int)));
@@ -1363,6 +1384,9 @@ int vp_ctx_set_option(vp_ctx_t c, const char* key, int64_t value) {
       c->nh[k == "nh_logits" ? 0 : k == "nh_dx" ? 1 : 2] = int(value);
     } else if (k == "accumulate_grad_w") {
       c->accumulate_dw = value != 0;
+    } else if (k == "persist_logits" || k == "persist_dw") {
+      require(value == 0 || value == 1, "vp_ctx_set_option: persist_* must be 0 or 1");
+      c->persist[k == "persist_logits" ? 0 : 2] = int(value);
     } else if (k == "fused_c1") {
       require(value == 0 || value == 1, "vp_ctx_set_option: fused_c1 must be 0 or 1");
       c->fused_c1 = value != 0;

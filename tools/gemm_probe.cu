@@ -4,6 +4,7 @@
 // pol: -1 default, 0 normal, 1 evict_first, 2 evict_last.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <string>
@@ -97,6 +98,27 @@ int main(int argc, char** argv) {
   lcfg.epoch = getenv("VP_LOCKSTEP") ? atoi(getenv("VP_LOCKSTEP")) : 0;
   lcfg.capacity = int64_t(1) << 20;
   CK(cudaMalloc(&lcfg.counters, size_t(lcfg.capacity) * sizeof(int)));
+  // VP_PERSIST=<MB>: persisting L2 window over the operand that is re-read
+  // across waves (K1: X; dW: the X operand) with a set-aside of that size
+  vp::L2Window win;
+  const vp::L2Window* winp = nullptr;
+  {
+    cudaDeviceProp pr;
+    CK(cudaGetDeviceProperties(&pr, 0));
+    printf("  L2 %d MB, persisting max %d MB, access-policy window max %d MB\n", pr.l2CacheSize >> 20,
+           pr.persistingL2CacheMaxSize >> 20, pr.accessPolicyMaxWindowSize >> 20);
+    const int pmb = getenv("VP_PERSIST") ? atoi(getenv("VP_PERSIST")) : 0;
+    if (pmb > 0 && (kind == "k1" || kind == "dw")) {
+      const size_t lim = std::min<size_t>(size_t(pmb) << 20, size_t(pr.persistingL2CacheMaxSize));
+      CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, lim));
+      win.ptr = X;
+      win.bytes = std::min<size_t>(size_t(T * h * 2), size_t(pr.accessPolicyMaxWindowSize));
+      win.hit_ratio = std::min(1.f, float(double(lim) / double(win.bytes)));
+      winp = &win;
+      printf("  persisting window %.1f MB, set-aside %.1f MB, hit ratio %.2f\n", win.bytes / 1e6, lim / 1e6,
+             win.hit_ratio);
+    }
+  }
   auto run = [&] {
     if (kind == "k1") {
       vp::EpiLogitStats::Params ep{P,   V,   tm,  ts,  T,   nullptr, 0,   V,   yt,  tq,
@@ -105,7 +127,7 @@ int main(int argc, char** argv) {
       CK(cudaMemsetAsync(bad, 0, T * 4));
       CK(cudaMemsetAsync(cnt, 0, 8));
       vp::launch_gemm<vp::EpiLogitStats>(2, {X, h, false}, {W, h, false}, int(T), int(V), int(h), raster, ep, nsm, 0,
-                                         pa, pb, mc, nh, nullptr, &lcfg);
+                                         pa, pb, mc, nh, nullptr, &lcfg, -1, winp);
     } else if (kind == "dx") {
       vp::EpiStoreF32::Params ep{out, h, nullptr, 0, nullptr};
       vp::launch_gemm<vp::EpiStoreF32>(2, {P, V, false}, {W, h, true}, int(T), int(h), int(V), raster, ep, nsm, 0, pa,
@@ -113,7 +135,7 @@ int main(int argc, char** argv) {
     } else if (kind == "dw") {
       vp::EpiStoreF32::Params ep{out, h, nullptr, 0, nullptr};
       vp::launch_gemm<vp::EpiStoreF32>(2, {P, V, true}, {X, h, true}, int(V), int(h), int(T), raster, ep, nsm, 0, pa,
-                                       pb, mc, nh, split_dx ? &scfg : nullptr, &lcfg);
+                                       pb, mc, nh, split_dx ? &scfg : nullptr, &lcfg, -1, winp);
     } else {  // sq8192: plain 8192^3 K-major GEMM (W as an 8192 x 8192 slice), fp32 out
       vp::EpiStoreF32::Params ep{out, 8192, nullptr, 0, nullptr};
       vp::launch_gemm<vp::EpiStoreF32>(2, {W, 8192, false}, {W + int64_t(8192) * 8192, 8192, false}, 8192, 8192,
