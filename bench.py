@@ -487,7 +487,7 @@ def run_ours(args):
         # C1 of the output layer: the fused reduce-scatter (dX epilogue -> the
         # token rows' owners over peer memory) or the dX all-reduce
         line["c1_exchange"] = ("fused: dX GEMM epilogue stores into the owners' peer buffers, owner combine, "
-                               "grad_x all-gather" if ctx.fused_c1_count > 0 else "dX all-reduce")
+                               "grad_x pulled by copy engines" if ctx.fused_c1_count > 0 else "dX all-reduce")
     if args.dry_run:
         line["dry_run"] = ("N ranks shared %d visible GPU(s) through the loopback backend: a functional run of the "
                            "multi-rank path, not a scaling measurement" % torch.cuda.device_count())

@@ -137,8 +137,9 @@ int vp_ctx_reserve(vp_ctx_t ctx, int64_t n_tok, int64_t h, int p);
  * 1 = the dX GEMM of pass S stores each A_k tile straight into the buffer of
  * the rank that owns those token rows, over peer memory (NVLink P2P or CUDA
  * IPC), the label rows follow, and at C1 each owner combines its rows from
- * local memory and the group all-gathers grad_x — a reduce-scatter fused into
- * the GEMM epilogue instead of an all-reduce of [n_tok x h] fp32 partials;
+ * local memory and every rank pulls the owners' rows into grad_x with its copy
+ * engines — a reduce-scatter fused into the GEMM epilogue and an SM-free
+ * all-gather instead of an all-reduce of [n_tok x h] fp32 partials;
  * grad_x has the bits of a one-GPU run over the same shards.  Default 1; the
  * group falls back to the all-reduce when a rank cannot map its peers.
  * 0 = always the all-reduce). */

@@ -394,8 +394,11 @@ std::vector<void*> Comm::open_peers(void* local, cudaStream_t st) {
   mine.host = host_hash();
   mine.ipc_ok = cudaIpcGetMemHandle(&mine.h, local) == cudaSuccess ? 1 : 0;
   (void)cudaGetLastError();
-  void* d = nullptr;
-  VP_CUDA(cudaMalloc(&d, sizeof(PeerRecord) * size_t(nranks + 1) + 16));
+  // a persistent staging buffer: no cudaFree here — it synchronises the whole
+  // device, and ranks that already left this exchange may have queued
+  // stream-side waits on flags this rank has not written yet
+  if (xbuf_ == nullptr) VP_CUDA(cudaMalloc(&xbuf_, sizeof(PeerRecord) * size_t(nranks + 1) + 16));
+  void* d = xbuf_;
   std::vector<PeerRecord> all(static_cast<size_t>(nranks));
   std::vector<void*> out(static_cast<size_t>(nranks), nullptr);
   std::vector<void*> opened;
@@ -443,10 +446,8 @@ std::vector<void*> Comm::open_peers(void* local, cudaStream_t st) {
     VP_CUDA(cudaStreamSynchronize(st));
   } catch (...) {
     for (void* p : opened) cudaIpcCloseMemHandle(p);
-    cudaFree(d);
     throw;
   }
-  cudaFree(d);
   if (fail != 0.f) {
     for (void* p : opened) cudaIpcCloseMemHandle(p);
     (void)cudaGetLastError();

@@ -31,7 +31,7 @@ enum class RedOp { Sum = 0, Max = 1 };
 
 class Comm {
  public:
-  virtual ~Comm() = default;
+  virtual ~Comm() { release_peer_staging(); }
   virtual const char* backend() const = 0;
   // recv[k * count + i] = send_k[i]  (rank order)
   virtual void all_gather(const void* send, void* recv, size_t count, DType dt, cudaStream_t st) = 0;
@@ -61,8 +61,14 @@ class Comm {
   void close_peers(const std::vector<void*>& peers);
   int nranks = 1, rank = 0;
 
+ protected:
+  void release_peer_staging() {
+    if (xbuf_) cudaFree(xbuf_), xbuf_ = nullptr;
+  }
+
  private:
   std::vector<void*> ipc_opened_;
+  void* xbuf_ = nullptr;  // open_peers' staging buffer (kept: see open_peers)
 };
 
 // NCCL from a 128-byte ncclUniqueId; max_ctas bounds NCCL's SM use.

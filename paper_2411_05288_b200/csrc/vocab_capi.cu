@@ -201,8 +201,7 @@ struct vp_ctx_s {
   std::vector<void*> sym_peers;
   std::vector<std::pair<void*, std::vector<void*>>> sym_retired;
   bool sym_failed = false;    // some rank could not map its peers: the all-reduce path
-  DevBuf gfull;               // grad_x all-gather target when n_tok != nranks * R
-  DevBuf bar;                 // one float: the alg1 C2 barrier
+  DevBuf bar;                 // one float: group barriers of the fused exchange
   bool distributed() const { return comm != nullptr && (nranks > 1 || force_collectives); }
   // the NCCL / loopback group; callers check distributed() first
   vp::Comm& cm() const { return *comm; }
@@ -708,23 +707,30 @@ const vp::RankBounds& rank_bounds(vp_ctx_s* c, const vp_shard_t* s) {
   return c->bounds;
 }
 
-// ---- fused C1 over peer memory (alg2 in a group; option "fused_c1") ---------
+// ---- fused C1 / C2 over peer memory (option "fused_c1") ----------------------
 // Rank o owns token rows [o R, min(T, (o + 1) R)), R a multiple of 32 so one
-// epilogue store box (32 rows) never straddles two owners.  See
-// k_alg2_combine_owned for the data flow.
+// epilogue store box (32 rows) never straddles two owners.  Each rank's peer
+// buffer (mapped on every peer) holds
+//   slots [nranks][R][h] fp32 — A_k of my rows, stored by rank k's dX epilogue
+//   B     [R][h] bf16      — the label rows of my tokens, pushed by the label's owner
+//   G     [R][h] fp32      — my rows of grad_x after the combine, pulled by every
+//                            rank's copy engines
+// See k_alg2_combine_owned for the arithmetic.
 struct FusedLayout {
   int64_t R = 0;
-  int n_own = 0;          // ranks that own at least one row
-  size_t slot_bytes = 0;  // [nranks][R][h] fp32
-  size_t need = 0;        // + B [R][h] bf16
+  int n_own = 0;  // ranks that own at least one row
+  size_t slot_off = 0, b_off = 0, g_off = 0, need = 0;
 };
 
 FusedLayout fused_layout(const vp_ctx_s* c, int64_t T, int64_t h) {
   FusedLayout L;
   L.R = round_up(ceil_div(T, c->nranks), 32);
   L.n_own = int(ceil_div(T, L.R));
-  L.slot_bytes = size_t(c->nranks) * size_t(L.R) * size_t(h) * sizeof(float);
-  L.need = L.slot_bytes + size_t(L.R) * size_t(h) * sizeof(__nv_bfloat16);
+  const size_t rowf = size_t(L.R) * size_t(h);
+  L.slot_off = 0;
+  L.b_off = L.slot_off + size_t(c->nranks) * rowf * sizeof(float);
+  L.g_off = L.b_off + size_t(round_up(int64_t(rowf * sizeof(__nv_bfloat16)), 256));
+  L.need = L.g_off + rowf * sizeof(float);
   return L;
 }
 
@@ -771,10 +777,33 @@ bool use_fused_c1(vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* s, int n, 
   return ensure_sym(c, L.need);
 }
 
-// alg2_pass_S with the dX epilogue routed to the token rows' owners and the
-// label rows B_k pushed after it.
+// Routed dX of pass S (alg2) / pass T (alg1): output rows go to slot `rank`
+// of their owners' buffers (the epilogue's TMA stores, over NVLink for a
+// peer), then the label rows B_k (VM.cpp:185-188, :176) into the owners' B.
 void gemm_dx_routed(vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* s, vp_state_s* st, const float* row_scale,
-                    const FusedLayout& L);
+                    const FusedLayout& L) {
+  const int64_t T = b->n_tok, h = b->h;
+  vp::EpiStoreF32::Params ep{nullptr, h, nullptr, 0, row_scale};
+  ep.route_n = L.n_own;
+  ep.route_rows = int(L.R);
+  vp::PeerRows pr{};
+  for (int o = 0; o < L.n_own; ++o) {
+    char* peer = static_cast<char*>(c->sym_peers[size_t(o)]);
+    float* base = reinterpret_cast<float*>(peer + L.slot_off) + size_t(c->rank) * size_t(L.R) * size_t(h);
+    const int64_t rows = std::min(L.R, T - o * L.R);
+    ep.route_map[o] = vp::make_store_map(base, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, uint64_t(h), uint64_t(rows),
+                                         uint64_t(h), VP_F32_BOX128 ? 128 : 64);
+    pr.p[o] = peer + L.b_off;
+  }
+  gemm_dx_ep(c, st, s, ep);
+  vp::k_push_label_rows<<<c->grid_for(T * h / 8, 256), 256, 0, c->stream>>>(
+      static_cast<const __nv_bfloat16*>(s->W), s->ldw, s->row_begin, s->row_end, b->labels, int(T), int(h),
+      int(L.R), pr);
+  VP_KCHECK();
+  ++c->launches;
+}
+
+// alg2_pass_S with the dX epilogue routed to the token rows' owners.
 void alg2_S_fused(vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* s, vp_state_s* st, const FusedLayout& L) {
   pass_S_common(c, b, s, st);
   NvtxRange nr("vp:S:A=softmax'W->owners");
@@ -782,17 +811,22 @@ void alg2_S_fused(vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* s, vp_stat
   st->has_grad_terms = false;  // A_k is in the owners' buffers, not in the state
 }
 
-// The owner's combine of its token rows (from local memory) and the group's
-// grad_x all-gather (+ the loss all-reduce when `loss`), on the comm stream
-// when `overlap`.  alg2 C1: slots hold A_k, scaled here by c_k from the
-// gathered stats; alg1 C2 (`prescaled`): slots hold c_k A_k.
+// The owner's combine of its token rows (local memory only) into G, then the
+// grad_x all-gather by copy engines: `barrier` (a small collective on the
+// compute stream: the loss all-reduce in alg2) orders every owner's combine
+// before any pull, and one peer-to-peer copy per owner pulls its rows straight
+// into grad_x — on the comm stream when `overlap`, so pass T's GEMM keeps
+// every SM (no NCCL kernel runs beside it).  alg2 C1: slots hold A_k, scaled
+// here by c_k from the gathered stats; alg1 C2 (`prescaled`): slots hold c_k A_k.
+template <class Barrier>
 void owner_combine_gather(vp_ctx_s* c, const vp_shard_t* s, const vp_batch_t* b, vp_stats_t g, bool prescaled,
-                          float* loss, float* gx, int64_t ldgx, const FusedLayout& L, bool overlap) {
+                          float* gx, int64_t ldgx, const FusedLayout& L, bool overlap, Barrier&& barrier) {
   const int64_t T = b->n_tok, h = b->h, R = L.R;
   const vp::RankBounds& RB = rank_bounds(c, s);
+  char* mine = static_cast<char*>(c->sym);
   vp::OwnedCombine S{};
-  S.slots = static_cast<const float*>(c->sym);
-  S.B = reinterpret_cast<const __nv_bfloat16*>(static_cast<const char*>(c->sym) + L.slot_bytes);
+  S.slots = reinterpret_cast<const float*>(mine + L.slot_off);
+  S.B = reinterpret_cast<const __nv_bfloat16*>(mine + L.b_off);
   S.gathered = prescaled ? nullptr : static_cast<const float*>(c->gathered.p);
   for (int k = 0; k < c->nranks; ++k) {
     S.rb[k] = RB.rb[k];
@@ -803,30 +837,28 @@ void owner_combine_gather(vp_ctx_s* c, const vp_shard_t* s, const vp_batch_t* b,
   S.row0 = int(c->rank * R);
   S.rows = int(std::max<int64_t>(0, std::min(R, T - c->rank * R)));
   S.prescaled = prescaled ? 1 : 0;
-  const bool exact = R * c->nranks == T && ldgx == h;
-  float* full = exact ? gx : c->buf<float>(c->gfull, size_t(c->nranks * R * h));
-  float* mine = full + c->rank * R * h;
   const int64_t V = global_vocab(c, s, 1);
   if (S.rows > 0) {
     vp::k_alg2_combine_owned<<<c->grid_for(int64_t(S.rows) * h / 4, 256), 256, 0, c->stream>>>(
-        S, g.m, g.sum, b->labels, int(T), int(h), mine, h, V, c->d_err, kErrLabel);
+        S, g.m, g.sum, b->labels, int(T), int(h), reinterpret_cast<float*>(mine + L.g_off), h, V, c->d_err,
+        kErrLabel);
     VP_KCHECK();
     ++c->launches;
   }
-  NvtxRange nx("vp:allgather(dX)");
+  barrier();  // every owner's G is complete (and, for the next step, read)
+  NvtxRange nx("vp:gather(dX): copy engines");
   cudaStream_t xs = c->stream;
   if (overlap) {
     VP_CUDA(cudaEventRecord(c->ev_ready, c->stream));
     VP_CUDA(cudaStreamWaitEvent(c->comm_stream, c->ev_ready, 0));
     xs = c->comm_stream;
   }
-  c->cm().group_start();
-  c->cm().all_gather(mine, full, size_t(R * h), vp::DType::F32, xs);
-  if (loss) c->cm().all_reduce(loss, loss, size_t(T), vp::DType::F32, vp::RedOp::Sum, xs);
-  c->cm().group_end();
-  if (!exact)
-    VP_CUDA(cudaMemcpy2DAsync(gx, size_t(ldgx) * sizeof(float), full, size_t(h) * sizeof(float),
-                              size_t(h) * sizeof(float), size_t(T), cudaMemcpyDeviceToDevice, xs));
+  for (int o = 0; o < L.n_own; ++o) {
+    const int64_t rows = std::min(R, T - o * R);
+    const char* src = static_cast<const char*>(c->sym_peers[size_t(o)]) + L.g_off;
+    VP_CUDA(cudaMemcpy2DAsync(gx + o * R * ldgx, size_t(ldgx) * sizeof(float), src, size_t(h) * sizeof(float),
+                              size_t(h) * sizeof(float), size_t(rows), cudaMemcpyDefault, xs));
+  }
   if (overlap) {
     VP_CUDA(cudaEventRecord(c->ev_done, c->comm_stream));
     c->reduce_pending = true;
@@ -834,43 +866,30 @@ void owner_combine_gather(vp_ctx_s* c, const vp_shard_t* s, const vp_batch_t* b,
   ++c->fused_count;
 }
 
+// One-float collective on the compute stream: a group barrier that is
+// stream-ordered on every rank (NCCL or loopback).
+void group_barrier(vp_ctx_s* c) {
+  float* bar = c->buf<float>(c->bar, 1);
+  c->cm().all_reduce(bar, bar, 1, vp::DType::F32, vp::RedOp::Max, c->stream);
+}
+
 // alg2_barrier_C1 (VM.cpp:193-211) for the fused layout: stats all-gather and
-// merge, the loss at the label owner, then the owners' combine + gather.
+// merge (which also orders every rank's routed stores before the combine),
+// the loss at the label owner + its sum all-reduce (T floats, before pass T),
+// then the owners' combine and the SM-free gather.
 void alg2_C1_fused(vp_ctx_s* c, const vp_state_t st, const vp_shard_t* s, const vp_batch_t* b, double fault_scale,
                    vp_stats_t out, float* loss, float* gx, int64_t ldgx, const FusedLayout& L, bool overlap) {
   NvtxRange nr("vp:C1(fused)");
   require(gx != nullptr && ldgx >= b->h && ldgx % 4 == 0 && aligned16(gx), "alg2_barrier_C1: bad grad_x buffer");
   merge_stats(c, &st, 1, fault_scale, out);
   loss_of(c, &st, s, 1, out, b, loss, /*reduce=*/false);
-  owner_combine_gather(c, s, b, out, false, loss, gx, ldgx, L, overlap);
-}
-
-// Routed dX of a T pass / pass S: out rows go to their owners' slot `rank`,
-// then the label rows B_k (VM.cpp:185-188, :176) into the owners' B rows.
-void gemm_dx_routed(vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* s, vp_state_s* st, const float* row_scale,
-                    const FusedLayout& L) {
-  const int64_t T = b->n_tok, h = b->h;
-  vp::EpiStoreF32::Params ep{nullptr, h, nullptr, 0, row_scale};
-  ep.route_n = L.n_own;
-  ep.route_rows = int(L.R);
-  vp::PeerRows pr{};
-  for (int o = 0; o < L.n_own; ++o) {
-    float* base = static_cast<float*>(c->sym_peers[size_t(o)]) + size_t(c->rank) * size_t(L.R) * size_t(h);
-    const int64_t rows = std::min(L.R, T - o * L.R);
-    ep.route_map[o] = vp::make_store_map(base, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, uint64_t(h), uint64_t(rows),
-                                         uint64_t(h), VP_F32_BOX128 ? 128 : 64);
-    pr.p[o] = static_cast<char*>(c->sym_peers[size_t(o)]) + L.slot_bytes;
-  }
-  gemm_dx_ep(c, st, s, ep);
-  vp::k_push_label_rows<<<c->grid_for(T * h / 8, 256), 256, 0, c->stream>>>(
-      static_cast<const __nv_bfloat16*>(s->W), s->ldw, s->row_begin, s->row_end, b->labels, int(T), int(h),
-      int(L.R), pr);
-  VP_KCHECK();
-  ++c->launches;
+  owner_combine_gather(c, s, b, out, false, gx, ldgx, L, overlap, [&] {
+    c->cm().all_reduce(loss, loss, size_t(b->n_tok), vp::DType::F32, vp::RedOp::Sum, c->stream);
+  });
 }
 
 // alg1 with the fused C2: pass T's dX (c (.) softmax' W_k, VM.cpp:176) goes
-// to the owners; after T a barrier, the owners' combine, the gather.
+// to the owners; after T a barrier, the owners' combine, a barrier, the pulls.
 void run_alg1_fused(vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* s, vp_state_t st, double fault_scale,
                     vp_stats_t out, float* loss, float* gx, int64_t ldgx, float* gw, int64_t ldgw,
                     const FusedLayout& L) {
@@ -888,28 +907,24 @@ void run_alg1_fused(vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* s, vp_st
                     b->ldx, b->h, -1.f, gw, ldgw, 1, kErrLabel);
   }
   NvtxRange nr("vp:C2(fused)");
-  // every rank's routed stores are complete (stream order + the collective)
-  float* bar = c->buf<float>(c->bar, 1);
-  c->cm().all_reduce(bar, bar, 1, vp::DType::F32, vp::RedOp::Max, c->stream);
-  owner_combine_gather(c, s, b, out, true, nullptr, gx, ldgx, L, false);
+  group_barrier(c);  // every rank's routed stores and label rows have landed
+  owner_combine_gather(c, s, b, out, true, gx, ldgx, L, false, [&] { group_barrier(c); });
 }
 
+// The exchange after the combine needs no SM, so pass T's dW GEMM keeps all
+// of them (the all-reduce path leaves comm_sms to NCCL during T).
 void run_alg2_fused(vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* s, vp_state_t st, double fault_scale,
                     vp_stats_t out, float* loss, float* gx, int64_t ldgx, float* gw, int64_t ldgw,
                     const FusedLayout& L) {
   alg2_S_fused(c, b, s, st, L);
   const bool overlap = c->overlap_c1 && c->comm_stream != nullptr;
   alg2_C1_fused(c, st, s, b, fault_scale, out, loss, gx, ldgx, L, overlap);
-  const int sms = c->gemm_sms;
-  if (overlap) c->gemm_sms = std::max(2, (c->gemm_sms - c->comm_sms) / 2 * 2);
   try {
     alg2_T(c, st, out, b, s, gw, ldgw);
   } catch (...) {
-    c->gemm_sms = sms;
     join_allreduces(c);
     throw;
   }
-  c->gemm_sms = sms;
   join_allreduces(c);
 }
 
@@ -1296,10 +1311,10 @@ int vp_ctx_destroy(vp_ctx_t c) {
       c->comm->close_peers(c->sym_peers);
       for (auto& r : c->sym_retired) c->comm->close_peers(r.second);
     }
+    c->bar.release();
     if (c->sym) cudaFree(c->sym);
     for (auto& r : c->sym_retired) cudaFree(r.first);
-    c->gfull.release();
-    c->bar.release();
+
     c->comm.reset();
     if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
     if (c->ev_ready) cudaEventDestroy(c->ev_ready);
