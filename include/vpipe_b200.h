@@ -132,6 +132,11 @@ int vp_ctx_reserve(vp_ctx_t ctx, int64_t n_tok, int64_t h, int p);
  * raster_dw=-8 policy_dw=0 policyb_dw=2, DRAM bytes per launch fall to about
  * the algorithmic bytes, but in-step throughput measured 0.5-1.5% lower
  * (profiles/r02y_*, r02z_*); default 0),
+ * "peer_input" (vp_input_forward_gathered in a group: 1 = every rank writes
+ * its owned rows at their token index into a peer-mapped buffer and, after a
+ * one-float barrier, reads every row from its owner's buffer (NVLink P2P / CUDA
+ * IPC): two kernels and no host-side sizes, so the call is capturable;
+ * default 1; 0 or an unmappable group = the packed broadcasts),
  * "fused_c1" (vp_run_alg2 / vp_run_alg2_chunked / vp_run_alg1 in a group of
  * nranks > 1 (alg1: the dX of pass T, then C2):
  * 1 = the dX GEMM of pass S stores each A_k tile straight into the buffer of
@@ -160,6 +165,9 @@ int64_t vp_ctx_launch_count(vp_ctx_t ctx);
 /* Number of fused C1 exchanges (option "fused_c1") this context has run;
  * -1 for a null context (evidence counter). */
 int64_t vp_ctx_fused_c1_count(vp_ctx_t ctx);
+/* Number of vp_input_forward_gathered calls that took the peer-pull path
+ * (option "peer_input"); -1 for a null context (evidence counter). */
+int64_t vp_ctx_peer_input_count(vp_ctx_t ctx);
 /* Per-GEMM CUDA-event timing on the launching stream.  Returns (and resets)
  * the accumulated milliseconds / launch counts per GEMM kind since the last
  * call — [0] logits+stats (K1), [1] fp32 logits (naive F1), [2] dX (K3),

@@ -77,6 +77,17 @@ struct DevBuf {
   }
 };
 
+// A device buffer mapped on every rank of the group (Comm::open_peers).
+// Grow-only; a grown buffer and its mappings stay alive until the context is
+// destroyed (graphs keep the old pointers).
+struct SymBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  std::vector<void*> peers;  // every rank's buffer as mapped here (own included)
+  std::vector<std::pair<void*, std::vector<void*>>> retired;
+  bool failed = false;       // some rank could not map its peers: the collective path
+};
+
 // deferred device-side argument errors (d_err bits), reported by vp_ctx_sync
 constexpr int kErrInputFwd = 1, kErrInputBwd = 2, kErrLabel = 4;
 
@@ -196,11 +207,10 @@ struct vp_ctx_s {
   // the context is destroyed (graphs keep the old pointers).
   bool fused_c1 = true;
   int64_t fused_count = 0;
-  void* sym = nullptr;
-  size_t sym_bytes = 0;
-  std::vector<void*> sym_peers;
-  std::vector<std::pair<void*, std::vector<void*>>> sym_retired;
-  bool sym_failed = false;    // some rank could not map its peers: the all-reduce path
+  SymBuf sym;     // output layer (slots, B, G)
+  SymBuf in_sym;  // input layer: owned rows by token index, two halves (call parity)
+  bool peer_input = true;  // option "peer_input": the input forward pulls rows over peer memory
+  int64_t in_calls = 0, peer_input_count = 0;
   DevBuf bar;                 // one float: group barriers of the fused exchange
   bool distributed() const { return comm != nullptr && (nranks > 1 || force_collectives); }
   // the NCCL / loopback group; callers check distributed() first
@@ -734,15 +744,15 @@ FusedLayout fused_layout(const vp_ctx_s* c, int64_t T, int64_t h) {
   return L;
 }
 
-// Collective: every rank's peer buffer holds >= need bytes and is mapped on
+// Collective: every rank's buffer `sb` holds >= need bytes and is mapped on
 // every peer.  false (on every rank) when some rank cannot map its peers.
-bool ensure_sym(vp_ctx_s* c, size_t need) {
-  if (c->sym_failed) return false;
-  if (need <= c->sym_bytes) return true;
+bool ensure_sym(vp_ctx_s* c, SymBuf& sb, size_t need) {
+  if (sb.failed) return false;
+  if (need <= sb.bytes) return true;
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   VP_CUDA(cudaStreamIsCapturing(c->stream, &cs));
   require(cs == cudaStreamCaptureStatusNone,
-          "fused_c1: the peer buffers must be sized outside graph capture (run the step once eagerly first)");
+          "peer buffers must be sized outside graph capture (run the step once eagerly first)");
   const size_t bytes = size_t(round_up(int64_t(need), int64_t(2) << 20));
   void* p = nullptr;
   VP_CUDA(cudaMalloc(&p, bytes));
@@ -755,13 +765,13 @@ bool ensure_sym(vp_ctx_s* c, size_t need) {
   }
   if (peers.empty()) {
     cudaFree(p);
-    c->sym_failed = true;
+    sb.failed = true;
     return false;
   }
-  if (c->sym) c->sym_retired.emplace_back(c->sym, c->sym_peers);
-  c->sym = p;
-  c->sym_bytes = bytes;
-  c->sym_peers = std::move(peers);
+  if (sb.p) sb.retired.emplace_back(sb.p, sb.peers);
+  sb.p = p;
+  sb.bytes = bytes;
+  sb.peers = std::move(peers);
   return true;
 }
 
@@ -769,12 +779,12 @@ bool ensure_sym(vp_ctx_s* c, size_t need) {
 // same branch); per-rank buffer requirements are checked, not negotiated.
 bool use_fused_c1(vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* s, int n, FusedLayout& L) {
   if (!(c->fused_c1 && c->distributed() && c->nranks > 1 && n == 1 && c->nranks <= vp::kMaxRoute &&
-        b->h % 8 == 0 && !c->sym_failed))
+        b->h % 8 == 0 && !c->sym.failed))
     return false;
   require(s->ldw % 8 == 0 && aligned16(s->W),
           "fused_c1: the shard needs ldw % 8 == 0 and a 16-byte aligned W (or set fused_c1 = 0 on every rank)");
   L = fused_layout(c, b->n_tok, b->h);
-  return ensure_sym(c, L.need);
+  return ensure_sym(c, c->sym, L.need);
 }
 
 // Routed dX of pass S (alg2) / pass T (alg1): output rows go to slot `rank`
@@ -788,7 +798,7 @@ void gemm_dx_routed(vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* s, vp_st
   ep.route_rows = int(L.R);
   vp::PeerRows pr{};
   for (int o = 0; o < L.n_own; ++o) {
-    char* peer = static_cast<char*>(c->sym_peers[size_t(o)]);
+    char* peer = static_cast<char*>(c->sym.peers[size_t(o)]);
     float* base = reinterpret_cast<float*>(peer + L.slot_off) + size_t(c->rank) * size_t(L.R) * size_t(h);
     const int64_t rows = std::min(L.R, T - o * L.R);
     ep.route_map[o] = vp::make_store_map(base, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, uint64_t(h), uint64_t(rows),
@@ -823,7 +833,7 @@ void owner_combine_gather(vp_ctx_s* c, const vp_shard_t* s, const vp_batch_t* b,
                           float* gx, int64_t ldgx, const FusedLayout& L, bool overlap, Barrier&& barrier) {
   const int64_t T = b->n_tok, h = b->h, R = L.R;
   const vp::RankBounds& RB = rank_bounds(c, s);
-  char* mine = static_cast<char*>(c->sym);
+  char* mine = static_cast<char*>(c->sym.p);
   vp::OwnedCombine S{};
   S.slots = reinterpret_cast<const float*>(mine + L.slot_off);
   S.B = reinterpret_cast<const __nv_bfloat16*>(mine + L.b_off);
@@ -855,7 +865,7 @@ void owner_combine_gather(vp_ctx_s* c, const vp_shard_t* s, const vp_batch_t* b,
   }
   for (int o = 0; o < L.n_own; ++o) {
     const int64_t rows = std::min(R, T - o * R);
-    const char* src = static_cast<const char*>(c->sym_peers[size_t(o)]) + L.g_off;
+    const char* src = static_cast<const char*>(c->sym.peers[size_t(o)]) + L.g_off;
     VP_CUDA(cudaMemcpy2DAsync(gx + o * R * ldgx, size_t(ldgx) * sizeof(float), src, size_t(h) * sizeof(float),
                               size_t(h) * sizeof(float), size_t(rows), cudaMemcpyDefault, xs));
   }
@@ -1307,13 +1317,15 @@ int vp_ctx_destroy(vp_ctx_t c) {
     if (!c) return;
     c->activate();
     cudaStreamSynchronize(c->stream);
-    if (c->comm) {
-      c->comm->close_peers(c->sym_peers);
-      for (auto& r : c->sym_retired) c->comm->close_peers(r.second);
+    for (SymBuf* sb : {&c->sym, &c->in_sym}) {
+      if (c->comm) {
+        c->comm->close_peers(sb->peers);
+        for (auto& r : sb->retired) c->comm->close_peers(r.second);
+      }
+      if (sb->p) cudaFree(sb->p);
+      for (auto& r : sb->retired) cudaFree(r.first);
     }
     c->bar.release();
-    if (c->sym) cudaFree(c->sym);
-    for (auto& r : c->sym_retired) cudaFree(r.first);
 
     c->comm.reset();
     if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
@@ -1402,6 +1414,9 @@ int vp_ctx_set_option(vp_ctx_t c, const char* key, int64_t value) {
     } else if (k == "persist_logits" || k == "persist_dw") {
       require(value == 0 || value == 1, "vp_ctx_set_option: persist_* must be 0 or 1");
       c->persist[k == "persist_logits" ? 0 : 2] = int(value);
+    } else if (k == "peer_input") {
+      require(value == 0 || value == 1, "vp_ctx_set_option: peer_input must be 0 or 1");
+      c->peer_input = value != 0;
     } else if (k == "fused_c1") {
       require(value == 0 || value == 1, "vp_ctx_set_option: fused_c1 must be 0 or 1");
       c->fused_c1 = value != 0;
@@ -1463,6 +1478,7 @@ int vp_ctx_set_option(vp_ctx_t c, const char* key, int64_t value) {
 
 int64_t vp_ctx_launch_count(vp_ctx_t c) { return c ? c->launches : -1; }
 int64_t vp_ctx_fused_c1_count(vp_ctx_t c) { return c ? c->fused_count : -1; }
+int64_t vp_ctx_peer_input_count(vp_ctx_t c) { return c ? c->peer_input_count : -1; }
 
 int vp_ctx_set_logit_shift(vp_ctx_t c, const float* shift) {
   return api([&] {
@@ -1999,6 +2015,29 @@ int vp_input_forward_gathered(vp_ctx_t c, const int64_t* tokens, int64_t n_tok, 
       return;
     }
     require(n_tok < (int64_t(1) << 31), "input_forward_gathered: too many tokens");
+    if (c->peer_input && c->nranks <= vp::kMaxRoute && !c->in_sym.failed &&
+        ensure_sym(c, c->in_sym, 2 * size_t(round_up(n_tok * h * 2, 256)))) {
+      // peer pull: owned rows at their token index in my buffer (half `par`),
+      // a group barrier, then row i read from its owner's buffer
+      NvtxRange nr("vp:input_forward(peer pull)");
+      const vp::RankBounds& B = rank_bounds(c, s);
+      const size_t half = c->in_sym.bytes / 2 / 256 * 256;
+      const size_t off = size_t(c->in_calls++ & 1) * half;
+      vp::k_input_own_rows<<<c->grid_for(n_tok, 8), 256, 0, c->stream>>>(
+          tokens, int(n_tok), static_cast<const __nv_bfloat16*>(s->W), s->ldw, s->row_begin, s->row_end, int(h),
+          reinterpret_cast<__nv_bfloat16*>(static_cast<char*>(c->in_sym.p) + off), c->d_err);
+      VP_KCHECK();
+      group_barrier(c);
+      vp::PeerBufs P{};
+      for (int k = 0; k < c->nranks; ++k)
+        P.p[k] = reinterpret_cast<const __nv_bfloat16*>(static_cast<const char*>(c->in_sym.peers[size_t(k)]) + off);
+      vp::k_input_pull_rows<<<c->grid_for(n_tok, 8), 256, 0, c->stream>>>(tokens, int(n_tok), B, P, int(h),
+                                                                         static_cast<__nv_bfloat16*>(out), ldo);
+      VP_KCHECK();
+      c->launches += 2;
+      ++c->peer_input_count;
+      return;
+    }
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
     VP_CUDA(cudaStreamIsCapturing(c->stream, &cap));
     require(cap == cudaStreamCaptureStatusNone,

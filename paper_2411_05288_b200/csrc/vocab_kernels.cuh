@@ -673,4 +673,51 @@ __global__ void k_owner_unpack(const int64_t* __restrict__ tok, int n, RankBound
   }
 }
 
+// ---- input layer, N > 1, over peer memory (option "peer_input") ------------
+// Every rank writes the rows it owns at their token index into its own
+// peer-visible buffer (one half per call parity); after a group barrier every
+// rank pulls row i from the buffer of token i's owner — over NVLink for a peer
+// — straight into its output.  No packing positions, no host-side sizes, one
+// tiny collective: capturable.  Pure copies: bit-exact.
+__global__ void k_input_own_rows(const int64_t* __restrict__ tok, int n, const __nv_bfloat16* __restrict__ W,
+                                 int64_t ldw, int64_t rb, int64_t re, int h, __nv_bfloat16* __restrict__ buf,
+                                 int* __restrict__ err) {
+  const int warps = blockDim.x >> 5, lane = threadIdx.x & 31;
+  for (int i = blockIdx.x * warps + (threadIdx.x >> 5); i < n; i += gridDim.x * warps) {
+    const int64_t t = tok[i];
+    if (t < 0 && lane == 0) atomicOr(err, 1);  // VM.cpp:232
+    if (t < rb || t >= re) continue;
+    const uint4* s = reinterpret_cast<const uint4*>(W + (t - rb) * ldw);
+    uint4* d = reinterpret_cast<uint4*>(buf + int64_t(i) * h);
+    for (int j = lane; j < h / 8; j += 32) d[j] = __ldg(s + j);
+  }
+}
+struct PeerBufs {
+  const __nv_bfloat16* p[kMaxLocalShards];  // rank k's current half, as mapped here
+};
+__global__ void k_input_pull_rows(const int64_t* __restrict__ tok, int n, RankBounds B, PeerBufs P, int h,
+                                  __nv_bfloat16* __restrict__ out, int64_t ldo) {
+  const int warps = blockDim.x >> 5, lane = threadIdx.x & 31;
+  const int hv = h / 8;
+  for (int i = blockIdx.x * warps + (threadIdx.x >> 5); i < n; i += gridDim.x * warps) {
+    const int k = owner_of(B, tok[i]);
+    uint4* d = reinterpret_cast<uint4*>(out + int64_t(i) * ldo);
+    if (k < 0) {
+      for (int j = lane; j < hv; j += 32) d[j] = make_uint4(0u, 0u, 0u, 0u);
+      continue;
+    }
+    const uint4* s = reinterpret_cast<const uint4*>(P.p[k] + int64_t(i) * h);
+    // four 16-byte loads in flight per lane before the stores (NVLink latency)
+    for (int j0 = lane; j0 < hv; j0 += 128) {
+      uint4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (j0 + 32 * u < hv) v[u] = s[j0 + 32 * u];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (j0 + 32 * u < hv) d[j0 + 32 * u] = v[u];
+    }
+  }
+}
+
 }  // namespace vp

@@ -79,6 +79,11 @@ class Context:
         """Fused C1 exchanges run so far (dX GEMM -> owner over peer memory)."""
         return int(self.lib.vp_ctx_fused_c1_count(self.handle))
 
+    @property
+    def peer_input_count(self) -> int:
+        """Input forwards that pulled their rows over peer memory."""
+        return int(self.lib.vp_ctx_peer_input_count(self.handle))
+
     def gemm_timing(self, enable: bool):
         """Accumulated (ms, launches) per GEMM kind since the last call
         (logits, logits_f32, dx, dw), then switches event timing on/off."""

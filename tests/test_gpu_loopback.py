@@ -194,11 +194,14 @@ def test_input_layer_across_ranks_is_bit_exact(p):
     _close(ctxs)
 
 
+@pytest.mark.parametrize("peer", [1, 0])
 @pytest.mark.parametrize("p,ids", [(2, "uniform"), (4, "zipf"), (8, "uniform"), (8, "hot")])
-def test_input_layer_owner_gather_and_grad_broadcast(p, ids):
-    # forward without the zero-padded all-reduce: each rank packs the rows it
-    # owns, one grouped broadcast per rank, unpack -> W[tok] bit-exact on every
-    # rank (tokens past V: zero rows, as the reference's unowned rows).
+def test_input_layer_owner_gather_and_grad_broadcast(p, ids, peer):
+    # forward without the zero-padded all-reduce -> W[tok] bit-exact on every
+    # rank (tokens past V: zero rows, as the reference's unowned rows):
+    # peer=1 (default) every rank writes its owned rows at their token index
+    # into its peer-mapped buffer and pulls each row from its owner's buffer;
+    # peer=0 each rank packs its rows, one grouped broadcast per rank, unpack.
     # backward: grad_out lives on one rank (root p-1, the last pipeline stage)
     # and is broadcast before every shard's scatter (R/PAPER.md:582).
     V, h, T = 1000 * p, 136, 3001
@@ -215,6 +218,8 @@ def test_input_layer_owner_gather_and_grad_broadcast(p, ids):
     grad = torch.from_numpy(rng.standard_normal((T, h)).astype(np.float32)).cuda()
     torch.cuda.synchronize()
     ctxs = vpd.local_group(p)
+    for c in ctxs:
+        c.set_option("peer_input", peer)
 
     def rank(r, ctx):
         sh = _shard(W, p, r)
@@ -234,6 +239,33 @@ def test_input_layer_owner_gather_and_grad_broadcast(p, ids):
         assert torch.equal(g, grad), r
         rb, re = vpd.shard_rows(V, p, r)
         assert np.array_equal(dE.cpu().numpy(), oracle.input_backward_f32(g_np, t[:-5], re - rb, rb)), r
+    assert [c.peer_input_count for c in ctxs] == [peer] * p
+    _close(ctxs)
+
+
+def test_input_peer_pull_repeated_calls():
+    # back-to-back forwards alternate the two halves of the peer buffers (a
+    # rank's next write never races a peer's pull of the previous call); a
+    # larger batch grows the buffers
+    p, V, h = 4, 4000, 256
+    rng = np.random.default_rng(3)
+    W = torch.from_numpy(rng.standard_normal((V, h)).astype(np.float32)).to(torch.bfloat16).cuda()
+    ctxs = vpd.local_group(p)
+    calls = [(700, 1), (700, 2), (2100, 3), (64, 4), (700, 5)]
+    toks = [torch.from_numpy(np.random.default_rng(sd).integers(0, V, T).astype(np.int64)).cuda() for T, sd in calls]
+    torch.cuda.synchronize()
+
+    def rank(r, ctx):
+        sh = _shard(W, p, r)
+        outs = [vm.input_forward_gathered(ctx, t, sh) for t in toks]
+        ctx.sync()
+        return outs
+
+    res = vpd.run_ranks(ctxs, rank)
+    for r in range(p):
+        for t, out in zip(toks, res[r]):
+            assert torch.equal(out, W[t]), r
+    assert [c.peer_input_count for c in ctxs] == [len(calls)] * p
     _close(ctxs)
 
 
