@@ -732,15 +732,17 @@ struct FusedLayout {
   size_t slot_off = 0, b_off = 0, g_off = 0, need = 0;
 };
 
-FusedLayout fused_layout(const vp_ctx_s* c, int64_t T, int64_t h) {
+// `base`: byte offset of this layout's region in the peer buffer (the
+// executor keeps one region per microbatch); need = base + region bytes.
+FusedLayout fused_layout(const vp_ctx_s* c, int64_t T, int64_t h, size_t base = 0) {
   FusedLayout L;
   L.R = round_up(ceil_div(T, c->nranks), 32);
   L.n_own = int(ceil_div(T, L.R));
   const size_t rowf = size_t(L.R) * size_t(h);
-  L.slot_off = 0;
+  L.slot_off = base;
   L.b_off = L.slot_off + size_t(c->nranks) * rowf * sizeof(float);
   L.g_off = L.b_off + size_t(round_up(int64_t(rowf * sizeof(__nv_bfloat16)), 256));
-  L.need = L.g_off + rowf * sizeof(float);
+  L.need = size_t(round_up(int64_t(L.g_off + rowf * sizeof(float)), 256));
   return L;
 }
 
@@ -898,6 +900,23 @@ void alg2_C1_fused(vp_ctx_s* c, const vp_state_t st, const vp_shard_t* s, const 
   });
 }
 
+// alg1_pass_T (VM.cpp:164-179) with the dX partial routed to the owners.
+void alg1_T_routed(vp_ctx_s* c, vp_state_s* st, vp_stats_t g, const vp_batch_t* b, const vp_shard_t* s, float* gw,
+                   int64_t ldgw, const FusedLayout& L) {
+  NvtxRange nr("vp:T(alg1, dX->owners)");
+  check_batch(b);
+  check_shard(s, b->h);
+  check_state(st, b, s);
+  require(st->has_S && st->form == kLocal, "alg1_pass_T: state/stats length mismatch");
+  require(g.m && g.sum, "alg1_pass_T: null stats");
+  check_grad_w(gw, ldgw, b->h, "alg1_pass_T: grad_w needs ldgw >= h, ldgw % 4 == 0 and a 16-byte aligned base");
+  const float* sc = global_scale(c, st, g);
+  gemm_dx_routed(c, b, s, st, sc, L);
+  gemm_dw(c, st, scaled_x(c, b, sc), b->h, gw, ldgw);
+  segment_scatter(c, b->labels, b->n_tok, s->row_begin, s->row_end, static_cast<const __nv_bfloat16*>(b->X), b->ldx,
+                  b->h, -1.f, gw, ldgw, 1, kErrLabel);
+}
+
 // alg1 with the fused C2: pass T's dX (c (.) softmax' W_k, VM.cpp:176) goes
 // to the owners; after T a barrier, the owners' combine, a barrier, the pulls.
 void run_alg1_fused(vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* s, vp_state_t st, double fault_scale,
@@ -906,16 +925,8 @@ void run_alg1_fused(vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* s, vp_st
   pass_S_common(c, b, s, st);
   merge_stats(c, &st, 1, fault_scale, out);
   loss_of(c, &st, s, 1, out, b, loss);
-  {
-    NvtxRange nr("vp:T(alg1, dX->owners)");
-    require(gx != nullptr && ldgx >= b->h && ldgx % 4 == 0 && aligned16(gx), "run_alg1: bad grad_x buffer");
-    check_grad_w(gw, ldgw, b->h, "alg1_pass_T: grad_w needs ldgw >= h, ldgw % 4 == 0 and a 16-byte aligned base");
-    const float* sc = global_scale(c, st, out);
-    gemm_dx_routed(c, b, s, st, sc, L);
-    gemm_dw(c, st, scaled_x(c, b, sc), b->h, gw, ldgw);
-    segment_scatter(c, b->labels, b->n_tok, s->row_begin, s->row_end, static_cast<const __nv_bfloat16*>(b->X),
-                    b->ldx, b->h, -1.f, gw, ldgw, 1, kErrLabel);
-  }
+  require(gx != nullptr && ldgx >= b->h && ldgx % 4 == 0 && aligned16(gx), "run_alg1: bad grad_x buffer");
+  alg1_T_routed(c, st, out, b, s, gw, ldgw, L);
   NvtxRange nr("vp:C2(fused)");
   group_barrier(c);  // every rank's routed stores and label rows have landed
   owner_combine_gather(c, s, b, out, true, gx, ldgx, L, false, [&] { group_barrier(c); });
@@ -1130,10 +1141,28 @@ void run_program(vp_ctx_s* c, const vp::Program& prog, const vp_batch_t* batches
     for (int i = 0; i < n; ++i) check_state(st(ls, i), &batches[i], &shards[ls]);
   }
   const bool overlap = dist && c->overlap_c1 && c->comm_stream != nullptr;
+  // Fused exchange (option "fused_c1"): one peer-buffer region per microbatch,
+  // so S (alg2) / T (alg1) of several microbatches may precede their barriers
+  std::vector<FusedLayout> FL;
+  {
+    bool fused = dist && c->fused_c1 && c->nranks > 1 && c->nranks <= vp::kMaxRoute && !c->sym.failed;
+    for (int i = 0; fused && i < n; ++i) fused = batches[i].h % 8 == 0;
+    if (fused) {
+      require(shards[0].ldw % 8 == 0 && aligned16(shards[0].W),
+              "fused_c1: the shard needs ldw % 8 == 0 and a 16-byte aligned W (or set fused_c1 = 0 on every rank)");
+      size_t region = 0;
+      for (int i = 0; i < n; ++i) region = std::max(region, fused_layout(c, batches[i].n_tok, batches[i].h).need);
+      for (int i = 0; i < n; ++i) FL.push_back(fused_layout(c, batches[i].n_tok, batches[i].h, size_t(i) * region));
+      if (!ensure_sym(c, c->sym, size_t(n) * region)) FL.clear();
+    }
+  }
+  const bool fused = !FL.empty();
   const bool acc0 = c->accumulate_dw;
   const int sms0 = c->gemm_sms;
   c->accumulate_dw = true;
-  if (overlap) c->gemm_sms = std::max(2, (c->gemm_sms - c->comm_sms) / 2 * 2);
+  // the all-reduce path leaves comm_sms to NCCL during the overlap; the fused
+  // exchange's gather runs on copy engines
+  if (overlap && !fused) c->gemm_sms = std::max(2, (c->gemm_sms - c->comm_sms) / 2 * 2);
   auto restore = [&] {
     c->accumulate_dw = acc0;
     c->gemm_sms = sms0;
@@ -1148,10 +1177,13 @@ void run_program(vp_ctx_s* c, const vp::Program& prog, const vp_batch_t* batches
       const int ls = dist ? 0 : d, i = ps.microbatch;
       vp_state_s* s_ = st(ls, i);
       if (ps.kind == vp::PKind::S) {
-        if (alg2) alg2_S(c, &batches[i], &shards[ls], s_);
+        if (alg2 && fused) alg2_S_fused(c, &batches[i], &shards[ls], s_, FL[size_t(i)]);
+        else if (alg2) alg2_S(c, &batches[i], &shards[ls], s_);
         else pass_S_common(c, &batches[i], &shards[ls], s_);
       } else if (alg2) {
         alg2_T(c, s_, stats[i], &batches[i], &shards[ls], gw[ls], ldgw);
+      } else if (fused) {
+        alg1_T_routed(c, s_, stats[i], &batches[i], &shards[ls], gw[ls], ldgw, FL[size_t(i)]);
       } else {
         // Algorithm 1: dX partial (local: the state's buffer; NCCL: grad_x, reduced by C2)
         alg1_T(c, s_, stats[i], &batches[i], &shards[ls], dist ? gx[i] : s_->A, dist ? ldgx : batches[i].h, gw[ls],
@@ -1168,6 +1200,13 @@ void run_program(vp_ctx_s* c, const vp::Program& prog, const vp_batch_t* batches
         if (dist)
           c->cm().broadcast(b->X, const_cast<void*>(b->X), size_t((T - 1) * b->ldx + b->h), vp::DType::BF16, p - 1,
                             c->stream);  // the logical extent of X: (T-1) ldx + h elements
+      } else if (k == vp::PKind::C1 && fused && alg2) {
+        alg2_C1_fused(c, sts[0], shards, b, 1.0, stats[i], loss[i], gx[i], ldgx, FL[size_t(i)], overlap);
+      } else if (k == vp::PKind::C2 && fused) {
+        NvtxRange nr("vp:C2(fused)");
+        group_barrier(c);  // every rank's routed stores and label rows of microbatch i have landed
+        owner_combine_gather(c, shards, b, stats[i], true, gx[i], ldgx, FL[size_t(i)], overlap,
+                             [&] { group_barrier(c); });
       } else if (k == vp::PKind::C1) {
         if (alg2) {
           alg2_C1(c, sts.data(), shards, nsh, b, 1.0, stats[i], gx[i], ldgx, /*reduce=*/!overlap);

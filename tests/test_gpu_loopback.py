@@ -289,10 +289,13 @@ def test_label_out_of_range_raises_on_every_rank():
     _close(ctxs)
 
 
+@pytest.mark.parametrize("fused", [1, 0])
 @pytest.mark.parametrize("name", ["vocab2_p2_n4", "vocab2_p4_n8", "vocab1_p2_n4", "interlaced_p4_n8"])
-def test_executor_one_program_device_per_rank(name):
+def test_executor_one_program_device_per_rank(name, fused):
     # vp_program_run in a group: rank k executes device k's pass list (C0
-    # broadcast of X_i from device p-1, C1 / C2 exchanges on the comm stream)
+    # broadcast of X_i from device p-1, C1 / C2 exchanges on the comm stream;
+    # fused=1: the peer-memory exchange with one buffer region per microbatch,
+    # so several microbatches' S (alg2) / T (alg1) precede their barriers)
     import json
     golden = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "programs.json")))
     prog = vm.Program(golden[name]["text"])
@@ -311,6 +314,8 @@ def test_executor_one_program_device_per_rank(name):
     lctx.sync()
     torch.cuda.synchronize()
     ctxs = vpd.local_group(p)
+    for c in ctxs:
+        c.set_option("fused_c1", fused)
 
     def rank(r, ctx):
         # C0 broadcasts X_i from device p-1: the other ranks start from garbage
@@ -336,6 +341,7 @@ def test_executor_one_program_device_per_rank(name):
         gw_ref = gw_ref + ref.grad_w
     got = torch.cat([o[0].grad_w[0] for o in outs])[:, :h].cpu().numpy()
     assert rel_l2(got, gw_ref) <= GRAD_REL_L2
+    assert [c.fused_c1_count for c in ctxs] == [n * fused] * p
     _close(ctxs)
     lctx.close()
 
