@@ -560,10 +560,11 @@ def run_reference_input(args):
 
 def run_input(args):
     """BASELINE configs[3]: V=256000, h=4096, 16384 token ids.  One step =
-    input_forward of this rank's shard (masked 16-byte-vector gather) + the
-    sum all-reduce across ranks + input_backward (deterministic ascending-i
-    scatter-add, accumulated into the rank's embedding-gradient buffer as in
-    training)."""
+    the input layer forward over the group (vp_input_forward_gathered: at N=1
+    the masked 16-byte-vector gather; at N>1 owned rows written into
+    peer-mapped buffers and every row pulled from its owner over NVLink) +
+    input_backward (deterministic ascending-i scatter-add, accumulated into the
+    rank's embedding-gradient buffer as in training)."""
     import torch
     import torch.distributed as dist
 
@@ -606,8 +607,7 @@ def run_input(args):
     def step(timed=False):
         if timed:
             ev[0].record(stream)
-        vm.input_forward(ctx, tok, shard, out=emb)
-        vm.allreduce_sum(ctx, emb)
+        vm.input_forward_gathered(ctx, tok, shard, out=emb)
         if timed:
             ev[1].record(stream)
         vm.input_backward(ctx, grad, tok, shard, out=dE, accumulate=True)
@@ -664,8 +664,7 @@ def run_input(args):
                     issue_copy(i + 1)
                 b = i % 2
                 stream.wait_event(ready[b])
-                vm.input_forward(ctx, bufs[b][0], shard, out=emb)
-                vm.allreduce_sum(ctx, emb)
+                vm.input_forward_gathered(ctx, bufs[b][0], shard, out=emb)
                 vm.input_backward(ctx, bufs[b][1], bufs[b][0], shard, out=dE, accumulate=True)
                 consumed[b].record(stream)
                 out_h.copy_(emb[0], non_blocking=True)
@@ -680,7 +679,7 @@ def run_input(args):
         me = max_over_ranks(e0.elapsed_time(e1) / args.steps)
         e2e = {"value": T / (me / 1e3), "unit": "tokens/s", "ms_per_step": me,
                "h2d_bytes_per_step": tok_h.numel() * 8 + grad_h.numel() * 2, "d2h_bytes_per_step": h * 2,
-               "path": "vp_input_forward / vp_allreduce_sum / vp_input_backward via ctypes; ids + grad from pinned "
+               "path": "vp_input_forward_gathered / vp_input_backward via ctypes; ids + grad from pinned "
                        "host (double-buffered on a copy stream, overlapping the previous step)"}
     if rank != 0:
         ctx.close()
@@ -705,15 +704,15 @@ def run_input(args):
         "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
         "data": f"synthetic ({args.ids} ids, W~N(0,0.02^2), grad~N(0,1), seed 1234)",
-        "config": {"workload": "vocab-parallel input embedding: masked gather + all-reduce fwd, deterministic "
-                               "scatter-add bwd (accumulating)", "tokens": T, "hidden": h, "vocab": V,
+        "config": {"workload": "vocab-parallel input embedding: masked gather fwd (N>1: owned rows pulled from "
+                               "their owners over peer memory), deterministic scatter-add bwd (accumulating)", "tokens": T, "hidden": h, "vocab": V,
                    "ids": args.ids, "owned_ids": owned_ids, "distinct_rows": owned_rows,
                    "vocab_rows_per_gpu": rows, "parallelism": f"vocab{world}"},
         "e2e": e2e, "gpu_launches": launches,
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm, "traffic": None,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback",
-                     "phase_ms": {"forward+allreduce": f_ms, "backward": b_ms},
+                     "phase_ms": {"forward(+exchange)": f_ms, "backward": b_ms},
                      "bytes_per_launch": {"input_forward": fwd_bytes, "input_backward": bwd_bytes}},
         "cpu_baseline": cpu, "clocks": clk.summary(), "comm": ctx.comm_backend,
     }

@@ -567,7 +567,20 @@ __global__ void k_input_forward(const int64_t* __restrict__ tok, int n, const __
     const uint4* s = reinterpret_cast<const uint4*>(W + (own ? (t - rb) : 0) * ldw);
     const int hv = h / 8;
     if (!accumulate) {
-      for (int j = lane; j < hv; j += 32) d[j] = own ? __ldg(s + j) : make_uint4(0u, 0u, 0u, 0u);
+      if (!own) {
+        for (int j = lane; j < hv; j += 32) d[j] = make_uint4(0u, 0u, 0u, 0u);
+        continue;
+      }
+      // four 16-byte loads in flight per lane before the stores
+      for (int j0 = lane; j0 < hv; j0 += 128) {
+        uint4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (j0 + 32 * u < hv) v[u] = __ldg(s + j0 + 32 * u);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (j0 + 32 * u < hv) d[j0 + 32 * u] = v[u];
+      }
     } else if (own) {
       for (int j = lane; j < hv; j += 32) {
         uint4 a = d[j];

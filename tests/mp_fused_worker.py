@@ -37,9 +37,19 @@ def main():
         report[f"loss_err_{step}"] = float(np.abs(out.loss.double().cpu().numpy() - ref.loss).max())
         report[f"gx_rel_{step}"] = rel_l2(out.grad_x[:, :h].double().cpu().numpy(), ref.grad_x)
         report[f"gw_rel_{step}"] = rel_l2(out.grad_w[0][:, :h].double().cpu().numpy(), ref.grad_w[rb:re])
+    # the input layer's peer pull reads the owners' rows through the IPC mappings
+    tok = torch.from_numpy(np.random.default_rng(5).integers(0, V, 777).astype(np.int64)).cuda()
+    Wfull = torch.from_numpy(np.random.default_rng(6).standard_normal((V, h)).astype(np.float32)).to(
+        torch.bfloat16).cuda()
+    rb, re = vpd.shard_rows(V, world, rank)
+    emb = vm.input_forward_gathered(ctx, tok, vm.EmbeddingShard(Wfull[rb:re], rank, rb, re))
+    ctx.sync()
+    report["input_exact"] = bool(torch.equal(emb, Wfull[tok]))
+    report["peer_input"] = ctx.peer_input_count
     report["fused"] = ctx.fused_c1_count
     report["ok"] = all(report[f"loss_err_{s}"] <= LOSS_ABS and report[f"gx_rel_{s}"] <= GRAD_REL_L2 and
-                       report[f"gw_rel_{s}"] <= GRAD_REL_L2 for s in range(2)) and report["fused"] == 2
+                       report[f"gw_rel_{s}"] <= GRAD_REL_L2 for s in range(2)) and report["fused"] == 2 and \
+        report["input_exact"] and report["peer_input"] == 1
     with open(os.path.join(sys.argv[1], f"rank{rank}.json"), "w") as f:
         json.dump(report, f)
     ctx.close()
