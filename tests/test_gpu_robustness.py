@@ -117,3 +117,34 @@ def test_cooperative_gemms_beside_sm_holding_kernels():
     r = subprocess.run([sys.executable, "-c", STRESS % nsm], capture_output=True, text=True, timeout=600)
     out = r.stdout + r.stderr
     assert r.returncode == 0 and "stress-ok" in out, out[-4000:]
+
+
+FUSED = PRELUDE + (
+    "from paper_2411_05288_b200 import dist as vpd\n"
+    "X, W, g = oracle.random_instance(300, 64, 1600, 1)\n"
+    "Xd = torch.from_numpy(X.astype(np.float32)).to(torch.bfloat16).cuda()\n"
+    "Wd = torch.from_numpy(W.astype(np.float32)).to(torch.bfloat16).cuda()\n"
+    "b = vm.TokenBatch(Xd, torch.from_numpy(g).cuda())\n"
+    "p = 4\n"
+    "ctxs = vpd.local_group(p)\n"
+    "def rank(r, c):\n"
+    "    rb, re = vpd.shard_rows(1600, p, r)\n"
+    "    sh = [vm.EmbeddingShard(Wd[rb:re], r, rb, re)]\n"
+    "    vm.run_alg2(c, b, sh); vm.run_alg1(c, b, sh); vm.run_alg2_chunked(c, b, sh, 128)\n"
+    "    vm.input_forward_gathered(c, b.labels, sh[0])\n"
+    "    c.sync()\n"
+    "    return c.fused_c1_count, c.peer_input_count\n"
+    "res = vpd.run_ranks(ctxs, rank)\n"
+    "assert all(r == (5, 1) for r in res), res\n"
+    "for c in ctxs: c.close()\n"
+    "print('sanitizer-run-ok')\n")
+
+
+def test_fused_exchange_memcheck():
+    # the peer-memory paths (routed dX epilogue, label-row push, owner combine,
+    # copy-engine gather, input peer pull) at ragged sizes under memcheck
+    r = subprocess.run([_sanitizer(), "--tool", "memcheck", sys.executable, "-c", FUSED],
+                       capture_output=True, text=True, timeout=1200)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0 and "sanitizer-run-ok" in out, out[-4000:]
+    assert "ERROR SUMMARY: 0 errors" in out, out[-4000:]
