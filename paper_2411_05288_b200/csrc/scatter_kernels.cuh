@@ -29,6 +29,7 @@
 // chunks) and its sum order is fixed, so the output bits do not.
 #pragma once
 #include <cuda_bf16.h>
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -111,9 +112,13 @@ __global__ void k_sc_fill(const int64_t* __restrict__ tok, int n, int64_t rb, in
 // Orders every repeated row's segment ascending.  c <= 32: one warp, rank by
 // comparison; larger: a bitmap of the n token indices in shared memory
 // (dynamic, ceil(n / 32) words), compacted in order by a block prefix sum.
+__device__ __forceinline__ void sc_sort_segments(int n, const ScatterWs& w, unsigned* sc_bits, int* wsum);
 __global__ void __launch_bounds__(kScThreads) k_sc_sort(int n, ScatterWs w) {
   extern __shared__ unsigned sc_bits[];
   __shared__ int wsum[kScThreads / 32];
+  sc_sort_segments(n, w, sc_bits, wsum);
+}
+__device__ __forceinline__ void sc_sort_segments(int n, const ScatterWs& w, unsigned* sc_bits, int* wsum) {
   const int nw = (n + 31) >> 5;
   const int nrep = w.ctr[kScRep];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -163,6 +168,70 @@ __global__ void __launch_bounds__(kScThreads) k_sc_sort(int n, ScatterWs w) {
     }
     __syncthreads();  // sc_bits / wsum reused by the next segment
   }
+}
+
+// The four planning kernels in one cooperative launch (grid-wide barriers
+// between the phases): zero the per-row state of the rows this batch touches
+// (instead of a memset of every row of the shard), count, plan, fill, sort.
+// The launch gaps and the shard-sized memset were most of the planning time.
+__global__ void __launch_bounds__(kScThreads) k_sc_prepare(const int64_t* __restrict__ tok, int n, int64_t rb,
+                                                         int64_t re, int nchunks, ScatterWs w, int* __restrict__ err,
+                                                         int err_bit) {
+  extern __shared__ unsigned sc_bits[];
+  __shared__ int wsum[kScThreads / 32];
+  cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+  const int t0 = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
+  for (int i = t0; i < n; i += nt) {
+    const int64_t t = tok[i];
+    if (sc_owned(t, rb, re)) {
+      const int r = int(t - rb);
+      w.cnt[r] = 0;
+      w.headr[r] = 0;
+      w.fill[r] = 0;
+    }
+  }
+  if (t0 < kScCtrs) w.ctr[t0] = 0;
+  grid.sync();
+  for (int i = t0; i < n; i += nt) {
+    const int64_t t = tok[i];
+    if (t < 0 && err_bit) atomicOr(err, err_bit);
+    if (sc_owned(t, rb, re)) {
+      const int r = int(t - rb);
+      atomicAdd(w.cnt + r, 1);
+      atomicMax(w.headr + r, n - i);
+    }
+  }
+  grid.sync();
+  for (int i = t0; i < n; i += nt) {
+    const int64_t t = tok[i];
+    if (!sc_owned(t, rb, re)) continue;
+    const int r = int(t - rb);
+    if (n - w.headr[r] != i) continue;
+    const int c = w.cnt[r];
+    if (c == 1) {
+      w.uni[atomicAdd(w.ctr + kScUni, 1)] = make_int2(r, i);
+      continue;
+    }
+    const int s = atomicAdd(w.ctr + kScSeg, c);
+    w.seg[r] = s;
+    w.rep[atomicAdd(w.ctr + kScRep, 1)] = make_int4(r, s, c, 0);
+    if (c < kScHot) {
+      w.small[atomicAdd(w.ctr + kScSmall, 1)] = make_int4(r, s, c, 0);
+    } else {
+      const int b = atomicAdd(w.ctr + kScHotSlots, nchunks);
+      for (int q = 0; q < nchunks && b + q < w.hot_cap; ++q) w.hot[b + q] = make_int4(r, s, c, q);
+    }
+  }
+  grid.sync();
+  for (int i = t0; i < n; i += nt) {
+    const int64_t t = tok[i];
+    if (!sc_owned(t, rb, re)) continue;
+    const int r = int(t - rb);
+    if (w.cnt[r] < 2) continue;
+    w.list[w.seg[r] + atomicAdd(w.fill + r, 1)] = i;
+  }
+  grid.sync();
+  sc_sort_segments(n, w, sc_bits, wsum);
 }
 
 template <typename Src>

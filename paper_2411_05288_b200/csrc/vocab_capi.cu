@@ -429,27 +429,49 @@ void segment_scatter(vp_ctx_s* c, const int64_t* tok, int64_t n, int64_t rb, int
   w.hot = w.rep + n;
   w.uni = reinterpret_cast<int2*>(w.hot + hot_cap);
   w.hot_cap = int(hot_cap);
-  VP_CUDA(cudaMemsetAsync(z, 0, size_t(4 * rows + vp::kScCtrs) * sizeof(int), c->stream));
-  const int g = c->grid_for(n, 256);
-  vp::k_sc_count<<<g, 256, 0, c->stream>>>(tok, int(n), rb, re, w, c->d_err, err_bit);
-  VP_KCHECK();
-  vp::k_sc_plan<<<g, 256, 0, c->stream>>>(tok, int(n), rb, re, nchunks, w);
-  VP_KCHECK();
-  vp::k_sc_fill<<<g, 256, 0, c->stream>>>(tok, int(n), rb, re, w);
-  VP_KCHECK();
   const size_t bits = size_t((n + 31) / 32) * sizeof(unsigned);
   require(bits <= 200 * 1024, "scatter: token count too large for the segment sort");
-  static bool sort_attr = false;
-  if (!sort_attr && bits > 48 * 1024) {
-    VP_CUDA(cudaFuncSetAttribute(vp::k_sc_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    sort_attr = true;
+  if (vp::g_cooperative && bits <= 48 * 1024) {
+    // one cooperative planning kernel (the profilers' kernel replay cannot
+    // relaunch cooperative grids: there the four kernels below run instead)
+    static int coop_blocks[64] = {};
+    int dev = 0;
+    VP_CUDA(cudaGetDevice(&dev));
+    int& per_sm = coop_blocks[dev & 63];
+    if (per_sm == 0) {
+      VP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, vp::k_sc_prepare, vp::kScThreads, 48 * 1024));
+      per_sm = std::max(1, std::min(per_sm, 2));
+    }
+    const int grid = int(std::min<int64_t>(int64_t(c->num_sms) * per_sm, std::max<int64_t>(1, ceil_div(n, 256))));
+    const int64_t* tk = tok;
+    int nn = int(n), nc = nchunks, eb = err_bit;
+    int* errp = c->d_err;
+    void* args[] = {&tk, &nn, &rb, &re, &nc, &w, &errp, &eb};
+    VP_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(vp::k_sc_prepare), dim3(unsigned(grid)),
+                                        dim3(vp::kScThreads), args, bits, c->stream));
+    c->launches += 1;
+  } else {
+    VP_CUDA(cudaMemsetAsync(z, 0, size_t(4 * rows + vp::kScCtrs) * sizeof(int), c->stream));
+    const int g = c->grid_for(n, 256);
+    vp::k_sc_count<<<g, 256, 0, c->stream>>>(tok, int(n), rb, re, w, c->d_err, err_bit);
+    VP_KCHECK();
+    vp::k_sc_plan<<<g, 256, 0, c->stream>>>(tok, int(n), rb, re, nchunks, w);
+    VP_KCHECK();
+    vp::k_sc_fill<<<g, 256, 0, c->stream>>>(tok, int(n), rb, re, w);
+    VP_KCHECK();
+    static bool sort_attr = false;
+    if (!sort_attr && bits > 48 * 1024) {
+      VP_CUDA(cudaFuncSetAttribute(vp::k_sc_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      sort_attr = true;
+    }
+    vp::k_sc_sort<<<c->num_sms * 2, vp::kScThreads, bits, c->stream>>>(int(n), w);
+    VP_KCHECK();
+    c->launches += 4;
   }
-  vp::k_sc_sort<<<c->num_sms * 2, vp::kScThreads, bits, c->stream>>>(int(n), w);
-  VP_KCHECK();
   vp::k_sc_apply<Src><<<unsigned(hot_cap + n), vp::kScThreads, vp::kScRingBytes, c->stream>>>(
       w, src, lds, int(h), sign, dst, ldd, accumulate);
   VP_KCHECK();
-  c->launches += 5;
+  c->launches += 1;
 }
 
 // alg1_pass_S (VM.cpp:151-162): Y = X W_k^T with the fused stats epilogue
