@@ -388,7 +388,7 @@ def _local_and_group(p, T, h, V, seed, opts=(), alg="alg2"):
 
 
 @pytest.mark.parametrize("alg", ["alg2", "alg1"])
-@pytest.mark.parametrize("p,T", [(2, 256), (4, 256), (8, 512), (2, 96), (8, 96), (4, 1000)])
+@pytest.mark.parametrize("p,T", [(2, 256), (4, 256), (8, 512), (2, 96), (8, 96), (4, 1000), (4, 1), (8, 33)])
 def test_fused_c1_has_the_one_gpu_bits(p, T, alg):
     # T = p * R exactly (grad_x gathered in place) and ragged T (owners of
     # 32-row multiples, some ranks owning nothing at T=96, p=8)
