@@ -563,8 +563,10 @@ def run_input(args):
     the input layer forward over the group (vp_input_forward_gathered: at N=1
     the masked 16-byte-vector gather; at N>1 owned rows written into
     peer-mapped buffers and every row pulled from its owner over NVLink) +
-    input_backward (deterministic ascending-i scatter-add, accumulated into the
-    rank's embedding-gradient buffer as in training)."""
+    the group backward (vp_input_backward_gathered: grad_out from rank 0, the
+    first pipeline stage; each rank's deterministic ascending-i scatter-add of
+    the rows its shard owns, accumulated into its embedding-gradient buffer as
+    in training)."""
     import torch
     import torch.distributed as dist
 
@@ -610,7 +612,8 @@ def run_input(args):
         vm.input_forward_gathered(ctx, tok, shard, out=emb)
         if timed:
             ev[1].record(stream)
-        vm.input_backward(ctx, grad, tok, shard, out=dE, accumulate=True)
+        vm.input_backward_gathered(ctx, grad if rank == 0 else None, tok, shard, root=0, h=h, out=dE,
+                                   accumulate=True)
         if timed:
             ev[2].record(stream)
 
@@ -665,7 +668,8 @@ def run_input(args):
                 b = i % 2
                 stream.wait_event(ready[b])
                 vm.input_forward_gathered(ctx, bufs[b][0], shard, out=emb)
-                vm.input_backward(ctx, bufs[b][1], bufs[b][0], shard, out=dE, accumulate=True)
+                vm.input_backward_gathered(ctx, bufs[b][1] if rank == 0 else None, bufs[b][0], shard, root=0,
+                                           h=h, out=dE, accumulate=True)
                 consumed[b].record(stream)
                 out_h.copy_(emb[0], non_blocking=True)
 
@@ -679,7 +683,7 @@ def run_input(args):
         me = max_over_ranks(e0.elapsed_time(e1) / args.steps)
         e2e = {"value": T / (me / 1e3), "unit": "tokens/s", "ms_per_step": me,
                "h2d_bytes_per_step": tok_h.numel() * 8 + grad_h.numel() * 2, "d2h_bytes_per_step": h * 2,
-               "path": "vp_input_forward_gathered / vp_input_backward via ctypes; ids + grad from pinned "
+               "path": "vp_input_forward_gathered / vp_input_backward_gathered via ctypes; ids + grad from pinned "
                        "host (double-buffered on a copy stream, overlapping the previous step)"}
     if rank != 0:
         ctx.close()

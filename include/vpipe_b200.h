@@ -165,8 +165,9 @@ int64_t vp_ctx_launch_count(vp_ctx_t ctx);
 /* Number of fused C1 exchanges (option "fused_c1") this context has run;
  * -1 for a null context (evidence counter). */
 int64_t vp_ctx_fused_c1_count(vp_ctx_t ctx);
-/* Number of vp_input_forward_gathered calls that took the peer-pull path
- * (option "peer_input"); -1 for a null context (evidence counter). */
+/* Number of vp_input_forward_gathered / vp_input_backward_gathered calls that
+ * took the peer-memory path (option "peer_input"); -1 for a null context
+ * (evidence counter). */
 int64_t vp_ctx_peer_input_count(vp_ctx_t ctx);
 /* Per-GEMM CUDA-event timing on the launching stream.  Returns (and resets)
  * the accumulated milliseconds / launch counts per GEMM kind since the last
@@ -291,11 +292,12 @@ int vp_input_backward(vp_ctx_t ctx, const void* grad_out, int64_t ldg, int grad_
 /* The input layer's forward over the whole group without the zero-padded
  * all-reduce: every rank gets out[i] = W[tok_i] (a zero row when no shard owns
  * tok_i), i.e. input_forward summed over the shards (VM.cpp:227-236 +
- * R/PAPER.md:582), by an owner gather: ranks pack the rows they own and
- * exchange only those in one grouped broadcast per rank (about half the bytes
- * of the sum all-reduce; pure copies, bit-exact).  Synchronises the context
- * stream once (block sizes to the host); not capturable.  One rank: equals
- * vp_input_forward. */
+ * R/PAPER.md:582).  Default (option "peer_input"): owned rows are written at
+ * their token index into peer-mapped buffers and every rank pulls each row
+ * from its owner (about half the bytes of the sum all-reduce; capturable after
+ * the first call).  Fallback: ranks pack the rows they own and exchange them in
+ * one grouped broadcast per rank (synchronises the stream once; not
+ * capturable).  Pure copies, bit-exact.  One rank: equals vp_input_forward. */
 int vp_input_forward_gathered(vp_ctx_t ctx, const int64_t* tokens, int64_t n_tok, int64_t h,
                               const vp_shard_t* shard, void* out, int64_t ldo);
 /* The input layer's pre-backward broadcast (R/PAPER.md:582): grad_out of the
@@ -303,6 +305,18 @@ int vp_input_forward_gathered(vp_ctx_t ctx, const int64_t* tokens, int64_t n_tok
  * rank `root` to every rank of the group.  No-op without a group. */
 int vp_input_grad_broadcast(vp_ctx_t ctx, void* grad_out, int64_t ldg, int grad_is_f32, int64_t n_tok, int64_t h,
                             int root);
+/* The input layer's backward over the whole group: vp_input_grad_broadcast
+ * from `root` followed by vp_input_backward of this rank's shard, without
+ * sending every rank the whole gradient.  grad_out is read on `root` only
+ * (other ranks may pass NULL).  Default (option "peer_input"): root stages
+ * grad_out in a peer-mapped buffer and each rank's ordered scatter reads just
+ * the rows of the tokens its shard owns over NVLink (about 1/N of the
+ * gradient per rank instead of all of it); fallback: the broadcast into a
+ * context buffer.  Same bits as broadcast + input_backward.  One rank: equals
+ * vp_input_backward. */
+int vp_input_backward_gathered(vp_ctx_t ctx, const void* grad_out, int64_t ldg, int grad_is_f32,
+                               const int64_t* tokens, int64_t n_tok, int64_t h, const vp_shard_t* shard,
+                               float* grad_w, int64_t ldgw, int accumulate, int root);
 /* In-place sum all-reduce over the context's NCCL group (the input layer's
  * post-forward all-reduce, R/PAPER.md:582).  dtype 0 = fp32, 1 = bf16. */
 int vp_allreduce_sum(vp_ctx_t ctx, void* buf, int64_t count, int dtype);

@@ -90,6 +90,8 @@ SIGNATURES = {
     "vp_input_forward_gathered": (c_int, [c_void_p, c_void_p, c_int64, c_int64, POINTER(vp_shard_t), c_void_p,
                                           c_int64]),
     "vp_input_grad_broadcast": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_int64, c_int64, c_int]),
+    "vp_input_backward_gathered": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_void_p, c_int64, c_int64, c_void_p,
+                                           c_void_p, c_int64, c_int, c_int]),
     "vp_input_backward": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_void_p, c_int64, c_int64,
                                   POINTER(vp_shard_t), c_void_p, c_int64, c_int]),
     "vp_allreduce_sum": (c_int, [c_void_p, c_void_p, c_int64, c_int]),

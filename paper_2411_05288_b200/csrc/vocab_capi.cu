@@ -179,7 +179,7 @@ struct vp_ctx_s {
   double gemm_ms[4] = {0, 0, 0, 0};
   int64_t gemm_n[4] = {0, 0, 0, 0};
   // workspace
-  DevBuf inv, scale, xs, gathered, packed, tmp_m, tmp_s, heads, counts, vtmp;
+  DevBuf inv, scale, xs, gathered, packed, tmp_m, tmp_s, heads, counts, vtmp, gbuf;
 
   void activate() const {
     VP_CUDA(cudaSetDevice(device));
@@ -209,6 +209,8 @@ struct vp_ctx_s {
   int64_t fused_count = 0;
   SymBuf sym;     // output layer (slots, B, G)
   SymBuf in_sym;  // input layer: owned rows by token index, two halves (call parity)
+  SymBuf bwd_sym; // input backward: root's staged gradient, two halves (call parity)
+  int64_t bwd_calls = 0;
   bool peer_input = true;  // option "peer_input": the input forward pulls rows over peer memory
   int64_t in_calls = 0, peer_input_count = 0;
   DevBuf bar;                 // one float: group barriers of the fused exchange
@@ -1378,7 +1380,7 @@ int vp_ctx_destroy(vp_ctx_t c) {
     if (!c) return;
     c->activate();
     cudaStreamSynchronize(c->stream);
-    for (SymBuf* sb : {&c->sym, &c->in_sym}) {
+    for (SymBuf* sb : {&c->sym, &c->in_sym, &c->bwd_sym}) {
       if (c->comm) {
         c->comm->close_peers(sb->peers);
         for (auto& r : sb->retired) c->comm->close_peers(r.second);
@@ -1394,7 +1396,7 @@ int vp_ctx_destroy(vp_ctx_t c) {
     if (c->ev_done) cudaEventDestroy(c->ev_done);
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
     for (DevBuf* b : {&c->inv, &c->scale, &c->xs, &c->gathered, &c->packed, &c->tmp_m, &c->tmp_s,
-                      &c->heads, &c->counts})
+                      &c->heads, &c->counts, &c->vtmp, &c->gbuf})
       b->release();
     if (c->d_err) cudaFree(c->d_err);
     if (c->split.flags) cudaFree(c->split.flags);
@@ -2137,6 +2139,67 @@ int vp_input_forward_gathered(vp_ctx_t c, const int64_t* tokens, int64_t n_tok, 
 
 // The input layer's pre-backward broadcast (R/PAPER.md:582): grad_out of the
 // embedding output, produced on one rank, to every vocabulary shard.
+int vp_input_backward_gathered(vp_ctx_t c, const void* grad, int64_t ldg, int grad_is_f32, const int64_t* tokens,
+                               int64_t n_tok, int64_t h, const vp_shard_t* s, float* gw, int64_t ldgw, int accumulate,
+                               int root) {
+  return api([&] {
+    require(c != nullptr && gw != nullptr && tokens != nullptr, "input_backward: null argument");
+    require(n_tok >= 0, "input_backward: grad/token length mismatch");
+    check_shard(s, h);
+    const bool dist = c->distributed();
+    require(!dist || (root >= 0 && root < c->nranks), "input_backward_gathered: root out of range");
+    const bool has_grad = !dist || c->rank == root;
+    require(!has_grad || grad != nullptr, "input_backward: null argument");
+    require(h % 8 == 0 && ldg >= h && ldg % 8 == 0 && ldgw >= h && ldgw % 4 == 0 && aligned16(gw) &&
+                (!has_grad || aligned16(grad)),
+            "input_backward: h/ld must be multiples of 8");
+    c->activate();
+    NvtxRange nr("vp:input_backward(group)");
+    const int64_t rows = s->row_end - s->row_begin;
+    if (!accumulate)
+      VP_CUDA(cudaMemset2DAsync(gw, size_t(ldgw) * sizeof(float), 0, size_t(h) * sizeof(float), size_t(rows),
+                                c->stream));
+    if (n_tok == 0) return;
+    require(n_tok < (int64_t(1) << 31), "input_backward_gathered: too many tokens");
+    const size_t esz = grad_is_f32 ? 4 : 2;
+    auto scatter = [&](const void* src, int64_t lds) {
+      if (grad_is_f32)
+        segment_scatter(c, tokens, n_tok, s->row_begin, s->row_end, static_cast<const float*>(src), lds, h, 1.f, gw,
+                        ldgw, 1, kErrInputBwd);
+      else
+        segment_scatter(c, tokens, n_tok, s->row_begin, s->row_end, static_cast<const __nv_bfloat16*>(src), lds, h,
+                        1.f, gw, ldgw, 1, kErrInputBwd);
+    };
+    if (!dist) {
+      scatter(grad, ldg);
+      return;
+    }
+    const size_t dense = size_t(n_tok) * size_t(h) * esz;
+    if (c->peer_input && c->nranks <= vp::kMaxRoute && !c->bwd_sym.failed &&
+        ensure_sym(c, c->bwd_sym, 2 * size_t(round_up(int64_t(dense), 256)))) {
+      // root stages grad_out (dense rows) in half `par` of its buffer; after a
+      // barrier every rank's scatter reads its owned tokens' rows from there
+      const size_t half = c->bwd_sym.bytes / 2 / 256 * 256;
+      const size_t off = size_t(c->bwd_calls++ & 1) * half;
+      if (c->rank == root)
+        VP_CUDA(cudaMemcpy2DAsync(static_cast<char*>(c->bwd_sym.p) + off, size_t(h) * esz, grad, size_t(ldg) * esz,
+                                  size_t(h) * esz, size_t(n_tok), cudaMemcpyDeviceToDevice, c->stream));
+      group_barrier(c);
+      scatter(static_cast<const char*>(c->bwd_sym.peers[size_t(root)]) + off, h);
+      ++c->peer_input_count;
+      return;
+    }
+    // fallback: the whole gradient broadcast into a context buffer
+    void* buf = c->buf<char>(c->gbuf, dense);
+    if (c->rank == root)
+      VP_CUDA(cudaMemcpy2DAsync(buf, size_t(h) * esz, grad, size_t(ldg) * esz, size_t(h) * esz, size_t(n_tok),
+                                cudaMemcpyDeviceToDevice, c->stream));
+    c->cm().broadcast(buf, buf, size_t(n_tok) * size_t(h), grad_is_f32 ? vp::DType::F32 : vp::DType::BF16, root,
+                      c->stream);
+    scatter(buf, h);
+  });
+}
+
 int vp_input_grad_broadcast(vp_ctx_t c, void* grad, int64_t ldg, int grad_is_f32, int64_t n_tok, int64_t h,
                             int root) {
   return api([&] {

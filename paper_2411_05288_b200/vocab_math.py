@@ -557,6 +557,34 @@ def input_backward(ctx: Context, grad_out: torch.Tensor, tokens: torch.Tensor, s
     return out
 
 
+def input_backward_gathered(ctx: Context, grad_out: Optional[torch.Tensor], tokens: torch.Tensor,
+                            shard: EmbeddingShard, root: int, h: Optional[int] = None,
+                            grad_is_f32: bool = False, out: Optional[torch.Tensor] = None,
+                            accumulate: bool = False) -> torch.Tensor:
+    """input_grad_broadcast from `root` + input_backward of this rank's shard
+    (vp_input_backward_gathered): grad_out [n_tok, h] is read on `root` only
+    (None elsewhere); each rank reads just the rows its shard owns."""
+    _need_cuda(tokens, torch.int64, "input_backward tokens")
+    n = tokens.numel()
+    if grad_out is not None:
+        if grad_out.shape[0] != n:
+            raise ValueError("input_backward: grad/token length mismatch")
+        if grad_out.dtype not in (torch.bfloat16, torch.float32):
+            raise ValueError("input_backward: grad_out must be bf16 or fp32")
+        h = grad_out.shape[1]
+        grad_is_f32 = grad_out.dtype == torch.float32
+        ldg = grad_out.stride(0)
+    else:
+        h = h if h is not None else shard.W.shape[1]
+        ldg = h
+    if out is None:
+        out = torch.empty(shard.rows(), h, dtype=torch.float32, device=_dev(ctx))
+    s = shard.c()
+    check(ctx.lib.vp_input_backward_gathered(ctx.handle, _p(grad_out), ldg, int(grad_is_f32), _p(tokens), n, h,
+                                             ctypes.byref(s), _p(out), out.stride(0), int(accumulate), int(root)))
+    return out
+
+
 def allreduce_sum(ctx: Context, t: torch.Tensor) -> torch.Tensor:
     """In-place sum over the context's NCCL group (no-op without one)."""
     if t.dtype not in (torch.float32, torch.bfloat16):

@@ -227,7 +227,11 @@ def test_input_layer_owner_gather_and_grad_broadcast(p, ids, peer):
         g = grad.clone() if r == p - 1 else torch.zeros_like(grad)
         vm.input_grad_broadcast(ctx, g, root=p - 1)
         dE = vm.input_backward(ctx, g[:-5], tok[:-5], sh)
+        # broadcast + backward in one call: grad_out on the root only
+        dE2 = vm.input_backward_gathered(ctx, grad[:-5] if r == p - 1 else None, tok[:-5], sh, root=p - 1, h=h,
+                                         grad_is_f32=True)
         ctx.sync()
+        assert torch.equal(dE2, dE), r
         return out, g, dE
 
     outs = vpd.run_ranks(ctxs, rank)
@@ -239,7 +243,7 @@ def test_input_layer_owner_gather_and_grad_broadcast(p, ids, peer):
         assert torch.equal(g, grad), r
         rb, re = vpd.shard_rows(V, p, r)
         assert np.array_equal(dE.cpu().numpy(), oracle.input_backward_f32(g_np, t[:-5], re - rb, rb)), r
-    assert [c.peer_input_count for c in ctxs] == [peer] * p
+    assert [c.peer_input_count for c in ctxs] == [2 * peer] * p  # the forward and the gathered backward
     _close(ctxs)
 
 
