@@ -64,6 +64,15 @@ def test_null_and_shape_errors_map_to_einval():
         _lib.check(lib.vp_ctx_set_option(None, b"cta_group", 2))
 
 
+def test_peer_memory_entry_points_reject_a_null_context():
+    # the exchange counters and the group backward (vp_input_backward_gathered)
+    lib = _lib.load()
+    assert lib.vp_ctx_fused_c1_count(None) == -1
+    assert lib.vp_ctx_peer_input_count(None) == -1
+    rc = lib.vp_input_backward_gathered(None, None, 8, 0, None, 4, 8, None, None, 8, 0, 0)
+    assert rc == _lib.VP_EINVAL and b"null argument" in lib.vp_last_error()
+
+
 def test_shard_weights_views_and_errors():
     W = torch.arange(12 * 8, dtype=torch.float32).reshape(12, 8).to(torch.bfloat16)
     shards = vm.shard_weights(W, 3)
