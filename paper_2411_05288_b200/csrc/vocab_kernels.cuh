@@ -87,18 +87,33 @@ __global__ void __launch_bounds__(512) k_stats_reduce_ref(const float* __restric
   float m = -INFINITY, S = 0.f, R = 0.f;
   if (row < n) {
     R = row_ref[row];
-#pragma unroll 4
-    for (int j = w; j < ntiles; j += W) {
-      const int64_t o = int64_t(j) * ld + row;
-      const float mj = tile_m[o], sj = tile_s[o], qj = tile_q[o];
-      m = fmaxf(m, mj);
-      if (qj == R) {
-        S += sj;
-      } else if (qj < R) {
-        S += sj * expf(qj - R);
-      } else {
-        S = S * expf(R - qj) + sj;
-        R = qj;
+    // batches of kB tiles: all 3 x kB loads issued before the (order-fixed)
+    // merge consumes them, so a warp keeps 3 x kB x 128 B in flight
+    constexpr int kB = 8;
+    for (int j0 = w; j0 < ntiles; j0 += W * kB) {
+      float mj[kB], sj[kB], qj[kB];
+#pragma unroll
+      for (int u = 0; u < kB; ++u) {
+        const int j = j0 + u * W;
+        if (j < ntiles) {
+          const int64_t o = int64_t(j) * ld + row;
+          mj[u] = tile_m[o];
+          sj[u] = tile_s[o];
+          qj[u] = tile_q[o];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kB; ++u) {
+        if (j0 + u * W >= ntiles) break;
+        m = fmaxf(m, mj[u]);
+        if (qj[u] == R) {
+          S += sj[u];
+        } else if (qj[u] < R) {
+          S += sj[u] * expf(qj[u] - R);
+        } else {
+          S = S * expf(R - qj[u]) + sj[u];
+          R = qj[u];
+        }
       }
     }
   }
