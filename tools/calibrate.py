@@ -87,17 +87,28 @@ def main():
     bw = a.busbw * 1e9
     ar = lambda nbytes: 2.0 * (p - 1) / p * nbytes / bw * 1e3  # noqa: E731  ring all-reduce, ms
     ag = lambda nbytes: (p - 1) / p * nbytes * p / bw * 1e3  # noqa: E731   all-gather of nbytes per rank
+    # fused exchange (default): the dX partials reach their owners inside the dX
+    # GEMM's epilogue (pass S, NVLink traffic overlapped with the MMAs); the
+    # barrier's critical path is the stats all-gather, the owner combine and the
+    # loss all-reduce; the grad_x pull by the copy engines ((p-1)/p of T x h fp32
+    # per rank) runs beside pass T and only shows if it outlasts it
+    nvl = a.busbw * 1e9 * 1.2  # point-to-point copy-engine pulls: no ring overhead (assumed)
+    pull = (p - 1) / p * 4 * T * h / nvl * 1e3
     coll = {
         "C0_broadcast_X_ms": T * h * 2 / bw * 1e3,
-        "alg2_C1_ms": meas["alg2_C1_local"] + ag(8 * T) + ar(4 * T * h) + ar(4 * T),
+        "alg2_C1_ms_allreduce": meas["alg2_C1_local"] + ag(8 * T) + ar(4 * T * h) + ar(4 * T),
+        "alg2_C1_ms": meas["alg2_C1_local"] + ag(8 * T) + ar(4 * T) + max(0.0, pull - meas["alg2_T"]),
+        "alg2_gather_pull_ms_beside_T": pull,
         "alg1_C1_ms": meas["alg1_C1_local"] + ag(8 * T),
         "alg1_C2_ms": ar(4 * T * h),
+        "alg1_C2_ms_fused": meas["alg2_C1_local"] + pull,
     }
     unit_rate = 3.0 * R * 1e-3  # flops per ms, x3: the simulator's table-unit convention
     sched = os.path.join(ROOT, "oracle", "_ref", "vpipe_sched")
     sims = {}
     for method, S, Tt, C in (("vocab2", meas["alg2_S"], meas["alg2_T"], coll["alg2_C1_ms"]),
-                             ("vocab1", meas["alg1_S"], meas["alg1_T"], max(coll["alg1_C1_ms"], coll["alg1_C2_ms"]))):
+                             ("vocab1", meas["alg1_S"], meas["alg1_T"],
+                              max(coll["alg1_C1_ms"], coll["alg1_C2_ms_fused"]))):
         if os.path.exists(sched):
             r = subprocess.run([sched, "simulate", method, "1", str(T), str(h), str(V), str(a.layers), str(p),
                                 str(a.microbatches), repr(unit_rate), repr(S), repr(Tt), repr(C)],
