@@ -88,6 +88,14 @@ void* vp_ctx_get_stream(vp_ctx_t ctx);
 int vp_ctx_sync(vp_ctx_t ctx);
 /* Pre-size the workspace for up to n_tok tokens, hidden h, p exchange parts. */
 int vp_ctx_reserve(vp_ctx_t ctx, int64_t n_tok, int64_t h, int p);
+/* Device memory plan for one rank (no GPU needed): bytes of one shard state
+ * (vp_state_create: P, tile stats, A), of the context workspace at that shape
+ * (after vp_ctx_reserve and the first input/output calls), and of the peer
+ * buffers of the fused exchanges in a group of nranks > 1 (0 otherwise).
+ * Any output pointer may be NULL.  For sizing shards and microbatches against
+ * the 180 GB of HBM3e (SURVEY.md §8b "vp_workspace_query"). */
+int vp_workspace_query(int64_t n_tok, int64_t h, int64_t rows, int nranks, int64_t* state_bytes,
+                       int64_t* ctx_bytes, int64_t* peer_bytes);
 /* Options: "cta_group" (1 or 2, default 2), "gemm_sms" (SMs used by GEMMs),
  * "raster_{logits,dx,dw}" (tile order, see GemmGeom::raster),
  * "policy_{logits,dx,dw}" (TMA L2 policy of both operands: -1 per-epilogue default,

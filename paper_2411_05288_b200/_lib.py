@@ -44,6 +44,8 @@ SIGNATURES = {
     "vp_ctx_launch_count": (c_int64, [c_void_p]),
     "vp_ctx_fused_c1_count": (c_int64, [c_void_p]),
     "vp_ctx_peer_input_count": (c_int64, [c_void_p]),
+    "vp_workspace_query": (c_int, [c_int64, c_int64, c_int64, c_int, POINTER(c_int64), POINTER(c_int64),
+                                   POINTER(c_int64)]),
     "vp_debug_occupy_sms": (c_int, [c_void_p, c_void_p, c_int, c_int64]),
     "vp_ctx_set_logit_shift": (c_int, [c_void_p, c_void_p]),
     "vp_shard_logits": (c_int, [c_void_p, POINTER(vp_batch_t), POINTER(vp_shard_t), c_void_p, c_int64]),

@@ -247,6 +247,18 @@ struct vp_state_s {
 
 namespace {
 
+// Bytes vp_state_create allocates for one shard state (P, tile stats, per-row
+// arrays, overflow fix lists); vp_workspace_query reports the same figure.
+int64_t state_bytes(int64_t n_tok, int64_t h, int64_t rows) {
+  const int64_t ldp = round_up(rows, 64), ntiles = ceil_div(rows, vp::kTileN), nblk = ceil_div(n_tok, 128) + 2;
+  return n_tok * ldp * 2                         // P (bf16)
+         + 3 * ntiles * n_tok * 4                // tile m, s, q
+         + 6 * n_tok * 4                         // m', sum', y_tgt, row_ref, cfac, row_bad
+         + n_tok * 4 + nblk * 4 + 2 * 4          // bad_list, ref_flag, counters
+         + ceil_div(n_tok, 32) * ntiles * 8      // fix_list
+         + n_tok * h * 4;                        // A (alg2) / dX partial
+}
+
 void free_state_buffers(vp_state_s* st) {
   for (void* p : {static_cast<void*>(st->P), static_cast<void*>(st->tile_m), static_cast<void*>(st->tile_s),
                   static_cast<void*>(st->m_loc), static_cast<void*>(st->s_loc), static_cast<void*>(st->ytgt),
@@ -1428,6 +1440,31 @@ int vp_ctx_sync(vp_ctx_t c) {
       if (err & kErrLabel) throw std::invalid_argument("TokenBatch: label out of range");
       if (err & kErrInputFwd) throw std::invalid_argument("input_forward: token out of range");
       throw std::invalid_argument("input_backward: token out of range");
+    }
+  });
+}
+
+int vp_workspace_query(int64_t n_tok, int64_t h, int64_t rows, int nranks, int64_t* state_b, int64_t* ctx_b,
+                       int64_t* peer_b) {
+  return api([&] {
+    require(n_tok >= 1 && h >= 1 && rows >= 1 && nranks >= 1, "vp_workspace_query: empty shape");
+    if (state_b) *state_b = state_bytes(n_tok, h, rows);
+    if (ctx_b) {
+      const int64_t nchunks = ceil_div(h, vp::kScChunk), hot_cap = ceil_div(n_tok, vp::kScHot) * nchunks;
+      const int64_t fixed = (int64_t(1) << 20) * 4                         // lockstep counters
+                            + 2 * (int64_t(1) << 14) * 4                   // split-K flags
+                            + (int64_t(148 / 2 + 2) * 256 * 512 + (1 << 16)) * 4;  // split-K workspace
+      *ctx_b = fixed + 4 * n_tok * 4 + n_tok * h * 2 + 2 * n_tok * 4 + 2 * n_tok * nranks * 4  // reserve()
+               + (4 * rows + vp::kScCtrs) * 4 + (11 * n_tok + 4 * hot_cap + 4) * 4;           // scatter
+    }
+    if (peer_b) {
+      *peer_b = 0;
+      if (nranks > 1) {  // fused exchange (output layer) + input-layer peer buffers
+        const int64_t R = round_up(ceil_div(n_tok, nranks), 32), rowf = R * h;
+        const int64_t out = round_up(int64_t(nranks) * rowf * 4 + round_up(rowf * 2, 256) + rowf * 4, 256);
+        const int64_t inl = 2 * round_up(n_tok * h * 2, 256);
+        *peer_b = round_up(out, int64_t(2) << 20) + 2 * round_up(inl, int64_t(2) << 20);
+      }
     }
   });
 }

@@ -585,6 +585,15 @@ def input_backward_gathered(ctx: Context, grad_out: Optional[torch.Tensor], toke
     return out
 
 
+def workspace_query(n_tok: int, h: int, rows: int, nranks: int = 1) -> dict:
+    """Device memory plan of one rank (vp_workspace_query; no GPU needed):
+    bytes of one shard state, of the context workspace and of the peer
+    buffers of the fused exchanges."""
+    a, b, c = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+    check(_lib.load().vp_workspace_query(n_tok, h, rows, nranks, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)))
+    return {"state_bytes": a.value, "ctx_bytes": b.value, "peer_bytes": c.value}
+
+
 def allreduce_sum(ctx: Context, t: torch.Tensor) -> torch.Tensor:
     """In-place sum over the context's NCCL group (no-op without one)."""
     if t.dtype not in (torch.float32, torch.bfloat16):

@@ -73,6 +73,24 @@ def test_peer_memory_entry_points_reject_a_null_context():
     assert rc == _lib.VP_EINVAL and b"null argument" in lib.vp_last_error()
 
 
+def test_workspace_query_plans_the_headline_and_an_8_way_shard():
+    # host-only memory plan (vp_workspace_query): P dominates a shard state
+    T, h, V = 8192, 4096, 256000
+    one = vm.workspace_query(T, h, V, 1)
+    P = T * V * 2
+    stats = 3 * (V // 128) * T * 4
+    A = T * h * 4
+    assert P + stats + A <= one["state_bytes"] <= P + stats + A + 8 * 2**20  # + per-row arrays, fix lists
+    assert one["peer_bytes"] == 0 and one["ctx_bytes"] > T * h * 2
+    eight = vm.workspace_query(T, h, V // 8, 8)
+    assert eight["state_bytes"] < one["state_bytes"] // 6
+    assert eight["peer_bytes"] >= 8 * (T // 8) * h * 4  # slots of the fused exchange
+    total = eight["state_bytes"] + eight["ctx_bytes"] + eight["peer_bytes"]
+    assert total < 4 * 2**30  # an 8-way shard of the headline fits in a few GB of the 180 GB
+    lib = _lib.load()
+    assert lib.vp_workspace_query(0, h, V, 1, None, None, None) == _lib.VP_EINVAL
+
+
 def test_shard_weights_views_and_errors():
     W = torch.arange(12 * 8, dtype=torch.float32).reshape(12, 8).to(torch.bfloat16)
     shards = vm.shard_weights(W, 3)
