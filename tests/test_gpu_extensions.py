@@ -132,3 +132,18 @@ def test_tied_embeddings_step_matches_the_oracle(p, ws):
     assert rel_l2(diff, dE) <= 1e-5
     assert np.abs(out.loss.double().cpu().numpy() - ref.loss).max() <= LOSS_ABS
     tctx.close()
+
+
+def test_workspace_query_matches_the_state_allocation(ctx):
+    # vp_workspace_query's shard-state figure against what vp_state_create
+    # actually takes from the device (cudaMalloc granularity: a few MB)
+    import torch
+    T, h, rows = 4096, 4096, 64000
+    plan = vm.workspace_query(T, h, rows, 1)
+    torch.cuda.synchronize()
+    free0 = torch.cuda.mem_get_info()[0]
+    st = vm.ShardState(ctx, T, h, rows)
+    torch.cuda.synchronize()
+    used = free0 - torch.cuda.mem_get_info()[0]
+    assert abs(used - plan["state_bytes"]) <= 32 * 2**20, (used, plan)
+    st.close()
