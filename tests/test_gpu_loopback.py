@@ -489,3 +489,20 @@ def test_fused_c1_across_processes(tmp_path):
     reps = [json.load(open(tmp_path / f"rank{k}.json")) for k in range(2)]
     for rep in reps:
         assert rep["ok"], rep
+
+
+@pytest.mark.parametrize("alg", ["alg2", "alg1"])
+def test_fused_exchange_llama_vocab_8_ranks(alg):
+    # the Llama-3 vocabulary over 8 ranks (ragged 16032-row shards, 251
+    # k-blocks of dX per rank) through the fused exchange: the one-GPU bits
+    p, T, h, V = 8, 2048, 512, 128256
+    opts = (("splits_dx", 1), ("splits_dw", 1))
+    Xb, Wb, g, local, local_ctx, ctxs, outs = _local_and_group(p, T, h, V, 77, opts, alg)
+    assert [c.fused_c1_count for c in ctxs] == [1] * p
+    for o in outs:
+        assert torch.equal(o.loss, local.loss) and torch.equal(o.grad_x, local.grad_x)
+    assert torch.equal(torch.cat([o.grad_w[0] for o in outs]), local.grad_w_full())
+    ref = oracle.oracle_output_layer(Xb[:256], g[:256], Wb, want_softmax=False)
+    assert np.abs(outs[0].loss[:256].double().cpu().numpy() - ref.loss).max() <= LOSS_ABS
+    _close(ctxs)
+    local_ctx.close()
