@@ -506,3 +506,25 @@ def test_fused_exchange_llama_vocab_8_ranks(alg):
     assert np.abs(outs[0].loss[:256].double().cpu().numpy() - ref.loss).max() <= LOSS_ABS
     _close(ctxs)
     local_ctx.close()
+
+
+def test_fused_exchange_random_shapes():
+    # seeded random shapes (token counts, hidden sizes that are multiples of 8
+    # but not of the 32-column store box, vocabularies with ragged shards):
+    # fused group == one-GPU p-shard run, bit for bit
+    rng = np.random.default_rng(2024)
+    for case in range(10):
+        p = int(rng.integers(2, 9))
+        T = int(rng.integers(1, 700))
+        h = int(8 * rng.integers(1, 40))
+        V = int(p * rng.integers(40, 900))
+        alg = "alg2" if case % 3 else "alg1"
+        opts = (("splits_dx", 1), ("splits_dw", 1))
+        Xb, Wb, g, local, local_ctx, ctxs, outs = _local_and_group(p, T, h, V, 500 + case, opts, alg)
+        tag = (case, p, T, h, V, alg)
+        assert [c.fused_c1_count for c in ctxs] == [1] * p, tag
+        for o in outs:
+            assert torch.equal(o.loss, local.loss) and torch.equal(o.grad_x, local.grad_x), tag
+        assert torch.equal(torch.cat([o.grad_w[0] for o in outs]), local.grad_w_full()), tag
+        _close(ctxs)
+        local_ctx.close()
