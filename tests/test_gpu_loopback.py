@@ -528,3 +528,41 @@ def test_fused_exchange_random_shapes():
         assert torch.equal(torch.cat([o.grad_w[0] for o in outs]), local.grad_w_full()), tag
         _close(ctxs)
         local_ctx.close()
+
+
+def test_input_peer_paths_random_shapes():
+    # seeded random input-layer shapes through the peer-memory forward and the
+    # gathered backward: bit-equal to W[tok] and to the ascending-i oracle
+    rng = np.random.default_rng(99)
+    for case in range(8):
+        p = int(rng.integers(2, 9))
+        T = int(rng.integers(1, 3000))
+        h = int(8 * rng.integers(1, 64))
+        V = int(p * rng.integers(10, 400))
+        W = torch.from_numpy(rng.standard_normal((V, h)).astype(np.float32)).to(torch.bfloat16).cuda()
+        t = rng.integers(0, V + 7, T)  # a few ids past V: zero rows, ignored by the backward
+        tok = torch.from_numpy(t.astype(np.int64)).cuda()
+        grad = torch.from_numpy(rng.standard_normal((T, h)).astype(np.float32)).to(torch.bfloat16).cuda()
+        root = int(rng.integers(0, p))
+        torch.cuda.synchronize()
+        ctxs = vpd.local_group(p)
+
+        def rank(r, ctx):
+            sh = _shard(W, p, r)
+            out = vm.input_forward_gathered(ctx, tok, sh)
+            dE = vm.input_backward_gathered(ctx, grad if r == root else None, tok, sh, root=root, h=h)
+            ctx.sync()
+            return out, dE
+
+        res = vpd.run_ranks(ctxs, rank)
+        want = torch.zeros(T, h, dtype=torch.bfloat16, device="cuda")
+        own = tok < V
+        want[own] = W[tok[own]]
+        g_np = grad.float().cpu().numpy()
+        for r, (out, dE) in enumerate(res):
+            assert torch.equal(out, want), (case, r)
+            rb, re = vpd.shard_rows(V, p, r)
+            ref = oracle.input_backward_f32(g_np, t, re - rb, rb)
+            assert np.array_equal(dE.cpu().numpy(), ref), (case, r)
+        assert [c.peer_input_count for c in ctxs] == [2] * p
+        _close(ctxs)
