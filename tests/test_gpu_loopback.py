@@ -566,3 +566,72 @@ def test_input_peer_paths_random_shapes():
             assert np.array_equal(dE.cpu().numpy(), ref), (case, r)
         assert [c.peer_input_count for c in ctxs] == [2] * p
         _close(ctxs)
+
+
+@pytest.mark.parametrize("alg", ["alg2", "alg1"])
+def test_fused_exchange_fault_scale(alg):
+    # the reference's fault hook (sum scaled after the merge, VM.cpp:314 /
+    # :337-350) through the fused exchange: the one-GPU bits with the same fault
+    p, T, h, V = 4, 200, 64, 2000
+    fn = {"alg1": vm.run_alg1, "alg2": vm.run_alg2}[alg]
+    X, W, g = oracle.random_instance(T, h, V, 13)
+    _, _, batch, Wd = device_case(X, W, g)
+    lctx = vm.Context(0)
+    for k, v in (("splits_dx", 1), ("splits_dw", 1)):
+        lctx.set_option(k, v)
+    local = fn(lctx, batch, vm.shard_weights(Wd, p), fault_scale=1.5)
+    lctx.sync()
+    torch.cuda.synchronize()
+    ctxs = vpd.local_group(p)
+    for c in ctxs:
+        c.set_option("splits_dx", 1)
+        c.set_option("splits_dw", 1)
+    outs = vpd.run_ranks(ctxs, lambda r, c: fn(c, batch, [_shard(Wd, p, r)], fault_scale=1.5))
+    for c in ctxs:
+        c.sync()
+    assert [c.fused_c1_count for c in ctxs] == [1] * p
+    for o in outs:
+        assert torch.equal(o.loss, local.loss) and torch.equal(o.grad_x, local.grad_x)
+    assert torch.equal(torch.cat([o.grad_w[0] for o in outs]), local.grad_w_full())
+    _close(ctxs)
+    lctx.close()
+
+
+def test_executor_fused_microbatches_of_different_lengths():
+    # one peer region per microbatch sized for the longest; ragged lengths
+    import json
+    golden = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "programs.json")))
+    prog = vm.Program(golden["vocab2_p4_n8"]["text"])
+    p, n = prog.p, prog.n
+    h, V = 64, 96 * p
+    lens = [48, 100, 17, 64, 200, 33, 96, 1][:n]
+    W = None
+    mbs = []
+    for i in range(n):
+        X, W_i, g = oracle.random_instance(lens[i], h, V, 300 + i)
+        W = W_i if W is None else W
+        mbs.append(device_case(X, W, g))
+    Wd = mbs[0][3]
+    lctx = vm.Context(0)
+    local = vm.run_program(lctx, prog, [m[2] for m in mbs], vm.shard_weights(Wd, p))
+    lctx.sync()
+    torch.cuda.synchronize()
+    ctxs = vpd.local_group(p)
+
+    def rank(r, ctx):
+        batches = [vm.TokenBatch(m[2].X.clone() if r == p - 1 else torch.zeros_like(m[2].X), m[2].labels)
+                   for m in mbs]
+        res = vm.run_program(ctx, prog, batches, [_shard(Wd, p, r)])
+        ctx.sync()
+        return res
+
+    outs = vpd.run_ranks(ctxs, rank)
+    assert [c.fused_c1_count for c in ctxs] == [n] * p
+    for r, res in enumerate(outs):
+        for i in range(n):
+            assert torch.equal(res.grad_x[i], outs[0].grad_x[i])
+            assert torch.allclose(res.loss[i], local.loss[i], rtol=1e-5, atol=1e-6)
+            assert torch.allclose(res.grad_x[i], local.grad_x[i], rtol=1e-4, atol=1e-6)
+        assert torch.allclose(res.grad_w[0], local.grad_w[r], rtol=1e-4, atol=1e-6)
+    _close(ctxs)
+    lctx.close()
