@@ -816,7 +816,9 @@ bool ensure_sym(vp_ctx_s* c, SymBuf& sb, size_t need) {
 // The fused path is decided from the group-wide shape (every rank takes the
 // same branch); per-rank buffer requirements are checked, not negotiated.
 bool use_fused_c1(vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* s, int n, FusedLayout& L) {
-  if (!(c->fused_c1 && c->distributed() && c->nranks > 1 && n == 1 && c->nranks <= vp::kMaxRoute &&
+  // (a forced 1-rank group takes it too: the NCCL call sites and graph
+  // capture of the fused exchange are then testable on one GPU)
+  if (!(c->fused_c1 && c->distributed() && n == 1 && c->nranks <= vp::kMaxRoute &&
         b->h % 8 == 0 && !c->sym.failed))
     return false;
   require(s->ldw % 8 == 0 && aligned16(s->W),
@@ -1181,7 +1183,7 @@ void run_program(vp_ctx_s* c, const vp::Program& prog, const vp_batch_t* batches
   // so S (alg2) / T (alg1) of several microbatches may precede their barriers
   std::vector<FusedLayout> FL;
   {
-    bool fused = dist && c->fused_c1 && c->nranks > 1 && c->nranks <= vp::kMaxRoute && !c->sym.failed;
+    bool fused = dist && c->fused_c1 && c->nranks <= vp::kMaxRoute && !c->sym.failed;
     for (int i = 0; fused && i < n; ++i) fused = batches[i].h % 8 == 0;
     if (fused) {
       require(shards[0].ldw % 8 == 0 && aligned16(shards[0].W),

@@ -324,11 +324,54 @@ def test_nccl_exchange_path_with_a_one_rank_group(ctx):
         for x, y in ((a.loss, b.loss), (a.grad_x, b.grad_x), (a.grad_w_full(), b.grad_w_full()),
                      (a.stats.m, b.stats.m), (a.stats.sum, b.stats.sum)):
             assert torch.allclose(x, y, rtol=1e-6, atol=1e-7), alg
+    # alg1 and alg2 (x2) went through the fused exchange (peer buffers mapped
+    # over the NCCL group, loss all-reduce as the barrier, copy-engine gather)
+    assert nctx.fused_c1_count == 3
     t = torch.arange(16, dtype=torch.float32, device="cuda")
     vm.allreduce_sum(nctx, t)
     nctx.sync()
     assert torch.equal(t, torch.arange(16, dtype=torch.float32, device="cuda"))
     nctx.close()
+
+
+def test_fused_exchange_in_a_cuda_graph_over_nccl():
+    # the fused exchange's NCCL call sites (peer-pointer exchange, loss
+    # all-reduce as the barrier) and copy-engine gather captured into a CUDA
+    # graph on a 1-rank NCCL group; replays on new inputs equal eager runs
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        X, W, g = oracle.random_instance(256, 128, 1024, 8)
+        _, _, batch, Wd = device_case(X, W, g)
+        shards = vm.shard_weights(Wd, 1)
+        nctx = vm.Context(0)
+        nctx.comm_init(1, 0, vm.Context.unique_id())
+        nctx.set_option("force_collectives", 1)
+        states = [vm.ShardState(nctx, 256, 128, shards[0].rows())]
+        outs = vm._alloc_outputs(nctx, batch, shards)
+        vm.run_alg2(nctx, batch, shards, states=states, outputs=outs)  # sizes workspace + peer buffers
+        nctx.sync()
+        graph = vm.capture(nctx, lambda: vm.run_alg2(nctx, batch, shards, states=states, outputs=outs))
+        ectx = vm.Context(0)
+        for seed in (9, 10):
+            X2, Wn, g2 = oracle.random_instance(256, 128, 1024, seed)
+            Xb2, _, b2, _ = device_case(X2, W, g2)
+            batch.X.copy_(b2.X)
+            batch.labels.copy_(b2.labels)
+            graph.launch()
+            nctx.sync()
+            got = [outs[0].clone(), outs[1].clone(), torch.cat(outs[2]).clone()]
+            again = vm.run_alg2(nctx, batch, shards)  # eager, same context: the same bits
+            nctx.sync()
+            assert torch.equal(got[0], again.loss) and torch.equal(got[1], again.grad_x)
+            assert torch.equal(got[2], again.grad_w_full())
+            ref = oracle.oracle_output_layer(Xb2, g2, device_case(X, W, g)[1], want_softmax=False)
+            res = {"loss": got[0].double().cpu().numpy(), "grad_x": got[1].double().cpu().numpy(),
+                   "grad_w": got[2].double().cpu().numpy()}
+            assert_parity(res, ref, f"graph replay seed {seed}")
+        assert nctx.fused_c1_count == 4  # counted on the host: sizing run, captured call, two eager checks
+        graph.close()
+        ectx.close()
+        nctx.close()
 
 
 def test_tied_embeddings_accumulate_into_one_shard_gradient(ctx):
