@@ -175,3 +175,43 @@ def test_input_backward_every_multiplicity_class(ctx, T, h):
         ctx.sync()
         ref = oracle.input_backward_f32(g.float().cpu().numpy(), tok, s.rows(), s.row_begin)
         assert np.array_equal(dE.cpu().numpy(), ref), s.index
+
+
+def test_input_peer_paths_capture_over_nccl():
+    # the peer-memory input forward and the gathered backward on a forced
+    # 1-rank NCCL group: capturable after the first (sizing) call; replays on
+    # new ids / gradients are bit-exact
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        rng = np.random.default_rng(7)
+        V, h, T = 3000, 256, 1500
+        W = torch.from_numpy(rng.standard_normal((V, h)).astype(np.float32)).to(torch.bfloat16).cuda()
+        sh = vm.shard_weights(W, 1)[0]
+        tok = torch.from_numpy(rng.integers(0, V, T).astype(np.int64)).cuda()
+        grad = torch.from_numpy(rng.standard_normal((T, h)).astype(np.float32)).to(torch.bfloat16).cuda()
+        nctx = vm.Context(0)
+        nctx.comm_init(1, 0, vm.Context.unique_id())
+        nctx.set_option("force_collectives", 1)
+        emb = torch.empty(T, h, dtype=torch.bfloat16, device="cuda")
+        dE = torch.empty(V, h, dtype=torch.float32, device="cuda")
+
+        def step():
+            vm.input_forward_gathered(nctx, tok, sh, out=emb)
+            vm.input_backward_gathered(nctx, grad, tok, sh, root=0, out=dE)
+
+        step()
+        nctx.sync()
+        graph = vm.capture(nctx, step)
+        for seed in (1, 2):
+            r2 = np.random.default_rng(seed)
+            t2 = r2.integers(0, V, T)
+            tok.copy_(torch.from_numpy(t2.astype(np.int64)))
+            grad.copy_(torch.from_numpy(r2.standard_normal((T, h)).astype(np.float32)).to(torch.bfloat16))
+            graph.launch()
+            nctx.sync()
+            assert torch.equal(emb, W[tok])
+            ref = oracle.input_backward_f32(grad.float().cpu().numpy(), t2, V, 0)
+            assert np.array_equal(dE.cpu().numpy(), ref)
+        assert nctx.peer_input_count == 4  # host calls: the sizing step and the captured step
+        graph.close()
+        nctx.close()
