@@ -86,7 +86,7 @@ class ClockSampler:
     already producing samples when the timed region begins); `with sampler:`
     marks the timed region, and only samples whose nvidia-smi timestamps fall
     inside it are summarised."""
-    Q = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+    Q = ("timestamp,clocks.sm,clocks.max.sm,power.draw.instant,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
 
@@ -134,7 +134,7 @@ class ClockSampler:
         return keep or ([near] if near else [])
 
     def summary(self):
-        sm, smax, reasons = [], None, set()
+        sm, pw, smax, reasons = [], [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for f in self._in_region():
             if len(f) < 7:
@@ -144,13 +144,17 @@ class ClockSampler:
                 smax = float(f[1])
             except ValueError:
                 continue
+            try:
+                pw.append(float(f[2]))
+            except ValueError:
+                pass
             for n, v in zip(names, f[3:7]):
                 if v.lower().startswith("active"):
                     reasons.add(n)
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": smax, "reasons": sorted(reasons), "samples": 0}
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": smax, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "power_w": statistics.median(pw) if pw else None}
 
 
 # ---------------------------------------------------------------------------
@@ -483,6 +487,9 @@ def run_ours(args):
         "e2e": e2e, "graph": graph, "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu,
         "clocks": clk.summary(), "comm": ctx.comm_backend,
     }
+    pw = line["clocks"].get("power_w")
+    if pw:  # median instantaneous board power in the timed region (the 1 kW cap sets the clock)
+        line["energy"] = {"power_w": pw, "tokens_per_joule": value / (pw * world)}
     if world > 1:
         # C1 of the output layer: the fused reduce-scatter (dX epilogue -> the
         # token rows' owners over peer memory) or the dX all-reduce
