@@ -635,3 +635,56 @@ def test_executor_fused_microbatches_of_different_lengths():
         assert torch.allclose(res.grad_w[0], local.grad_w[r], rtol=1e-4, atol=1e-6)
     _close(ctxs)
     lctx.close()
+
+
+def test_fused_exchange_soak_back_to_back_steps():
+    # many back-to-back steps on one group without host synchronisation
+    # between them (the ordering across steps is all stream-side: routed
+    # stores after the previous loss barrier, combine after the stats
+    # all-gather, pulls before the next step's writes); alternating algorithms
+    # and the input layer; every step equals its one-GPU p-shard run bitwise
+    p, h = 4, 64
+    rng = np.random.default_rng(5)
+    steps = []
+    for it in range(24):
+        T = int(rng.integers(30, 400))
+        V = 400 * p
+        X, W, g = oracle.random_instance(T, h, V, 1000 + it)
+        steps.append((["alg2", "alg1", "chunked"][it % 3], device_case(X, W, g)))
+    lctx = vm.Context(0)
+    for k, v in (("splits_dx", 1), ("splits_dw", 1)):
+        lctx.set_option(k, v)
+    want = []
+    for alg, (_, _, batch, Wd) in steps:
+        sh = vm.shard_weights(Wd, p)
+        if alg == "chunked":
+            want.append(vm.run_alg2_chunked(lctx, batch, sh, 64))
+        else:
+            want.append({"alg1": vm.run_alg1, "alg2": vm.run_alg2}[alg](lctx, batch, sh))
+    lctx.sync()
+    torch.cuda.synchronize()
+    ctxs = vpd.local_group(p)
+    for c in ctxs:
+        c.set_option("splits_dx", 1)
+        c.set_option("splits_dw", 1)
+
+    def rank(r, c):
+        outs = []
+        for alg, (_, _, batch, Wd) in steps:
+            sh = [_shard(Wd, p, r)]
+            if alg == "chunked":
+                outs.append(vm.run_alg2_chunked(c, batch, sh, 64))
+            else:
+                outs.append({"alg1": vm.run_alg1, "alg2": vm.run_alg2}[alg](c, batch, sh))
+            vm.input_forward_gathered(c, batch.labels, sh[0])  # interleave the input layer's exchanges
+        c.sync()
+        return outs
+
+    res = vpd.run_ranks(ctxs, rank)
+    for it, (alg, _) in enumerate(steps):
+        for r in range(p):
+            assert torch.equal(res[r][it].loss, want[it].loss), (it, alg, r)
+            assert torch.equal(res[r][it].grad_x, want[it].grad_x), (it, alg, r)
+        assert torch.equal(torch.cat([res[r][it].grad_w[0] for r in range(p)]), want[it].grad_w_full()), (it, alg)
+    _close(ctxs)
+    lctx.close()
