@@ -456,6 +456,8 @@ def run_ours(args):
                 "peak_source": peak_src, "flops_per_launch": flops_launch, "gemms": kern,
                 "step_frac_of_peak": (6.0 * T * h * V / (ms / 1e3) / 1e12) / (world * peak),
                 "step_frac_of_nominal_2250": (6.0 * T * h * V / (ms / 1e3) / 1e12) / (world * 2250.0)}
+    if peaks and peaks.get("bf16_tflops") and achieved:
+        roofline["frac_of_burst"] = achieved / peaks["bf16_tflops"]  # MEASURED_PEAKS bf16_tflops (burst)
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
