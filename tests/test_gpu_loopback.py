@@ -690,33 +690,39 @@ def test_fused_exchange_soak_back_to_back_steps():
     lctx.close()
 
 
-def test_fused_exchange_at_the_headline_shape():
+@pytest.mark.parametrize("pinned", [True, False])
+def test_fused_exchange_at_the_headline_shape(pinned):
     # T=8192, h=4096, V=256000 as 2 loopback ranks through the fused exchange:
-    # bitwise the one-GPU 2-shard run (random bf16 operands drawn on the device)
+    # bitwise the one-GPU 2-shard run with split-K pinned (random bf16 operands
+    # drawn on the device); with the production split-K choice (ranks sharing
+    # the GPU get half its SMs, so their splits may differ) within fp32 noise
     p, T, h, V = 2, 8192, 4096, 256000
     gen = torch.Generator(device="cuda").manual_seed(21)
     X = torch.randn(T, h, device="cuda", generator=gen).to(torch.bfloat16)
     Wd = (torch.randn(V, h, device="cuda", generator=gen) * 0.02).to(torch.bfloat16)
     lab = torch.randint(0, V, (T,), device="cuda", generator=gen)
     batch = vm.TokenBatch(X, lab)
+    opts = (("splits_dx", 1), ("splits_dw", 1)) if pinned else ()
     lctx = vm.Context(0)
-    for k, v in (("splits_dx", 1), ("splits_dw", 1)):
+    for k, v in opts:
         lctx.set_option(k, v)
     local = vm.run_alg2(lctx, batch, vm.shard_weights(Wd, p))
     lctx.sync()
     torch.cuda.synchronize()
     ctxs = vpd.local_group(p)
     for c in ctxs:
-        c.set_option("splits_dx", 1)
-        c.set_option("splits_dw", 1)
+        for k, v in opts:
+            c.set_option(k, v)
     outs = vpd.run_ranks(ctxs, lambda r, c: vm.run_alg2(c, batch, [_shard(Wd, p, r)]))
     for c in ctxs:
         c.sync()
     assert [c.fused_c1_count for c in ctxs] == [1] * p
+    same = torch.equal if pinned else (lambda a, b: torch.allclose(a, b, rtol=1e-4, atol=1e-6))
     for o in outs:
-        assert torch.equal(o.loss, local.loss) and torch.equal(o.grad_x, local.grad_x)
+        assert torch.equal(o.grad_x, outs[0].grad_x)  # every rank holds the same bits
+        assert same(o.loss, local.loss) and same(o.grad_x, local.grad_x)
     for r in range(p):
         rb, re = vpd.shard_rows(V, p, r)
-        assert torch.equal(outs[r].grad_w[0], local.grad_w_full()[rb:re])
+        assert same(outs[r].grad_w[0], local.grad_w_full()[rb:re])
     _close(ctxs)
     lctx.close()
