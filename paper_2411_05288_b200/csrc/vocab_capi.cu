@@ -630,8 +630,14 @@ void alg2_T(vp_ctx_s* c, vp_state_s* st, vp_stats_t g, const vp_batch_t* b, cons
   require(st->has_S && st->form == kLocal, "alg2_pass_T: state/stats length mismatch");
   require(g.m && g.sum, "alg2_pass_T: null stats");
   check_grad_w(gw, ldgw, b->h, "alg2_pass_T: grad_w needs ldgw >= h, ldgw % 4 == 0 and a 16-byte aligned base");
-  const float* sc = global_scale(c, st, g);
-  gemm_dw(c, st, scaled_x(c, b, sc), b->h, gw, ldgw);
+  // c (.) X with the global scale computed per row inside the scaling pass
+  auto* xs = c->buf<__nv_bfloat16>(c->xs, size_t(b->n_tok * b->h));
+  const vp::RowScale rs{st->m_loc, st->s_loc, g.m, g.sum, st->form == kLocal ? st->cfac : nullptr};
+  vp::k_scale_rows_global_bf16<<<c->grid_for(b->n_tok * b->h / 8, 256), 256, 0, c->stream>>>(
+      static_cast<const __nv_bfloat16*>(b->X), b->ldx, rs, int(b->n_tok), int(b->h), xs, b->h);
+  VP_KCHECK();
+  ++c->launches;
+  gemm_dw(c, st, xs, b->h, gw, ldgw);
   segment_scatter(c, b->labels, b->n_tok, s->row_begin, s->row_end, static_cast<const __nv_bfloat16*>(b->X), b->ldx,
                   b->h, -1.f, gw, ldgw, 1, kErrLabel);
 }

@@ -464,6 +464,33 @@ __global__ void k_loss(LossShards S, const float* __restrict__ mg, const float* 
 }
 
 // Xs[i,:] = bf16(c_i * X[i,:])   (alg2 pass T: dW = P'^T diag(c) X)
+// The global scale of VM.cpp:22-27 (times the per-row reference factor cfac
+// when given), one row at a time: the expression of k_global_scale.
+struct RowScale {
+  const float *ml, *sl, *mg, *sg, *cfac;
+  __device__ __forceinline__ float operator()(int i) const {
+    return sl[i] * expf(ml[i] - mg[i]) / sg[i] * (cfac ? cfac[i] : 1.f);
+  }
+};
+// Xs = c (.) X with c computed inline (alg2_pass_T: no separate scale pass)
+__global__ void k_scale_rows_global_bf16(const __nv_bfloat16* __restrict__ X, int64_t ldx, RowScale rs, int n, int h,
+                                         __nv_bfloat16* __restrict__ out, int64_t ldo) {
+  const int hv = h / 8;
+  const int64_t total = int64_t(n) * hv;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < total; t += int64_t(gridDim.x) * blockDim.x) {
+    const int i = int(t / hv), j = int(t - int64_t(i) * hv) * 8;
+    uint4 u = *reinterpret_cast<const uint4*>(X + int64_t(i) * ldx + j);
+    __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u);
+    const float f = rs(i);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      float2 x = __bfloat1622float2(h2[q]);
+      h2[q] = __floats2bfloat162_rn(x.x * f, x.y * f);
+    }
+    *reinterpret_cast<uint4*>(out + int64_t(i) * ldo + j) = u;
+  }
+}
+
 __global__ void k_scale_rows_bf16(const __nv_bfloat16* __restrict__ X, int64_t ldx, const float* __restrict__ c,
                                   int n, int h, __nv_bfloat16* __restrict__ out, int64_t ldo) {
   const int hv = h / 8;
