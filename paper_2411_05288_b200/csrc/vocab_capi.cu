@@ -642,8 +642,11 @@ void alg2_T(vp_ctx_s* c, vp_state_s* st, vp_stats_t g, const vp_batch_t* b, cons
                   b->h, -1.f, gw, ldgw, 1, kErrLabel);
 }
 
+// loss != nullptr (one device, no group): the per-token loss is computed by
+// the combine kernel too (what loss_of would do, one launch fewer)
 void alg2_C1(vp_ctx_s* c, const vp_state_t* states, const vp_shard_t* shards, int n, const vp_batch_t* b,
-             double fault_scale, vp_stats_t out, float* gx, int64_t ldgx, bool reduce = true) {
+             double fault_scale, vp_stats_t out, float* gx, int64_t ldgx, bool reduce = true,
+             float* loss = nullptr) {
   NvtxRange nr("vp:C1");
   require(n >= 1 && states != nullptr, "alg2_barrier_C1: no states");
   check_batch(b);
@@ -666,10 +669,12 @@ void alg2_C1(vp_ctx_s* c, const vp_state_t* states, const vp_shard_t* shards, in
     S.re[k] = shards[k].row_end;
     S.ml[k] = states[k]->m_loc;
     S.sl[k] = states[k]->s_loc;
+    S.yt[k] = states[k]->ytgt;
   }
+  require(loss == nullptr || !c->distributed(), "alg2_barrier_C1: the fused loss is for one device");
   const int64_t V = global_vocab(c, shards, n);
   vp::k_alg2_combine<<<c->grid_for(b->n_tok * b->h / 4, 256), 256, 0, c->stream>>>(
-      S, out.m, out.sum, b->labels, int(b->n_tok), int(b->h), gx, ldgx, V, c->d_err, kErrLabel);
+      S, out.m, out.sum, b->labels, int(b->n_tok), int(b->h), gx, ldgx, V, c->d_err, kErrLabel, loss);
   VP_KCHECK();
   ++c->launches;
   if (c->distributed() && reduce) {
@@ -1008,8 +1013,13 @@ void run_alg(int alg, vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* shards
   if (alg == 2) {
     for (int k = 0; k < n; ++k) alg2_S(c, b, &shards[k], states[k]);
     const bool overlap = c->distributed() && c->overlap_c1 && c->comm_stream != nullptr;
-    alg2_C1(c, states, shards, n, b, fault_scale, out, gx, ldgx, /*reduce=*/!overlap);
-    loss_of(c, states, shards, n, out, b, loss, /*reduce=*/!overlap);
+    if (!c->distributed()) {
+      require(loss != nullptr, "loss: null output");
+      alg2_C1(c, states, shards, n, b, fault_scale, out, gx, ldgx, true, loss);  // + the loss, one launch
+    } else {
+      alg2_C1(c, states, shards, n, b, fault_scale, out, gx, ldgx, /*reduce=*/!overlap);
+      loss_of(c, states, shards, n, out, b, loss, /*reduce=*/!overlap);
+    }
     const int sms = c->gemm_sms;
     if (overlap) {
       // C1's only heavy exchange overlaps pass T (T is "arbitrarily delayable")

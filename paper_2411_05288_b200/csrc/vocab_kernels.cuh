@@ -284,17 +284,27 @@ struct CombineShards {
   int64_t rb[kMaxLocalShards], re[kMaxLocalShards];
   const float* ml[kMaxLocalShards];
   const float* sl[kMaxLocalShards];
+  const float* yt[kMaxLocalShards];  // y[i, g_i] of owned labels (the fused loss)
   int p;
 };
+// loss != nullptr: also the per-token loss of VM.cpp:287-292 (k_loss's
+// expression), by the thread of column group 0 of each row (one launch fewer)
 __global__ void k_alg2_combine(CombineShards S, const float* __restrict__ mg, const float* __restrict__ sg,
                                const int64_t* __restrict__ labels, int n, int h, float* __restrict__ gx,
-                               int64_t ldgx, int64_t V, int* __restrict__ err, int err_bit) {
+                               int64_t ldgx, int64_t V, int* __restrict__ err, int err_bit,
+                               float* __restrict__ loss = nullptr) {
   const int hv = h / 4;
   const int64_t total = int64_t(n) * hv;
   for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < total; t += int64_t(gridDim.x) * blockDim.x) {
     const int i = int(t / hv), c = int(t - int64_t(i) * hv) * 4;
     const int64_t g = labels[i];
     if (c == 0 && (g < 0 || (V >= 0 && g >= V))) atomicOr(err, err_bit);  // VM.cpp:18
+    if (c == 0 && loss != nullptr) {
+      float out = 0.f;
+      for (int k = 0; k < S.p; ++k)
+        if (g >= S.rb[k] && g < S.re[k]) out = mg[i] + logf(sg[i]) - S.yt[k][i];
+      loss[i] = out;
+    }
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int k = 0; k < S.p; ++k) {
       const float sc = S.sl[k][i] * expf(S.ml[k][i] - mg[i]) / sg[i];
