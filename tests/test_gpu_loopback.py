@@ -726,3 +726,42 @@ def test_fused_exchange_at_the_headline_shape(pinned):
         assert same(outs[r].grad_w[0], local.grad_w_full()[rb:re])
     _close(ctxs)
     lctx.close()
+
+
+def test_tied_embeddings_over_a_group():
+    # tied input / output embeddings with vocabulary parallelism over p ranks
+    # (R/PAPER.md:333): the input forward pulls rows over peer memory, the
+    # output layer runs the fused exchange, and each rank's shard gradient
+    # accumulates dW_k (output) + dE_k (the gathered input backward, gradient
+    # from the root) in ONE buffer; checked against the oracle
+    p, T, h, V = 4, 160, 64, 1024
+    X, W, g = oracle.random_instance(T, h, V, 61)
+    Xb, Wb, batch, Wd = device_case(X, W, g)
+    rng = np.random.default_rng(7)
+    toks = rng.integers(0, V, T)
+    toks[:30] = toks[0]
+    tok_d = torch.from_numpy(toks).cuda()
+    grad_emb = torch.from_numpy(rng.standard_normal((T, h)).astype(np.float32)).cuda().to(torch.bfloat16)
+    torch.cuda.synchronize()
+    ctxs = vpd.local_group(p)
+
+    def rank(r, c):
+        sh = _shard(Wd, p, r)
+        emb = vm.input_forward_gathered(c, tok_d, sh)
+        gbuf = torch.empty(sh.rows(), h, dtype=torch.float32, device="cuda")
+        outs = vm._alloc_outputs(c, batch, [sh])
+        vm.run_alg2(c, batch, [sh], outputs=(outs[0], outs[1], [gbuf], outs[3]))
+        vm.input_backward_gathered(c, grad_emb if r == 0 else None, tok_d, sh, root=0, h=h, out=gbuf,
+                                   accumulate=True)
+        c.sync()
+        return emb, gbuf
+
+    res = vpd.run_ranks(ctxs, rank)
+    for emb, _ in res:
+        assert torch.equal(emb, Wd[tok_d])
+    ref = oracle.oracle_output_layer(Xb, g, Wb, want_softmax=False)
+    dE = oracle.input_backward_f32(grad_emb.float().cpu().numpy(), toks, V, 0).astype(np.float64)
+    got = torch.cat([gb for _, gb in res])[:, :h].double().cpu().numpy()
+    assert rel_l2(got, ref.grad_w + dE) <= GRAD_REL_L2
+    assert [c.fused_c1_count for c in ctxs] == [1] * p and [c.peer_input_count for c in ctxs] == [2] * p
+    _close(ctxs)
