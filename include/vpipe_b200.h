@@ -145,8 +145,9 @@ int vp_workspace_query(int64_t n_tok, int64_t h, int64_t rows, int nranks, int64
  * one-float barrier, reads every row from its owner's buffer (NVLink P2P / CUDA
  * IPC): two kernels and no host-side sizes, so the call is capturable;
  * default 1; 0 or an unmappable group = the packed broadcasts),
- * "fused_c1" (vp_run_alg2 / vp_run_alg2_chunked / vp_run_alg1 in a group of
- * nranks > 1 (alg1: the dX of pass T, then C2):
+ * "fused_c1" (vp_run_alg2 / vp_run_alg2_chunked / vp_run_alg1 / vp_program_run
+ * in a group of nranks > 1, or a 1-rank group with "force_collectives" (alg1:
+ * the dX of pass T, then C2):
  * 1 = the dX GEMM of pass S stores each A_k tile straight into the buffer of
  * the rank that owns those token rows, over peer memory (NVLink P2P or CUDA
  * IPC), the label rows follow, and at C1 each owner combines its rows from
