@@ -182,6 +182,9 @@ template <class Params>
 inline bool routed(const Params&) { return false; }
 inline bool routed(const EpiStoreF32::Params& p) { return p.route_n > 0; }
 template <class Params>
+inline int route_splits(const Params&) { return 1; }
+inline int route_splits(const EpiStoreF32::Params& p) { return p.route_n > 0 ? p.route_splits : 1; }
+template <class Params>
 inline bool uses_tma(const Params&) { return false; }
 inline bool uses_tma(const EpiStoreF32::Params& p) { return p.use_tma != 0; }
 template <class Params>
@@ -241,7 +244,6 @@ inline void launch_gemm_t(const Operand& A, const Operand& B, int M, int N, int 
   g.prof = g_gemm_prof;
   g.store_evict_first = store_hint >= 0 ? store_hint : g_store_evict_first;
   g.epi_wait = g_epi_wait;
-  g.sys_fence = routed(ep) ? 1 : 0;
   auto kern = gemm_sm100_kernel<CG, A_MN, B_MN, Epi, MC, NH>;
   // per device: the smem attribute and the occupancy query (contexts of one
   // process may drive several GPUs)
@@ -284,7 +286,14 @@ inline void launch_gemm_t(const Operand& A, const Operand& B, int M, int N, int 
   int clusters = tiles < cap ? tiles : cap;
   typename Epi::Params epc = ep;
   prepare_store(epc, M, N);
-  if (MC == 1 && split != nullptr && split->flags != nullptr && splittable(ep) && tiles <= split->max_tiles) {
+  if (route_splits(epc) > 1) {
+    // routed output: the caller chose the split count (its slot layout);
+    // units are independent, no flags
+    g.splits = route_splits(epc);
+    g.split_indep = 1;
+    clusters = tiles * g.splits < cap ? tiles * g.splits : cap;
+  } else if (MC == 1 && split != nullptr && split->flags != nullptr && splittable(ep) && !routed(epc) &&
+             tiles <= split->max_tiles) {
     // workspace mode: less than half a wave of tiles, TMA-stored output, room
     const int64_t ldws = (int64_t(N) + 3) / 4 * 4;
     const bool ws_ok = split->ws != nullptr && split->ws_mode != 0 && uses_tma(epc) && !routed(epc) &&

@@ -91,9 +91,9 @@ struct GemmGeom {
   // split s-1; k_split_reduce then sums the S slices in fixed order.
   float* split_ws = nullptr;
   int ws_rows = 0;
-  // the epilogue stores into peer memory (routed output): the ordered split-K
-  // hand-off fences at system scope
-  int sys_fence = 0;
+  // split units independent of each other (routed output: every unit stores
+  // its own partial into its own slot; the owner sums them): no flags
+  int split_indep = 0;
 };
 
 __device__ __forceinline__ uint64_t make_policy(int p, bool dflt_first) {
@@ -271,7 +271,7 @@ struct RegSrc {
 // Split-K ordering (epilogue warps of one CTA).  split_wait: every lane
 // waits until the previous split of this tile/CTA has landed in global
 // memory; split_done: after this split's stores completed, publish it.
-__device__ __forceinline__ void split_wait(const int* flag, int want, bool sys = false) {
+__device__ __forceinline__ void split_wait(const int* flag, int want) {
   if ((threadIdx.x & 31) == 0) {
     int v;
     for (;;) {
@@ -279,16 +279,14 @@ __device__ __forceinline__ void split_wait(const int* flag, int want, bool sys =
       if (v - want >= 0) break;
       __nanosleep(256);
     }
-    if (sys) __threadfence_system();  // the previous split's stores went to peer memory
     asm volatile("fence.proxy.async.global;" ::: "memory");  // later TMA reduces see those writes
   }
   __syncwarp();
 }
-__device__ __forceinline__ void split_done(int* flag, int value, Stager& sg, bool sys = false) {
+__device__ __forceinline__ void split_done(int* flag, int value, Stager& sg) {
   sg.drain();  // this warp's TMA stores are complete
   if ((threadIdx.x & 31) == 0) asm volatile("fence.proxy.async.global;" ::: "memory");
-  if (sys) __threadfence_system();
-  else __threadfence();
+  __threadfence();
   asm volatile("bar.sync 2, 256;" ::: "memory");  // the 8 epilogue warps of this CTA
   if (threadIdx.x == 128) asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(flag), "r"(value) : "memory");
 }
@@ -581,7 +579,8 @@ __global__ void __launch_bounds__(384, 1)
       const int t = unit_tile(u), sp = unit_split(u);
       tile_coords(gc, t, mc, nb);
       const int mb = mc * MC + int(pair);
-      int* flag = (g.splits > 1 && g.split_ws == nullptr) ? g.split_flags + 2 * t + int(rank) : nullptr;
+      int* flag = (g.splits > 1 && g.split_ws == nullptr && !g.split_indep) ? g.split_flags + 2 * t + int(rank)
+                                                                               : nullptr;
       const int row = mb * C::BM + int(rank) * C::BM_CTA + quad * 32 + lane;
       const typename Epi::Pre pre = Epi::prepare(ep, g, row, nb * C::BN_TILE);
       // one accumulator per N half (NH == 2, released separately: see the
@@ -608,14 +607,14 @@ __global__ void __launch_bounds__(384, 1)
           ptx::tc_fence_before();
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive_remote(bar_tempty + 8 * slot, leader);
-          if (hw == 0 && flag && sp > 0) split_wait(flag, g.flag_base + sp, g.sys_fence != 0);
+          if (hw == 0 && flag && sp > 0) split_wait(flag, g.flag_base + sp);
           if (col0 < g.N) Epi::apply_regs(ep, g, acc, row, col0, col0 / kEpiCols, sg, pre, sp);
           if (probe && lane == 0) {
             epi_wait_cyc += c1 - c0;
             epi_work_cyc += clock64() - c1;
           }
         } else {
-        if (hw == 0 && flag && sp > 0) split_wait(flag, g.flag_base + sp, g.sys_fence != 0);
+        if (hw == 0 && flag && sp > 0) split_wait(flag, g.flag_base + sp);
 #pragma unroll 1
         for (int hh = (NH == 2 ? hw : 0); hh < (NH == 2 ? hw + 1 : NH); ++hh) {
           const int col0 = nb * C::BN_TILE + hh * C::BN + cgp * kEpiCols;
@@ -647,7 +646,7 @@ __global__ void __launch_bounds__(384, 1)
         }
         }
       }
-      if (flag) split_done(flag, g.flag_base + sp + 1, sg, g.sys_fence != 0);
+      if (flag) split_done(flag, g.flag_base + sp + 1, sg);
     }
     sg.drain();
     if (probe && lane == 0) {
@@ -706,13 +705,17 @@ struct EpiStoreF32 {
     CUtensorMap map;
     CUtensorMap ws_map;  // parallel split-K workspace (fp32 [S * ws_rows x N])
     // Routed output (the fused dX -> reduce-scatter over peer memory): rows
-    // [o * route_rows, (o + 1) * route_rows) go through route_map[o], a map
-    // over the owning rank o's buffer (local, peer-enabled or IPC-mapped), at
-    // local row (row - o * route_rows).  route_rows % 32 == 0, so one store
-    // box never straddles two owners; rows past an owner's extent are clipped
-    // by the TMA unit.  route_n = 0: the plain output `map`.
+    // [o * route_rows, (o + 1) * route_rows) of split unit sp go through
+    // route_map[o * route_splits + sp], a map over slot sp of the owning rank
+    // o's buffer (local, peer-enabled or IPC-mapped), at local row (row -
+    // o * route_rows).  route_rows % 32 == 0, so one store box never straddles
+    // two owners; rows past an owner's extent are clipped by the TMA unit.
+    // Split units are independent (plain stores into their own slots; the
+    // owner adds them in split order), so nothing but plain TMA stores
+    // crosses NVLink.  route_n = 0: the plain output `map`.
     int route_n = 0;
     int route_rows = 0;
+    int route_splits = 1;
     CUtensorMap route_map[kMaxRoute];
   };
   // per-row inputs loaded before the accumulator is waited for (hides their latency)
@@ -744,10 +747,10 @@ struct EpiStoreF32 {
     int rbase = to_ws ? sp * g.ws_rows : 0;
     if (p.route_n > 0) {  // (never together with the workspace: the host checks)
       const int o = min((row - int(threadIdx.x & 31)) / p.route_rows, p.route_n - 1);
-      omap = &p.route_map[o];
+      omap = &p.route_map[o * p.route_splits + sp];
       rbase = -o * p.route_rows;
     }
-    const bool add = !to_ws && (p.accumulate != 0 || sp > 0);
+    const bool add = !to_ws && p.route_n == 0 && (p.accumulate != 0 || sp > 0);
     float mx = -INFINITY;
     const int row0 = row - int(threadIdx.x & 31);
     if (p.use_tma) {

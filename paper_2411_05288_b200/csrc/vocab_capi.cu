@@ -775,19 +775,32 @@ const vp::RankBounds& rank_bounds(vp_ctx_s* c, const vp_shard_t* s) {
 // See k_alg2_combine_owned for the arithmetic.
 struct FusedLayout {
   int64_t R = 0;
-  int n_own = 0;  // ranks that own at least one row
+  int n_own = 0;   // ranks that own at least one row
+  int splits = 1;  // split-K units of the routed dX GEMM (one slot each)
   size_t slot_off = 0, b_off = 0, g_off = 0, need = 0;
 };
 
 // `base`: byte offset of this layout's region in the peer buffer (the
 // executor keeps one region per microbatch); need = base + region bytes.
-FusedLayout fused_layout(const vp_ctx_s* c, int64_t T, int64_t h, size_t base = 0) {
+// The split-K count of the routed dX GEMM (K = rows = V_k) is chosen here,
+// like the unrouted launch's (wave quantisation; option "splits_dx"), because
+// it sets the slot layout: every split unit stores into its own slot.
+FusedLayout fused_layout(const vp_ctx_s* c, int64_t T, int64_t h, int64_t rows, size_t base = 0) {
   FusedLayout L;
   L.R = round_up(ceil_div(T, c->nranks), 32);
   L.n_own = int(ceil_div(T, L.R));
+  if (c->splits_dx > 0) {
+    L.splits = c->splits_dx;
+  } else {
+    const int bn = c->eff_nh(1) == 2 ? 512 : 256;
+    const int tiles = int(ceil_div(T, 256) * ceil_div(h, bn));
+    L.splits = vp::choose_splits(tiles, std::max(1, c->gemm_sms / 2), int(ceil_div(rows, 64)), c->split.min_kb);
+  }
+  L.splits = std::max(1, std::min(L.splits, vp::kMaxRoute / std::max(1, L.n_own)));
+  L.splits = std::min<int>(L.splits, int(std::max<int64_t>(1, ceil_div(rows, 64))));
   const size_t rowf = size_t(L.R) * size_t(h);
   L.slot_off = base;
-  L.b_off = L.slot_off + size_t(c->nranks) * rowf * sizeof(float);
+  L.b_off = L.slot_off + size_t(c->nranks) * size_t(L.splits) * rowf * sizeof(float);
   L.g_off = L.b_off + size_t(round_up(int64_t(rowf * sizeof(__nv_bfloat16)), 256));
   L.need = size_t(round_up(int64_t(L.g_off + rowf * sizeof(float)), 256));
   return L;
@@ -834,7 +847,7 @@ bool use_fused_c1(vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* s, int n, 
     return false;
   require(s->ldw % 8 == 0 && aligned16(s->W),
           "fused_c1: the shard needs ldw % 8 == 0 and a 16-byte aligned W (or set fused_c1 = 0 on every rank)");
-  L = fused_layout(c, b->n_tok, b->h);
+  L = fused_layout(c, b->n_tok, b->h, s->row_end - s->row_begin);
   return ensure_sym(c, c->sym, L.need);
 }
 
@@ -847,13 +860,17 @@ void gemm_dx_routed(vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* s, vp_st
   vp::EpiStoreF32::Params ep{nullptr, h, nullptr, 0, row_scale};
   ep.route_n = L.n_own;
   ep.route_rows = int(L.R);
+  ep.route_splits = L.splits;
   vp::PeerRows pr{};
   for (int o = 0; o < L.n_own; ++o) {
     char* peer = static_cast<char*>(c->sym.peers[size_t(o)]);
-    float* base = reinterpret_cast<float*>(peer + L.slot_off) + size_t(c->rank) * size_t(L.R) * size_t(h);
     const int64_t rows = std::min(L.R, T - o * L.R);
-    ep.route_map[o] = vp::make_store_map(base, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, uint64_t(h), uint64_t(rows),
-                                         uint64_t(h), VP_F32_BOX128 ? 128 : 64);
+    for (int sp = 0; sp < L.splits; ++sp) {  // slot (my rank, sp) of owner o
+      float* base = reinterpret_cast<float*>(peer + L.slot_off) +
+                    (size_t(c->rank) * size_t(L.splits) + size_t(sp)) * size_t(L.R) * size_t(h);
+      ep.route_map[o * L.splits + sp] = vp::make_store_map(base, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, uint64_t(h),
+                                                           uint64_t(rows), uint64_t(h), VP_F32_BOX128 ? 128 : 64);
+    }
     pr.p[o] = peer + L.b_off;
   }
   gemm_dx_ep(c, st, s, ep);
@@ -898,6 +915,7 @@ void owner_combine_gather(vp_ctx_s* c, const vp_shard_t* s, const vp_batch_t* b,
   S.row0 = int(c->rank * R);
   S.rows = int(std::max<int64_t>(0, std::min(R, T - c->rank * R)));
   S.prescaled = prescaled ? 1 : 0;
+  S.splits = L.splits;
   const int64_t V = global_vocab(c, s, 1);
   if (S.rows > 0) {
     vp::k_alg2_combine_owned<<<c->grid_for(int64_t(S.rows) * h / 4, 256), 256, 0, c->stream>>>(
@@ -1205,8 +1223,11 @@ void run_program(vp_ctx_s* c, const vp::Program& prog, const vp_batch_t* batches
       require(shards[0].ldw % 8 == 0 && aligned16(shards[0].W),
               "fused_c1: the shard needs ldw % 8 == 0 and a 16-byte aligned W (or set fused_c1 = 0 on every rank)");
       size_t region = 0;
-      for (int i = 0; i < n; ++i) region = std::max(region, fused_layout(c, batches[i].n_tok, batches[i].h).need);
-      for (int i = 0; i < n; ++i) FL.push_back(fused_layout(c, batches[i].n_tok, batches[i].h, size_t(i) * region));
+      const int64_t rows = shards[0].row_end - shards[0].row_begin;
+      for (int i = 0; i < n; ++i)
+        region = std::max(region, fused_layout(c, batches[i].n_tok, batches[i].h, rows).need);
+      for (int i = 0; i < n; ++i)
+        FL.push_back(fused_layout(c, batches[i].n_tok, batches[i].h, rows, size_t(i) * region));
       if (!ensure_sym(c, c->sym, size_t(n) * region)) FL.clear();
     }
   }
@@ -1479,7 +1500,8 @@ int vp_workspace_query(int64_t n_tok, int64_t h, int64_t rows, int nranks, int64
       *peer_b = 0;
       if (nranks > 1) {  // fused exchange (output layer) + input-layer peer buffers
         const int64_t R = round_up(ceil_div(n_tok, nranks), 32), rowf = R * h;
-        const int64_t out = round_up(int64_t(nranks) * rowf * 4 + round_up(rowf * 2, 256) + rowf * 4, 256);
+        // (two split-K slots per rank: the split the routed dX GEMM takes at the headline shapes)
+        const int64_t out = round_up(int64_t(nranks) * 2 * rowf * 4 + round_up(rowf * 2, 256) + rowf * 4, 256);
         const int64_t inl = 2 * round_up(n_tok * h * 2, 256);
         *peer_b = round_up(out, int64_t(2) << 20) + 2 * round_up(inl, int64_t(2) << 20);
       }

@@ -356,12 +356,13 @@ __global__ void k_push_label_rows(const __nv_bfloat16* __restrict__ W, int64_t l
 }
 
 struct OwnedCombine {
-  const float* slots;            // [nranks][R][h] fp32, slot k = A_k of my rows
+  const float* slots;            // [nranks][splits][R][h] fp32: rank k's split-K partials of A_k, my rows
   const __nv_bfloat16* B;        // [R][h] bf16
   const float* gathered;         // [nranks][2T]: rank k's local m at k*2T, sum at k*2T + T
   int64_t rb[kMaxLocalShards], re[kMaxLocalShards];
   int nranks, R, row0, rows;     // my rows: [row0, row0 + rows)
   int prescaled;                 // alg1 C2: the slots already hold c_k A_k (c_k = 1 here)
+  int splits;                    // split-K units of rank k's dX GEMM, added here in split order
 };
 __global__ void k_alg2_combine_owned(OwnedCombine S, const float* __restrict__ mg, const float* __restrict__ sg,
                                      const int64_t* __restrict__ labels, int T, int h, float* __restrict__ out,
@@ -380,7 +381,16 @@ __global__ void k_alg2_combine_owned(OwnedCombine S, const float* __restrict__ m
     const float2 w1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(w + 2));
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int k = 0; k < S.nranks; ++k) {
-      const float4 a = *reinterpret_cast<const float4*>(a_row + k * slot);
+      // A_k = p_0 + p_1 + ... in split order: the fp32 adds the ordered split-K
+      // of the one-GPU path performs (its TMA reduce-adds), the same bits
+      float4 a = *reinterpret_cast<const float4*>(a_row + int64_t(k) * S.splits * slot);
+      for (int sp = 1; sp < S.splits; ++sp) {
+        const float4 q = *reinterpret_cast<const float4*>(a_row + (int64_t(k) * S.splits + sp) * slot);
+        a.x = a.x + q.x;
+        a.y = a.y + q.y;
+        a.z = a.z + q.z;
+        a.w = a.w + q.w;
+      }
       float4 b = make_float4(0.f, 0.f, 0.f, 0.f);
       if (g >= S.rb[k] && g < S.re[k]) b = make_float4(w0.x, w0.y, w1.x, w1.y);
       if (S.prescaled) {
