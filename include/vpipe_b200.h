@@ -149,8 +149,8 @@ int vp_workspace_query(int64_t n_tok, int64_t h, int64_t rows, int nranks, int64
  * in a group of nranks > 1, or a 1-rank group with "force_collectives" (alg1:
  * the dX of pass T, then C2):
  * 1 = the dX GEMM of pass S stores each A_k tile straight into the buffer of
- * the rank that owns those token rows, over peer memory (NVLink P2P or CUDA
- * IPC), the label rows follow, and at C1 each owner combines its rows from
+ * the rank that owns those token rows from its epilogue, over peer memory
+ * (NVLink P2P or CUDA IPC), the label rows follow, and at C1 each owner combines its rows from
  * local memory and every rank pulls the owners' rows into grad_x with its copy
  * engines — a reduce-scatter fused into the GEMM epilogue and an SM-free
  * all-gather instead of an all-reduce of [n_tok x h] fp32 partials;

@@ -78,8 +78,8 @@ inline bool tma_store_ok(const void* p, int64_t ld, int esize) {
   return g_tma_store && (reinterpret_cast<uintptr_t>(p) & 15) == 0 && (ld * esize) % 16 == 0;
 }
 inline void prepare_store(EpiStoreF32::Params& ep, int M, int N) {
-  if (ep.route_n > 0) {  // routed: the caller built route_map[] (make_store_map per owner)
-    ep.use_tma = 1;
+  if (ep.route_n > 0) {  // routed: per-thread stores to the owners' slots (route_out)
+    ep.use_tma = 0;
     return;
   }
   ep.use_tma = tma_store_ok(ep.out, ep.ldo, 4);

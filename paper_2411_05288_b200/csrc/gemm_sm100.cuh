@@ -705,18 +705,18 @@ struct EpiStoreF32 {
     CUtensorMap map;
     CUtensorMap ws_map;  // parallel split-K workspace (fp32 [S * ws_rows x N])
     // Routed output (the fused dX -> reduce-scatter over peer memory): rows
-    // [o * route_rows, (o + 1) * route_rows) of split unit sp go through
-    // route_map[o * route_splits + sp], a map over slot sp of the owning rank
-    // o's buffer (local, peer-enabled or IPC-mapped), at local row (row -
-    // o * route_rows).  route_rows % 32 == 0, so one store box never straddles
-    // two owners; rows past an owner's extent are clipped by the TMA unit.
-    // Split units are independent (plain stores into their own slots; the
-    // owner adds them in split order), so nothing but plain TMA stores
-    // crosses NVLink.  route_n = 0: the plain output `map`.
+    // [o * route_rows, (o + 1) * route_rows) of split unit sp are stored to
+    // route_out[o * route_splits + sp], slot sp of the owning rank o's buffer
+    // (local, peer-enabled or IPC-mapped; row stride ldo), at local row
+    // (row - o * route_rows), by the per-thread 16-byte stores (use_tma = 0):
+    // plain st.global over NVLink, the most basic peer access.  Long-K GEMMs
+    // (dX: K = V_k) spend a negligible share of their time in the epilogue.
+    // Split units are independent (each into its own slot; the owner adds
+    // them in split order).  route_n = 0: the plain output.
     int route_n = 0;
     int route_rows = 0;
     int route_splits = 1;
-    CUtensorMap route_map[kMaxRoute];
+    float* route_out[kMaxRoute];
   };
   // per-row inputs loaded before the accumulator is waited for (hides their latency)
   struct Pre {
@@ -744,11 +744,13 @@ struct EpiStoreF32 {
     // slice (use_tma is guaranteed by the host); else ordered accumulation
     const bool to_ws = g.split_ws != nullptr;
     const CUtensorMap* omap = to_ws ? &p.ws_map : &p.map;
-    int rbase = to_ws ? sp * g.ws_rows : 0;
-    if (p.route_n > 0) {  // (never together with the workspace: the host checks)
+    const int rbase = to_ws ? sp * g.ws_rows : 0;
+    float* obase = p.out;  // direct stores: base and row of this thread's output row
+    int orow = row;
+    if (p.route_n > 0) {  // (direct stores only, never the workspace: the host checks)
       const int o = min((row - int(threadIdx.x & 31)) / p.route_rows, p.route_n - 1);
-      omap = &p.route_map[o * p.route_splits + sp];
-      rbase = -o * p.route_rows;
+      obase = p.route_out[o * p.route_splits + sp];
+      orow = row - o * p.route_rows;
     }
     const bool add = !to_ws && p.route_n == 0 && (p.accumulate != 0 || sp > 0);
     float mx = -INFINITY;
@@ -803,8 +805,8 @@ struct EpiStoreF32 {
 #endif
       });
     } else {
-      float* dst = p.out + int64_t(row) * p.ldo + col0;
-      const bool vec = ((p.ldo & 3) == 0) && ((reinterpret_cast<uintptr_t>(p.out) & 15) == 0);
+      float* dst = obase + int64_t(orow) * p.ldo + col0;
+      const bool vec = ((p.ldo & 3) == 0) && ((reinterpret_cast<uintptr_t>(obase) & 15) == 0);
       src(nch, [&](uint32_t (&r)[32], int c) {
         const int nv = nvalid - c * 32;
         if (p.row_scale) {

@@ -865,12 +865,10 @@ void gemm_dx_routed(vp_ctx_s* c, const vp_batch_t* b, const vp_shard_t* s, vp_st
   for (int o = 0; o < L.n_own; ++o) {
     char* peer = static_cast<char*>(c->sym.peers[size_t(o)]);
     const int64_t rows = std::min(L.R, T - o * L.R);
-    for (int sp = 0; sp < L.splits; ++sp) {  // slot (my rank, sp) of owner o
-      float* base = reinterpret_cast<float*>(peer + L.slot_off) +
-                    (size_t(c->rank) * size_t(L.splits) + size_t(sp)) * size_t(L.R) * size_t(h);
-      ep.route_map[o * L.splits + sp] = vp::make_store_map(base, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, uint64_t(h),
-                                                           uint64_t(rows), uint64_t(h), VP_F32_BOX128 ? 128 : 64);
-    }
+    (void)rows;  // (rows past T are masked by the epilogue: the last owner's slot has R rows)
+    for (int sp = 0; sp < L.splits; ++sp)  // slot (my rank, sp) of owner o
+      ep.route_out[o * L.splits + sp] = reinterpret_cast<float*>(peer + L.slot_off) +
+                                        (size_t(c->rank) * size_t(L.splits) + size_t(sp)) * size_t(L.R) * size_t(h);
     pr.p[o] = peer + L.b_off;
   }
   gemm_dx_ep(c, st, s, ep);
